@@ -1,0 +1,197 @@
+/*
+ * wsvd_b200.h -- C ABI of the B200-native WSVD decode path.
+ *
+ * This is the drop-in boundary for the reference's decode operator API
+ * (/root/reference/proj/include/wsvd/decode.hpp, namespace wsvd::decode).
+ * Everything below is extern "C", takes plain pointers and sizes, and never
+ * exposes CUDA or torch types (streams are passed as `void*` holding a
+ * cudaStream_t; NULL = the legacy default stream).  The C++ host API
+ * (include/wsvd/decode.hpp in this repo) and the Python package are built on
+ * these entry points; INTEGRATION.md shows the ctypes / C++ bindings.
+ *
+ * Ownership: the library owns all device memory behind a handle; tensors
+ * passed as `const float* x` etc. are DEVICE pointers unless the name ends in
+ * `_host`.  Every call returns WSVD_OK or a negative status; the message of
+ * the last failure on the calling thread is returned by wsvd_last_error().
+ * The status codes mirror the reference exception hierarchy
+ * (include/wsvd/errors.hpp:9-31) and its CLI exit codes
+ * (tools/wsvd_main.cpp:632-653).
+ *
+ * There is no CPU fallback: on a machine without an sm_100 device every
+ * compute entry point fails with WSVD_ECUDA.
+ */
+#ifndef WSVD_B200_H
+#define WSVD_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WSVD_ABI_VERSION 1
+
+/* status codes (errors.hpp:9-31) */
+#define WSVD_OK 0
+#define WSVD_ESHAPE (-1)   /* ShapeError: empty cache, head-count / width mismatch */
+#define WSVD_ECONFIG (-2)  /* ConfigError: tile 0, unknown dtype, bad option */
+#define WSVD_ENUMERIC (-3) /* NumericError: non-finite input, counter mismatch */
+#define WSVD_ECUDA (-4)    /* CUDA runtime / launch failure, no device */
+#define WSVD_EIO (-5)      /* IoError */
+#define WSVD_ENCCL (-6)    /* NCCL unavailable or failed */
+
+/* storage formats */
+typedef enum {
+    WSVD_F32 = 0,  /* fp32 storage, fp32 math (config 1) */
+    WSVD_BF16 = 1, /* bf16 storage, fp32 accumulate (config 2) */
+    WSVD_I8 = 2,   /* int8 values + scales, int32-exact accumulate (W8A8, INT8 cache) */
+    WSVD_I4 = 3    /* int4 values packed two per byte + scales (W4A8 weights) */
+} wsvd_dtype;
+
+/* roles of a factored head (factorize.hpp:15 Role::Q/K/V) */
+typedef enum { WSVD_ROLE_Q = 0, WSVD_ROLE_K = 1, WSVD_ROLE_V = 2 } wsvd_role;
+
+/* traffic streams, decode.hpp:16-24 order; counters are [loads(7) | stores(7) | flops(7)] */
+typedef enum {
+    WSVD_STREAM_LATENT_K = 0,
+    WSVD_STREAM_LATENT_V,
+    WSVD_STREAM_FULL_K,
+    WSVD_STREAM_FULL_V,
+    WSVD_STREAM_WEIGHTS_B,
+    WSVD_STREAM_QUERY,
+    WSVD_STREAM_OUTPUT,
+    WSVD_STREAM_COUNT
+} wsvd_stream;
+
+typedef struct wsvd_layer_s* wsvd_layer_t; /* device factors of one layer (or head shard) */
+typedef struct wsvd_cache_s* wsvd_cache_t; /* device latent cache of `batch` sequences */
+typedef struct wsvd_comm_s* wsvd_comm_t;   /* NCCL communicator for the O-proj all-reduce */
+
+/* Geometry of a layer object; replaces decode::LayerFactors' embed_dim /
+ * head_dim / heads.size() (decode.hpp:76-79).  A head-sharded rank holds
+ * heads [head_offset, head_offset + n_heads) of the full layer. */
+typedef struct {
+    int32_t embed_dim;    /* E */
+    int32_t head_dim;     /* H */
+    int32_t n_heads;      /* heads held by this object */
+    int32_t head_offset;  /* first global head (0 when unsharded) */
+    int32_t weight_dtype; /* wsvd_dtype of A and B factors */
+    int32_t act_rotation; /* I8/I4 only: 1 = activations are rotated by S1 = Hadamard
+                             (linalg.cpp:219-243; block H_128 when E is not a power of 2)
+                             before per-token quantisation (quant.cpp:131-150) */
+    int32_t device;       /* CUDA device ordinal */
+} wsvd_layer_desc;
+
+const char* wsvd_last_error(void);
+int wsvd_abi_version(void);
+/* number of visible sm_100 devices (0 on a machine without one) */
+int wsvd_device_count(int32_t* n);
+
+/* ---------------------------------------------------------------- layer --
+ * ranks: [n_heads][3] true ranks (q, k, v) per head, as in
+ * factorize::HeadFactors::rank (factorize.hpp:20-27).  Ranks may differ per
+ * head and role; the device zero-pads every head to one common width, which
+ * leaves results unchanged (SURVEY.md section 8(b) "Ragged ranks"). */
+int wsvd_layer_create(const wsvd_layer_desc* desc, const int32_t* ranks, wsvd_layer_t* out);
+int wsvd_layer_destroy(wsvd_layer_t layer);
+/* padded latent width used on the device */
+int wsvd_layer_rank_pad(wsvd_layer_t layer, int32_t* rpad);
+
+/* Upload one head's factors given in the reference HeadFactors layout:
+ * a row-major E x rank, b row-major rank x H, fp64 (factorize.hpp:20-27).
+ * F32 / BF16 layers round them (double -> float -> bf16, RNE).  I8 / I4
+ * layers quantise them on the host with the reference weight quantiser
+ * (quant.cpp:99-119, per-column scales, clip-grid search), after rotating a
+ * by S1 when act_rotation is set (insert_rotations, quant.cpp:182-189). */
+int wsvd_layer_set_head(wsvd_layer_t layer, int32_t head, int32_t role, const double* a,
+                        const double* b);
+/* Upload already-quantised factors (quant::QuantizedFactors, quant.hpp:98-107;
+ * checkpoint files .q.a.i8 / .q.a.scale.wsvd, checkpoint.cpp:220-244):
+ * a_q row-major E x rank int8 (I4: values in [-7, 7]), a_scales[rank];
+ * b_q row-major rank x H, b_scales[H].  The factors must already carry the
+ * rotations (S1 a S2^T, S2 b). */
+int wsvd_layer_set_head_quantized(wsvd_layer_t layer, int32_t head, int32_t role,
+                                  const int8_t* a_q, const double* a_scales, const int8_t* b_q,
+                                  const double* b_scales);
+/* O-projection rows of this shard (pipeline.cpp:329 `heads_row * W_o`):
+ * w_o_rows is row-major (n_heads * H) x e_out fp64, the rows of W_o that
+ * multiply this shard's heads.  dtype F32 or BF16. */
+int wsvd_layer_set_oproj(wsvd_layer_t layer, const double* w_o_rows, int32_t e_out,
+                         int32_t dtype);
+
+/* ---------------------------------------------------------------- cache --
+ * decode::LatentCache (decode.hpp:83-96) for `batch` sequences that advance
+ * together; capacity is the maximum length (preallocated, no regrowth).
+ * cache_dtype F32 / BF16 / I8 (I8 rows carry one fp16 scale per
+ * (token, head, K|V), the quantize_activation rule). */
+int wsvd_cache_create(wsvd_layer_t layer, int32_t batch, int32_t capacity, int32_t cache_dtype,
+                      wsvd_cache_t* out);
+int wsvd_cache_destroy(wsvd_cache_t cache);
+/* empties the cache (length 0) */
+int wsvd_cache_reset(wsvd_cache_t cache);
+/* decode with another factor set of identical geometry (the reference passes
+ * the LayerFactors to every call, decode.hpp:100-111); WSVD_ESHAPE when the
+ * head count, padded rank, E or H differ (decode.cpp:159-162). */
+int wsvd_cache_bind_layer(wsvd_cache_t cache, wsvd_layer_t layer);
+int wsvd_cache_length(wsvd_cache_t cache, int32_t* len);
+/* LatentCache::push + bump_length for every sequence and head at once:
+ * ck / cv host fp64 [batch][n_heads][rpad] (entries beyond a head's rank are
+ * ignored and stored as 0). */
+int wsvd_cache_push_host(wsvd_cache_t cache, const double* ck, const double* cv);
+/* latent_k(h) / latent_v(h) of sequence b, dequantised to fp64:
+ * ck, cv host [len][rpad]. */
+int wsvd_cache_read_host(wsvd_cache_t cache, int32_t b, int32_t head, double* ck, double* cv);
+/* raw device rows of sequence b, head h: rows [len][row_bytes] and (I8 only)
+ * fp16 scale pairs [len][2]; for bit-exact checks. */
+int wsvd_cache_row_bytes(wsvd_cache_t cache, int32_t* row_bytes);
+int wsvd_cache_read_raw(wsvd_cache_t cache, int32_t b, int32_t head, void* rows_host,
+                        uint16_t* scales_host);
+
+/* ------------------------------------------------------------ operators --
+ * append_token (decode.cpp:127-153), batched over the cache's sequences:
+ * x [batch][E] fp32, q_out [batch][n_heads][H] fp32 (may be NULL).  Writes
+ * the new latent rows at position length() and increments the length. */
+int wsvd_append_token(wsvd_cache_t cache, const float* x, float* q_out, void* stream);
+/* Appends T tokens per sequence at once (prefill): x [batch][T][E] fp32. */
+int wsvd_prefill(wsvd_cache_t cache, const float* x, int32_t T, void* stream);
+/* fused_decode_step (decode.cpp:155-206), batched: q [batch][n_heads][H] fp32,
+ * out [batch][n_heads][H] fp32.  tile_len mirrors TileConfig::tile_len
+ * (decode.hpp:51-53): 0 is rejected (WSVD_ECONFIG); any other value gives
+ * the same result up to reassociation, as in the reference. */
+int wsvd_fused_decode_step(wsvd_cache_t cache, const float* q, int32_t tile_len, float* out,
+                           void* stream);
+/* One attention-layer decode step for every sequence (pipeline.cpp:320-329):
+ * append x, attend with that token's own query, O-project this shard's
+ * heads.  y [batch][e_out] fp32 = this shard's partial sum (complete when
+ * unsharded).  attn_out [batch][n_heads][H] may be NULL. */
+int wsvd_layer_step(wsvd_cache_t cache, const float* x, float* attn_out, float* y, void* stream);
+/* Same, through host buffers: copies x_host [batch][E] in, y_host
+ * [batch][e_out] out (pinned or pageable), synchronising the stream. */
+int wsvd_layer_step_host(wsvd_cache_t cache, const float* x_host, float* y_host, void* stream);
+/* Capture wsvd_layer_step into a CUDA graph bound to (x, y, stream); later
+ * calls with the same arguments replay it (1 launch instead of ~5). */
+int wsvd_layer_step_graph(wsvd_cache_t cache, const float* x, float* y, void* stream);
+
+/* ----------------------------------------------------- traffic counters --
+ * Closed-form TrafficCounter increments (decode.cpp:132-149, 176-203;
+ * test_decode.cpp:229-292) for one call on this cache, ADDED to counter21
+ * (= [loads(7) | stores(7) | flops(7)] per stream, times batch). */
+int wsvd_traffic_append(wsvd_cache_t cache, uint64_t* counter21);
+int wsvd_traffic_fused(wsvd_cache_t cache, int32_t tile_len, uint64_t* counter21);
+
+/* ------------------------------------------------------ multi-GPU (NCCL) --
+ * Head-sharded layers: each rank holds n_heads/G
+ * heads and the matching W_o rows; after wsvd_layer_step the partial y is
+ * summed across ranks by one ncclAllReduce.  NCCL is loaded at run time
+ * (dlopen libnccl.so.2); WSVD_ENCCL when absent. */
+int wsvd_nccl_unique_id(uint8_t id[128]);
+int wsvd_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device,
+                     wsvd_comm_t* out);
+int wsvd_comm_destroy(wsvd_comm_t comm);
+int wsvd_allreduce_sum_f32(wsvd_comm_t comm, float* buf, int64_t count, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* WSVD_B200_H */

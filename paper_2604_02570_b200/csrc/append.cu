@@ -1,0 +1,232 @@
+// append.cu -- token-side kernels of the decode step.
+//
+//   act_quant        W8A8 / W4A8 activation path (SURVEY.md Appendix A steps
+//                    1-2): x_hat = x . S1^T by an in-place fp32 FWHT, then the
+//                    per-token quantiser of quant.cpp:131-150 with the same
+//                    fp32 operation order as the oracle (bit-exact).
+//   append_epilogue  finishes append_token (decode.cpp:127-153): sums the
+//                    projection's K-split partials, dequantises (int modes),
+//                    writes the K/V latent rows at the cache tail (bf16 / f32 /
+//                    int8 + fp16 row scale), up-projects the query latent
+//                    q_h = c_Q . B_Q and absorbs it into the key side,
+//                    qt = log2(e)/sqrt(H) * q_h . B_K^T, for the attention kernel.
+//   absorb_query     qt from a caller-supplied q (fused_decode_step's input).
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace wsvd_dev;
+
+namespace wsvd_k {
+
+namespace {
+
+// ----------------------------------------------------------- act quant --
+constexpr int kAqThreads = 256;
+
+__global__ void __launch_bounds__(kAqThreads) act_quant_kernel(const float* __restrict__ x, int E,
+                                                               int Kp, int rot, int rot_blk,
+                                                               float rot_scale,
+                                                               int8_t* __restrict__ xq,
+                                                               float* __restrict__ sx) {
+    extern __shared__ float v[];  // [E]
+    __shared__ float wmax[kAqThreads / 32];
+    const int m = blockIdx.x;
+    const float* xm = x + static_cast<size_t>(m) * E;
+    for (int i = threadIdx.x; i < E; i += kAqThreads) v[i] = xm[i];
+    if (rot) {
+        // stages len = 1, 2, 4, ... < rot_blk; pair p -> (lo, lo + len)
+        for (int len = 1; len < rot_blk; len <<= 1) {
+            __syncthreads();
+            for (int p = threadIdx.x; p < E / 2; p += kAqThreads) {
+                const int lo = (p / len) * (2 * len) + (p % len);
+                const float a = v[lo], b = v[lo + len];
+                v[lo] = __fadd_rn(a, b);
+                v[lo + len] = __fsub_rn(a, b);
+            }
+        }
+        __syncthreads();
+        for (int i = threadIdx.x; i < E; i += kAqThreads) v[i] = __fmul_rn(v[i], rot_scale);
+    }
+    __syncthreads();
+    float m_abs = 0.f;
+    for (int i = threadIdx.x; i < E; i += kAqThreads) m_abs = fmaxf(m_abs, fabsf(v[i]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m_abs = fmaxf(m_abs, __shfl_xor_sync(0xffffffffu, m_abs, o));
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = m_abs;
+    __syncthreads();
+    m_abs = 0.f;
+#pragma unroll
+    for (int w = 0; w < kAqThreads / 32; ++w) m_abs = fmaxf(m_abs, wmax[w]);
+    const float s = (m_abs == 0.f) ? 1.f : __fdiv_rn(m_abs, 127.f);
+    int8_t* q = xq + static_cast<size_t>(m) * Kp;
+    for (int i = threadIdx.x; i < Kp; i += kAqThreads) {
+        float r = 0.f;
+        if (i < E) r = fminf(fmaxf(roundf(__fdiv_rn(v[i], s)), -127.f), 127.f);
+        q[i] = static_cast<int8_t>(r);
+    }
+    if (threadIdx.x == 0) sx[m] = s;
+}
+
+// ------------------------------------------------------ factor access --
+WSVD_DEV float bload(const void* b, int bdtype, size_t idx) {
+    if (bdtype == F32) return reinterpret_cast<const float*>(b)[idx];
+    if (bdtype == BF16) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(b)[idx]);
+    return static_cast<float>(reinterpret_cast<const int8_t*>(b)[idx]);
+}
+
+// qt[i] = scale * sum_j q[j] * B_K[h][i][j]   (one warp per i)
+WSVD_DEV void absorb(const float* q_s, int R, int H, const void* bk, const float* bk_scale,
+                     int bdtype, int h, float scale, float* qt_out) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    const size_t base = static_cast<size_t>(h) * R * H;
+    for (int i = warp; i < R; i += nw) {
+        float acc = 0.f;
+        for (int j = lane; j < H; j += 32) {
+            float b = bload(bk, bdtype, base + static_cast<size_t>(i) * H + j);
+            if (bdtype == I8) b *= bk_scale[h * H + j];
+            acc = fmaf(q_s[j], b, acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) qt_out[i] = acc * scale;
+    }
+}
+
+// ----------------------------------------------------- append epilogue --
+constexpr int kEpThreads = 128;
+
+__global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const AppendArgs a) {
+    extern __shared__ float sm[];
+    float* c = sm;                 // [3][R] latents q, k, v
+    float* qh = sm + 3 * a.R;      // [H]
+    const int h = blockIdx.x, m = blockIdx.y;
+    const int b = m % a.B, tpos = m / a.B;  // rows are token-major: m = tpos * B + b
+    const int R = a.R, H = a.H;
+    const int pos = *a.d_len + tpos;
+
+    // ---- latents: fixed-order sum of the K-split partials (+ dequant)
+    const int nrow0 = h * 3 * R;
+    for (int i = threadIdx.x; i < 3 * R; i += kEpThreads) {
+        const size_t o = static_cast<size_t>(m) * a.Nrows + nrow0 + i;
+        const size_t stride = static_cast<size_t>(a.M) * a.Nrows;
+        float val;
+        if (a.wdtype == I8 || a.wdtype == I4) {
+            int acc = 0;
+            const int* P = reinterpret_cast<const int*>(a.P);
+            for (int s = 0; s < a.splits; ++s) acc += P[s * stride + o];
+            val = __fmul_rn(__fmul_rn(static_cast<float>(acc), a.sx[m]), a.a_scale[nrow0 + i]);
+        } else {
+            float acc = 0.f;
+            const float* P = reinterpret_cast<const float*>(a.P);
+            for (int s = 0; s < a.splits; ++s) acc += P[s * stride + o];
+            val = acc;
+        }
+        c[i] = val;
+    }
+    __syncthreads();
+
+    // ---- cache append: row [C_K | C_V] at position pos
+    const size_t bh = static_cast<size_t>(b) * a.nh + h;
+    uint8_t* row = a.cache + (bh * a.cap + pos) * a.row_bytes;
+    if (a.cdtype == I8) {
+        // per (token, head, role) scale: f16(max|c| / 127), 1 when it is 0
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        if (warp < 2) {
+            const float* src = c + (1 + warp) * R;
+            float mx = 0.f;
+            for (int i = lane; i < R; i += 32) mx = fmaxf(mx, fabsf(src[i]));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            __half hs = __float2half_rn(__fdiv_rn(mx, 127.f));
+            float s = __half2float(hs);
+            if (s == 0.f) {
+                hs = __float2half_rn(1.f);
+                s = 1.f;
+            }
+            int8_t* dst = reinterpret_cast<int8_t*>(row) + warp * R;
+            for (int i = lane; i < R; i += 32)
+                dst[i] = static_cast<int8_t>(fminf(fmaxf(roundf(__fdiv_rn(src[i], s)), -127.f), 127.f));
+            if (lane == 0) reinterpret_cast<__half*>(a.cscale + bh * a.cap + pos)[warp] = hs;
+        }
+    } else if (a.cdtype == BF16) {
+        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(row);
+        for (int i = threadIdx.x; i < 2 * R; i += kEpThreads) dst[i] = __float2bfloat16_rn(c[R + i]);
+    } else {
+        float* dst = reinterpret_cast<float*>(row);
+        for (int i = threadIdx.x; i < 2 * R; i += kEpThreads) dst[i] = c[R + i];
+    }
+
+    // ---- query: q_h = c_Q . B_Q (decode.cpp:140), then the absorbed key side
+    if (a.q_out != nullptr || a.qt != nullptr) {
+        const size_t bq0 = static_cast<size_t>(h) * R * H;
+        for (int j = threadIdx.x; j < H; j += kEpThreads) {
+            float acc = 0.f;
+            for (int i = 0; i < R; ++i) acc = fmaf(c[i], bload(a.bq, a.bdtype, bq0 + static_cast<size_t>(i) * H + j), acc);
+            if (a.bdtype == I8) acc *= a.bq_scale[h * H + j];
+            qh[j] = acc;
+            if (a.q_out) a.q_out[(static_cast<size_t>(m) * a.nh + h) * H + j] = acc;
+        }
+        __syncthreads();
+        if (a.qt) absorb(qh, R, H, a.bk, a.bk_scale, a.bdtype, h, a.qt_scale,
+                         a.qt + (static_cast<size_t>(m) * a.nh + h) * R);
+    }
+
+    // ---- commit: the last CTA advances the length by T
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const int total = gridDim.x * gridDim.y;
+        if (atomicAdd(a.done, 1) == total - 1) {
+            *a.d_len += a.T;
+            *a.done = 0;
+            __threadfence();
+        }
+    }
+}
+
+__global__ void __launch_bounds__(kEpThreads) absorb_query_kernel(const float* __restrict__ q, int nh,
+                                                                  int R, int H, const void* bk,
+                                                                  const float* bk_scale, int bdtype,
+                                                                  float scale, float* qt) {
+    extern __shared__ float qs[];
+    const int h = blockIdx.x, b = blockIdx.y;
+    const size_t o = (static_cast<size_t>(b) * nh + h);
+    for (int j = threadIdx.x; j < H; j += kEpThreads) qs[j] = q[o * H + j];
+    __syncthreads();
+    absorb(qs, R, H, bk, bk_scale, bdtype, h, scale, qt + o * R);
+}
+
+}  // namespace
+
+cudaError_t launch_act_quant(const float* x, int M, int E, int Kp, int rot, int rot_blk,
+                             float rot_scale, int8_t* xq, float* sx, cudaStream_t s) {
+    const int smem = E * 4;
+    static int attr_smem = 0;
+    if (smem > attr_smem) {
+        cudaError_t e = cudaFuncSetAttribute(act_quant_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_smem = smem;
+    }
+    act_quant_kernel<<<M, kAqThreads, smem, s>>>(x, E, Kp, rot, rot_blk, rot_scale, xq, sx);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_append_epilogue(const AppendArgs& a, cudaStream_t s) {
+    const int smem = (3 * a.R + a.H) * 4;
+    dim3 grid(a.nh, a.M);
+    append_epilogue_kernel<<<grid, kEpThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_absorb_query(const float* q, int B, int nh, int R, int H, const void* bk,
+                                const float* bk_scale, int bdtype, float qt_scale, float* qt,
+                                cudaStream_t s) {
+    dim3 grid(nh, B);
+    absorb_query_kernel<<<grid, kEpThreads, H * 4, s>>>(q, nh, R, H, bk, bk_scale, bdtype, qt_scale, qt);
+    return cudaGetLastError();
+}
+
+}  // namespace wsvd_k

@@ -1,0 +1,979 @@
+// capi.cu -- the extern "C" boundary (include/wsvd_b200.h): device-resident
+// layers and latent caches, operator launches, CUDA-graph replay, NCCL.
+//
+// Host-side responsibilities that the reference keeps inside its operators:
+//   * shape / config validation with the reference's error classes
+//     (decode.cpp:117-123, 129-131, 158-163, 112-115 -> WSVD_ESHAPE/ECONFIG);
+//   * the TrafficCounter closed forms (decode.cpp:132-149, 176-203);
+//   * factor preparation: rounding to bf16/fp32, or the reference weight
+//     quantiser (quant.cpp:99-119) after the S1 rotation (quant.cpp:182-189).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/wsvd_b200.h"
+#include "kernels.h"
+
+using namespace wsvd_k;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return set_err(WSVD_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t n = 0;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    cudaError_t alloc(size_t bytes) {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = bytes;
+        if (bytes == 0) return cudaSuccess;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+        return e;
+    }
+    template <typename T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+uint16_t f32_to_bf16_bits(float v) {
+    uint32_t u;
+    std::memcpy(&u, &v, 4);
+    if ((u & 0x7fffffffu) > 0x7f800000u) return static_cast<uint16_t>((u >> 16) | 0x40);
+    u += 0x7fffu + ((u >> 16) & 1u);
+    return static_cast<uint16_t>(u >> 16);
+}
+
+// Reference weight quantiser (quant.cpp:40-119): per-column symmetric RTN,
+// clip ratio from the grid 0.50..1.00 (first minimum wins), llround, clamp
+// to +-qmax, zero columns get scale 1.  w is row-major rows x cols.
+double quantize_weight_ref(const std::vector<double>& w, size_t rows, size_t cols, int bits,
+                           std::vector<int8_t>& q, std::vector<double>& scales) {
+    const long long lim = (1LL << (bits - 1)) - 1;
+    const double qd = static_cast<double>(lim);
+    std::vector<double> maxabs(cols, 0.0), s(cols);
+    for (size_t i = 0; i < rows; ++i)
+        for (size_t j = 0; j < cols; ++j) maxabs[j] = std::max(maxabs[j], std::abs(w[i * cols + j]));
+    double best_clip = 0.5, best_err = -1.0;
+    for (int g = 10; g <= 20; ++g) {
+        const double clip = static_cast<double>(g) / 20.0;
+        for (size_t j = 0; j < cols; ++j) s[j] = maxabs[j] == 0.0 ? 1.0 : clip * maxabs[j] / qd;
+        double err = 0.0;
+        for (size_t i = 0; i < rows; ++i)
+            for (size_t j = 0; j < cols; ++j) {
+                const long long qi = std::clamp(std::llround(w[i * cols + j] / s[j]), -lim, lim);
+                const double d = w[i * cols + j] - static_cast<double>(qi) * s[j];
+                err += d * d;
+            }
+        if (best_err < 0.0 || err < best_err) {
+            best_err = err;
+            best_clip = clip;
+        }
+    }
+    scales.assign(cols, 0.0);
+    q.assign(rows * cols, 0);
+    for (size_t j = 0; j < cols; ++j) scales[j] = maxabs[j] == 0.0 ? 1.0 : best_clip * maxabs[j] / qd;
+    for (size_t i = 0; i < rows; ++i)
+        for (size_t j = 0; j < cols; ++j)
+            q[i * cols + j] = static_cast<int8_t>(
+                std::clamp(std::llround(w[i * cols + j] / scales[j]), -lim, lim));
+    return best_clip;
+}
+
+// S1 = blockdiag(H_blk / sqrt(blk)) applied to the columns of a (E x r): fp64 FWHT.
+void rotate_columns(std::vector<double>& a, size_t E, size_t r, size_t blk) {
+    const double scale = 1.0 / std::sqrt(static_cast<double>(blk));
+    std::vector<double> col(E);
+    for (size_t j = 0; j < r; ++j) {
+        for (size_t i = 0; i < E; ++i) col[i] = a[i * r + j];
+        for (size_t b0 = 0; b0 < E; b0 += blk)
+            for (size_t len = 1; len < blk; len <<= 1)
+                for (size_t i = b0; i < b0 + blk; i += 2 * len)
+                    for (size_t k = i; k < i + len; ++k) {
+                        const double x = col[k], y = col[k + len];
+                        col[k] = x + y;
+                        col[k + len] = x - y;
+                    }
+        for (size_t i = 0; i < E; ++i) a[i * r + j] = col[i] * scale;
+    }
+}
+
+size_t rot_block(size_t E) {
+    if (E && !(E & (E - 1))) return E;
+    if (E % 128 == 0) return 128;
+    return 0;
+}
+
+int sm100_devices() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    int good = 0;
+    for (int d = 0; d < n; ++d) {
+        cudaDeviceProp p;
+        if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++good;
+    }
+    return good;
+}
+
+// ------------------------------------------------------------- NCCL (dlopen)
+struct NcclApi {
+    void* h = nullptr;
+    int (*getUniqueId)(void*) = nullptr;
+    int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+    int (*commDestroy)(void*) = nullptr;
+    const char* (*errStr)(int) = nullptr;
+    bool ok = false;
+};
+
+struct NcclId {
+    char b[128];
+};
+using CommInitFn = int (*)(void**, int, NcclId, int);
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return;
+        api.h = h;
+        api.getUniqueId = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclGetUniqueId"));
+        api.allReduce = reinterpret_cast<int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t)>(
+            dlsym(h, "ncclAllReduce"));
+        api.commDestroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+        api.errStr = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+        api.ok = api.getUniqueId && api.allReduce && api.commDestroy && dlsym(h, "ncclCommInitRank");
+    });
+    return api;
+}
+
+}  // namespace
+
+// ============================================================== handles ===
+struct wsvd_layer_s {
+    wsvd_layer_desc d{};
+    int R = 0, Kp = 0, Nrows = 0;
+    int bdtype = F32;                 // storage of B factors
+    std::vector<int32_t> ranks;       // [nh][3]
+    std::vector<uint8_t> have;        // [nh][3] uploaded
+    DevBuf A;                         // [Nrows][Kp] (or Kp/2 for I4)
+    DevBuf a_scale;                   // [Nrows] fp32
+    DevBuf B[3];                      // [nh][R][H] per role
+    DevBuf b_scale[3];                // [nh][H] per role
+    int rot_blk = 0;
+    float rot_scale = 1.f;
+    // O-projection
+    int e_out = 0, o_dtype = BF16, oKp = 0;
+    DevBuf Wo;                        // [e_out][oKp]
+};
+
+struct GraphKey {
+    const float* x = nullptr;
+    float* y = nullptr;
+    cudaStream_t s = nullptr;
+};
+
+struct wsvd_cache_s {
+    wsvd_layer_s* L = nullptr;
+    int B = 0, cap = 0, cap_alloc = 0, cdtype = BF16, row_bytes = 0;
+    int len = 0;                      // host mirror of *d_len
+    DevBuf data, scales, ctrl;        // ctrl: [0]=d_len, [1]=done
+    DevBuf qt, q_tmp, attn_ws, attn_cnt, attn_out;
+    DevBuf P, xq, sx;                 // projection workspace
+    int P_M = 0;                      // rows the projection workspace holds
+    DevBuf oP, y_tmp;                 // O-proj partials
+    DevBuf x_dev, y_dev;              // staging for the host-buffer step
+    int chunk = 512, max_chunks = 1, grid = 148;
+    int sms = 148;
+    cudaGraphExec_t gexec = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaStream_t gstream = nullptr;
+    bool gpending = false;
+    GraphKey gkey;
+    ~wsvd_cache_s() {
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (graph) cudaGraphDestroy(graph);
+        if (gstream) cudaStreamDestroy(gstream);
+    }
+    int* d_len() const { return ctrl.as<int>(); }
+    int* d_done() const { return ctrl.as<int>() + 1; }
+};
+
+struct wsvd_comm_s {
+    void* comm = nullptr;
+    int nranks = 1, rank = 0;
+};
+
+namespace {
+
+int check_layer(wsvd_layer_t l) {
+    if (!l) return set_err(WSVD_ECONFIG, "null layer handle");
+    for (size_t i = 0; i < l->have.size(); ++i)
+        if (!l->have[i])
+            return set_err(WSVD_ECONFIG, "factors of head " + std::to_string(i / 3) + " role " +
+                                             std::to_string(i % 3) + " were never uploaded");
+    return WSVD_OK;
+}
+
+int choose_ks(int wdtype, int M, int N, int Kp, int sms) {
+    // Largest split that keeps >= ~4 CTAs per SM in flight and fits 2 CTAs/SM.
+    int best = 256;
+    for (int ks : {256, 512, 1024, 2048}) {
+        if (Kp % ks) continue;
+        if (gemm_smem_bytes(wdtype, M, ks) > 100 * 1024) break;
+        const long ctas = static_cast<long>((N + 63) / 64) * (Kp / ks);
+        if (ctas < 4L * sms && ks != 256) break;
+        best = ks;
+    }
+    if (Kp % best) best = 128;
+    return best;
+}
+
+// projection of M token rows (fp32 x [M][E]) into the partial workspace
+int run_projection(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* splits_out) {
+    wsvd_layer_s* L = c->L;
+    const int wd = L->d.weight_dtype;
+    const int ks = (wd == F32) ? std::min(L->Kp, 1024) : choose_ks(wd, M, L->Nrows, L->Kp, c->sms);
+    const int splits = L->Kp / ks;
+    const size_t need = static_cast<size_t>(splits) * M * L->Nrows * 4;
+    if (c->P.n < need) CUDA_TRY(c->P.alloc(need));
+    GemmArgs g{};
+    g.W = L->A.p;
+    g.P = c->P.p;
+    g.M = M;
+    g.N = L->Nrows;
+    g.K = L->d.embed_dim;
+    g.Kp = L->Kp;
+    g.KS = ks;
+    g.ldx = L->d.embed_dim;
+    g.wdtype = wd;
+    if (wd == I8 || wd == I4) {
+        if (c->xq.n < static_cast<size_t>(M) * L->Kp) CUDA_TRY(c->xq.alloc(static_cast<size_t>(M) * L->Kp));
+        if (c->sx.n < static_cast<size_t>(M) * 4) CUDA_TRY(c->sx.alloc(static_cast<size_t>(M) * 4));
+        CUDA_TRY(launch_act_quant(x, M, L->d.embed_dim, L->Kp, L->d.act_rotation, L->rot_blk,
+                                  L->rot_scale, c->xq.as<int8_t>(), c->sx.as<float>(), s));
+        g.X = c->xq.p;
+    } else {
+        g.X = x;
+    }
+    CUDA_TRY(launch_gemm(g, s));
+    *splits_out = splits;
+    return WSVD_OK;
+}
+
+int run_append(wsvd_cache_s* c, const float* x, int T, float* q_out, float* qt, cudaStream_t s) {
+    wsvd_layer_s* L = c->L;
+    const int M = T * c->B;
+    int splits = 0;
+    int rc = run_projection(c, x, M, s, &splits);
+    if (rc) return rc;
+    AppendArgs a{};
+    a.P = c->P.p;
+    a.splits = splits;
+    a.M = M;
+    a.Nrows = L->Nrows;
+    a.wdtype = L->d.weight_dtype;
+    a.a_scale = L->a_scale.as<float>();
+    a.sx = c->sx.as<float>();
+    a.T = T;
+    a.B = c->B;
+    a.nh = L->d.n_heads;
+    a.R = L->R;
+    a.H = L->d.head_dim;
+    a.cache = c->data.as<uint8_t>();
+    a.cscale = c->scales.as<__half2>();
+    a.cdtype = c->cdtype;
+    a.cap = c->cap_alloc;
+    a.row_bytes = c->row_bytes;
+    a.d_len = c->d_len();
+    a.done = c->d_done();
+    a.bq = L->B[0].p;
+    a.bk = L->B[1].p;
+    a.bq_scale = L->b_scale[0].as<float>();
+    a.bk_scale = L->b_scale[1].as<float>();
+    a.bdtype = L->bdtype;
+    a.q_out = q_out;
+    a.qt = qt;
+    a.qt_scale = 1.4426950408889634f / std::sqrt(static_cast<float>(L->d.head_dim));
+    CUDA_TRY(launch_append_epilogue(a, s));
+    return WSVD_OK;
+}
+
+int run_attention(wsvd_cache_s* c, float* out, cudaStream_t s) {
+    wsvd_layer_s* L = c->L;
+    AttnArgs a{};
+    a.cache = c->data.as<uint8_t>();
+    a.cscale = c->scales.as<__half2>();
+    a.qt = c->qt.as<float>();
+    a.bv = L->B[2].p;
+    a.bv_scale = L->b_scale[2].as<float>();
+    a.bdtype = L->bdtype;
+    a.out = out;
+    a.ws = c->attn_ws.as<float>();
+    a.counters = c->attn_cnt.as<int>();
+    a.d_len = c->d_len();
+    a.B = c->B;
+    a.nh = L->d.n_heads;
+    a.H = L->d.head_dim;
+    a.R = L->R;
+    a.cap = c->cap_alloc;
+    a.chunk = c->chunk;
+    a.max_chunks = c->max_chunks;
+    a.cdtype = c->cdtype;
+    a.row_bytes = c->row_bytes;
+    a.grid = c->grid;
+    CUDA_TRY(launch_decode_attn(a, s));
+    return WSVD_OK;
+}
+
+int run_oproj(wsvd_cache_s* c, const float* attn, float* y, cudaStream_t s) {
+    wsvd_layer_s* L = c->L;
+    if (!L->Wo.p) return set_err(WSVD_ECONFIG, "layer has no O-projection (wsvd_layer_set_oproj)");
+    const int K = L->d.n_heads * L->d.head_dim;
+    const int ks = (L->o_dtype == F32) ? std::min(L->oKp, 1024) : choose_ks(L->o_dtype, c->B, L->e_out, L->oKp, c->sms);
+    const int splits = L->oKp / ks;
+    const size_t need = static_cast<size_t>(splits) * c->B * L->e_out * 4;
+    if (c->oP.n < need) CUDA_TRY(c->oP.alloc(need));
+    GemmArgs g{};
+    g.W = L->Wo.p;
+    g.X = attn;
+    g.P = c->oP.p;
+    g.M = c->B;
+    g.N = L->e_out;
+    g.K = K;
+    g.Kp = L->oKp;
+    g.KS = ks;
+    g.ldx = K;
+    g.wdtype = L->o_dtype;
+    CUDA_TRY(launch_gemm(g, s));
+    CUDA_TRY(launch_reduce_partials(c->oP.as<float>(), splits, c->B, L->e_out, y, s));
+    return WSVD_OK;
+}
+
+int layer_step_impl(wsvd_cache_s* c, const float* x, float* attn_out, float* y, cudaStream_t s) {
+    float* attn = attn_out ? attn_out : c->attn_out.as<float>();
+    int rc = run_append(c, x, 1, nullptr, c->qt.as<float>(), s);
+    if (rc) return rc;
+    rc = run_attention(c, attn, s);
+    if (rc) return rc;
+    return run_oproj(c, attn, y, s);
+}
+
+}  // namespace
+
+// ================================================================= C ABI ===
+extern "C" {
+
+const char* wsvd_last_error(void) { return g_err.c_str(); }
+int wsvd_abi_version(void) { return WSVD_ABI_VERSION; }
+
+int wsvd_device_count(int32_t* n) {
+    if (!n) return set_err(WSVD_ECONFIG, "null output");
+    *n = sm100_devices();
+    return WSVD_OK;
+}
+
+int wsvd_layer_create(const wsvd_layer_desc* desc, const int32_t* ranks, wsvd_layer_t* out) {
+    if (!desc || !ranks || !out) return set_err(WSVD_ECONFIG, "null argument");
+    const wsvd_layer_desc& d = *desc;
+    if (d.n_heads <= 0) return set_err(WSVD_ESHAPE, "latent cache over zero heads");
+    if (d.embed_dim <= 0 || d.head_dim <= 0) return set_err(WSVD_ESHAPE, "empty layer geometry");
+    if (d.weight_dtype < WSVD_F32 || d.weight_dtype > WSVD_I4)
+        return set_err(WSVD_ECONFIG, "unknown weight dtype " + std::to_string(d.weight_dtype));
+    if (d.act_rotation && d.weight_dtype != WSVD_I8 && d.weight_dtype != WSVD_I4)
+        return set_err(WSVD_ECONFIG, "act_rotation applies to I8/I4 weights only");
+    if (sm100_devices() == 0) return set_err(WSVD_ECUDA, "no sm_100 (B200) device visible");
+    int rmax = 0;
+    for (int i = 0; i < d.n_heads * 3; ++i) {
+        if (ranks[i] <= 0 || ranks[i] > d.head_dim)
+            return set_err(WSVD_ESHAPE, "rank " + std::to_string(ranks[i]) + " outside [1, head_dim]");
+        rmax = std::max(rmax, static_cast<int>(ranks[i]));
+    }
+    int R = round_up(rmax, 16);
+    if (R == 16 || R == 32 || R == 48 || R == 64) {
+    } else {
+        return set_err(WSVD_ECONFIG, "padded rank " + std::to_string(R) + " unsupported (max 64)");
+    }
+    CUDA_TRY(cudaSetDevice(d.device));
+    auto* L = new wsvd_layer_s();
+    L->d = d;
+    L->R = R;
+    L->Kp = round_up(d.embed_dim, 256);
+    L->Nrows = d.n_heads * 3 * R;
+    L->ranks.assign(ranks, ranks + d.n_heads * 3);
+    L->have.assign(d.n_heads * 3, 0);
+    L->bdtype = (d.weight_dtype == WSVD_I4) ? I8 : d.weight_dtype;
+    if (d.act_rotation) {
+        const size_t blk = rot_block(static_cast<size_t>(d.embed_dim));
+        if (!blk) {
+            delete L;
+            return set_err(WSVD_ESHAPE, "hadamard: embed_dim must be a power of two or a multiple of 128");
+        }
+        L->rot_blk = static_cast<int>(blk);
+        L->rot_scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(blk)));
+    }
+    const size_t row_bytes = (d.weight_dtype == WSVD_I4) ? L->Kp / 2
+                             : static_cast<size_t>(L->Kp) * (d.weight_dtype == WSVD_F32 ? 4 : d.weight_dtype == WSVD_BF16 ? 2 : 1);
+    const size_t bel = (L->bdtype == F32) ? 4 : (L->bdtype == BF16 ? 2 : 1);
+    cudaError_t e = L->A.alloc(static_cast<size_t>(L->Nrows) * row_bytes);
+    if (e == cudaSuccess) e = L->a_scale.alloc(static_cast<size_t>(L->Nrows) * 4);
+    for (int r = 0; r < 3 && e == cudaSuccess; ++r) {
+        e = L->B[r].alloc(static_cast<size_t>(d.n_heads) * R * d.head_dim * bel);
+        if (e == cudaSuccess) e = L->b_scale[r].alloc(static_cast<size_t>(d.n_heads) * d.head_dim * 4);
+    }
+    if (e != cudaSuccess) {
+        delete L;
+        return set_err(WSVD_ECUDA, std::string("layer allocation: ") + cudaGetErrorString(e));
+    }
+    *out = L;
+    return WSVD_OK;
+}
+
+int wsvd_layer_destroy(wsvd_layer_t layer) {
+    delete layer;
+    return WSVD_OK;
+}
+
+int wsvd_layer_rank_pad(wsvd_layer_t layer, int32_t* rpad) {
+    if (!layer || !rpad) return set_err(WSVD_ECONFIG, "null argument");
+    *rpad = layer->R;
+    return WSVD_OK;
+}
+
+static int upload_head(wsvd_layer_t L, int head, int role, const std::vector<int8_t>* aq,
+                       const std::vector<double>* as, const std::vector<double>* af,
+                       const std::vector<int8_t>* bq, const std::vector<double>* bs,
+                       const std::vector<double>* bf) {
+    const int E = L->d.embed_dim, H = L->d.head_dim, R = L->R;
+    const int r = L->ranks[head * 3 + role];
+    const int wd = L->d.weight_dtype;
+    CUDA_TRY(cudaSetDevice(L->d.device));
+    // ---- A: rows n = (head*3+role)*R + i, each the i-th column of a (E values)
+    const size_t n0 = static_cast<size_t>(head * 3 + role) * R;
+    const size_t rb = (wd == WSVD_I4) ? L->Kp / 2 : static_cast<size_t>(L->Kp) * (wd == WSVD_F32 ? 4 : wd == WSVD_BF16 ? 2 : 1);
+    std::vector<uint8_t> rows(static_cast<size_t>(R) * rb, 0);
+    std::vector<float> ascale(R, 1.f);
+    for (int i = 0; i < r; ++i) {
+        uint8_t* dst = rows.data() + static_cast<size_t>(i) * rb;
+        for (int k = 0; k < E; ++k) {
+            const size_t src = static_cast<size_t>(k) * r + i;
+            if (wd == WSVD_F32) {
+                reinterpret_cast<float*>(dst)[k] = static_cast<float>((*af)[src]);
+            } else if (wd == WSVD_BF16) {
+                reinterpret_cast<uint16_t*>(dst)[k] = f32_to_bf16_bits(static_cast<float>((*af)[src]));
+            } else if (wd == WSVD_I8) {
+                reinterpret_cast<int8_t*>(dst)[k] = (*aq)[src];
+            } else {
+                const int v = (*aq)[src];
+                if (v < -7 || v > 7) return set_err(WSVD_ENUMERIC, "int4 weight outside [-7, 7]");
+                uint8_t& byte = dst[k >> 1];
+                byte = static_cast<uint8_t>((k & 1) ? ((byte & 0x0f) | ((v & 0xf) << 4)) : ((byte & 0xf0) | (v & 0xf)));
+            }
+        }
+        if (as) ascale[i] = static_cast<float>((*as)[i]);
+    }
+    CUDA_TRY(cudaMemcpy(L->A.as<uint8_t>() + n0 * rb, rows.data(), rows.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(L->a_scale.as<float>() + n0, ascale.data(), R * 4, cudaMemcpyHostToDevice));
+    // ---- B: [head][R][H]
+    const size_t bel = (L->bdtype == F32) ? 4 : (L->bdtype == BF16 ? 2 : 1);
+    std::vector<uint8_t> bh(static_cast<size_t>(R) * H * bel, 0);
+    std::vector<float> bsc(H, 1.f);
+    for (int i = 0; i < r; ++i)
+        for (int j = 0; j < H; ++j) {
+            const size_t src = static_cast<size_t>(i) * H + j;
+            const size_t o = static_cast<size_t>(i) * H + j;
+            if (L->bdtype == F32) reinterpret_cast<float*>(bh.data())[o] = static_cast<float>((*bf)[src]);
+            else if (L->bdtype == BF16) reinterpret_cast<uint16_t*>(bh.data())[o] = f32_to_bf16_bits(static_cast<float>((*bf)[src]));
+            else reinterpret_cast<int8_t*>(bh.data())[o] = (*bq)[src];
+        }
+    if (bs)
+        for (int j = 0; j < H; ++j) bsc[j] = static_cast<float>((*bs)[j]);
+    CUDA_TRY(cudaMemcpy(L->B[role].as<uint8_t>() + static_cast<size_t>(head) * R * H * bel, bh.data(), bh.size(),
+                        cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(L->b_scale[role].as<float>() + static_cast<size_t>(head) * H, bsc.data(), H * 4,
+                        cudaMemcpyHostToDevice));
+    L->have[head * 3 + role] = 1;
+    return WSVD_OK;
+}
+
+int wsvd_layer_set_head(wsvd_layer_t L, int32_t head, int32_t role, const double* a, const double* b) {
+    if (!L || !a || !b) return set_err(WSVD_ECONFIG, "null argument");
+    if (head < 0 || head >= L->d.n_heads) return set_err(WSVD_ESHAPE, "head index out of range");
+    if (role < 0 || role > 2) return set_err(WSVD_ECONFIG, "role must be 0 (q), 1 (k) or 2 (v)");
+    const size_t E = L->d.embed_dim, H = L->d.head_dim;
+    const size_t r = L->ranks[head * 3 + role];
+    for (size_t i = 0; i < E * r; ++i)
+        if (!std::isfinite(a[i])) return set_err(WSVD_ENUMERIC, "non-finite entry in factor a");
+    for (size_t i = 0; i < r * H; ++i)
+        if (!std::isfinite(b[i])) return set_err(WSVD_ENUMERIC, "non-finite entry in factor b");
+    std::vector<double> af(a, a + E * r), bf(b, b + r * H);
+    const int wd = L->d.weight_dtype;
+    if (wd == WSVD_F32 || wd == WSVD_BF16) return upload_head(L, head, role, nullptr, nullptr, &af, nullptr, nullptr, &bf);
+    if (L->d.act_rotation) rotate_columns(af, E, r, L->rot_blk);
+    const int bits = (wd == WSVD_I8) ? 8 : 4;
+    std::vector<int8_t> aq, bq;
+    std::vector<double> as, bs;
+    quantize_weight_ref(af, E, r, bits, aq, as);
+    quantize_weight_ref(bf, r, H, bits, bq, bs);
+    return upload_head(L, head, role, &aq, &as, nullptr, &bq, &bs, nullptr);
+}
+
+int wsvd_layer_set_head_quantized(wsvd_layer_t L, int32_t head, int32_t role, const int8_t* a_q,
+                                  const double* a_scales, const int8_t* b_q, const double* b_scales) {
+    if (!L || !a_q || !a_scales || !b_q || !b_scales) return set_err(WSVD_ECONFIG, "null argument");
+    if (L->d.weight_dtype != WSVD_I8 && L->d.weight_dtype != WSVD_I4)
+        return set_err(WSVD_ECONFIG, "quantised upload needs an I8 or I4 layer");
+    if (head < 0 || head >= L->d.n_heads) return set_err(WSVD_ESHAPE, "head index out of range");
+    if (role < 0 || role > 2) return set_err(WSVD_ECONFIG, "role must be 0 (q), 1 (k) or 2 (v)");
+    const size_t E = L->d.embed_dim, H = L->d.head_dim;
+    const size_t r = L->ranks[head * 3 + role];
+    std::vector<int8_t> aq(a_q, a_q + E * r), bq(b_q, b_q + r * H);
+    std::vector<double> as(a_scales, a_scales + r), bs(b_scales, b_scales + H);
+    for (double s : as)
+        if (!(s > 0.0)) return set_err(WSVD_ENUMERIC, "quantization scales must be positive");
+    for (double s : bs)
+        if (!(s > 0.0)) return set_err(WSVD_ENUMERIC, "quantization scales must be positive");
+    return upload_head(L, head, role, &aq, &as, nullptr, &bq, &bs, nullptr);
+}
+
+int wsvd_layer_set_oproj(wsvd_layer_t L, const double* w, int32_t e_out, int32_t dtype) {
+    if (!L || !w) return set_err(WSVD_ECONFIG, "null argument");
+    if (e_out <= 0) return set_err(WSVD_ESHAPE, "e_out must be positive");
+    if (dtype != WSVD_F32 && dtype != WSVD_BF16) return set_err(WSVD_ECONFIG, "O-projection dtype must be F32 or BF16");
+    CUDA_TRY(cudaSetDevice(L->d.device));
+    const int K = L->d.n_heads * L->d.head_dim;
+    L->e_out = e_out;
+    L->o_dtype = dtype;
+    L->oKp = round_up(K, 256);
+    const size_t el = dtype == WSVD_F32 ? 4 : 2;
+    std::vector<uint8_t> rows(static_cast<size_t>(e_out) * L->oKp * el, 0);
+    for (int e = 0; e < e_out; ++e)
+        for (int k = 0; k < K; ++k) {
+            const double v = w[static_cast<size_t>(k) * e_out + e];
+            const size_t o = static_cast<size_t>(e) * L->oKp + k;
+            if (dtype == WSVD_F32) reinterpret_cast<float*>(rows.data())[o] = static_cast<float>(v);
+            else reinterpret_cast<uint16_t*>(rows.data())[o] = f32_to_bf16_bits(static_cast<float>(v));
+        }
+    CUDA_TRY(L->Wo.alloc(rows.size()));
+    CUDA_TRY(cudaMemcpy(L->Wo.p, rows.data(), rows.size(), cudaMemcpyHostToDevice));
+    return WSVD_OK;
+}
+
+int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t cache_dtype, wsvd_cache_t* out) {
+    if (!L || !out) return set_err(WSVD_ECONFIG, "null argument");
+    if (batch <= 0 || capacity <= 0) return set_err(WSVD_ESHAPE, "batch and capacity must be positive");
+    if (cache_dtype != WSVD_F32 && cache_dtype != WSVD_BF16 && cache_dtype != WSVD_I8)
+        return set_err(WSVD_ECONFIG, "cache dtype must be F32, BF16 or I8");
+    if (attn_smem_bytes(cache_dtype, L->R) <= 0) return set_err(WSVD_ECONFIG, "unsupported rank for this cache dtype");
+    CUDA_TRY(cudaSetDevice(L->d.device));
+    auto* c = new wsvd_cache_s();
+    c->L = L;
+    c->B = batch;
+    c->cap = capacity;
+    c->cap_alloc = round_up(capacity, 128);
+    c->cdtype = cache_dtype;
+    const int eb = cache_dtype == WSVD_F32 ? 4 : (cache_dtype == WSVD_BF16 ? 2 : 1);
+    c->row_bytes = 2 * L->R * eb;
+    const int nh = L->d.n_heads, H = L->d.head_dim;
+    cudaDeviceProp p;
+    CUDA_TRY(cudaGetDeviceProperties(&p, L->d.device));
+    c->sms = p.multiProcessorCount;
+    c->grid = c->sms * attn_occupancy(cache_dtype, L->R);
+    // chunk: ~16 units per CTA at full capacity, multiple of 128 tokens
+    long units_target = static_cast<long>(c->grid) * 16;
+    long tok = static_cast<long>(c->cap_alloc) * batch * nh;
+    int chunk = static_cast<int>(round_up(static_cast<int>(std::max(1L, tok / units_target)), 128));
+    chunk = std::max(128, std::min(chunk, 8192));
+    if (const char* env = getenv("WSVD_ATTN_CHUNK")) chunk = std::max(128, round_up(atoi(env), 128));
+    c->chunk = chunk;
+    c->max_chunks = (c->cap_alloc + chunk - 1) / chunk;
+    const size_t rows = static_cast<size_t>(batch) * nh * c->cap_alloc;
+    cudaError_t e = c->data.alloc(rows * c->row_bytes);
+    if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4);
+    if (e == cudaSuccess) e = c->ctrl.alloc(64);
+    if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
+    if (e == cudaSuccess) e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh * c->max_chunks * (L->R + 2) * 4);
+    if (e == cudaSuccess) e = c->attn_cnt.alloc(static_cast<size_t>(batch) * nh * 4);
+    if (e == cudaSuccess) e = c->attn_out.alloc(static_cast<size_t>(batch) * nh * H * 4);
+    if (e != cudaSuccess) {
+        delete c;
+        return set_err(WSVD_ECUDA, std::string("cache allocation: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return WSVD_OK;
+}
+
+int wsvd_cache_destroy(wsvd_cache_t c) {
+    delete c;
+    return WSVD_OK;
+}
+
+int wsvd_cache_reset(wsvd_cache_t c) {
+    if (!c) return set_err(WSVD_ECONFIG, "null cache");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemset(c->ctrl.p, 0, c->ctrl.n));
+    c->len = 0;
+    return WSVD_OK;
+}
+
+int wsvd_cache_bind_layer(wsvd_cache_t c, wsvd_layer_t L) {
+    if (!c || !L) return set_err(WSVD_ECONFIG, "null argument");
+    const wsvd_layer_s* o = c->L;
+    if (L->d.n_heads != o->d.n_heads)
+        return set_err(WSVD_ESHAPE, "cache holds " + std::to_string(o->d.n_heads) + " heads, factors " +
+                                        std::to_string(L->d.n_heads));
+    if (L->R != o->R || L->d.embed_dim != o->d.embed_dim || L->d.head_dim != o->d.head_dim ||
+        L->d.device != o->d.device)
+        return set_err(WSVD_ESHAPE, "factor geometry differs from the cache's layer");
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    if (c->graph) {
+        cudaGraphDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    c->gpending = false;
+    c->gkey = GraphKey{};
+    c->L = L;
+    return WSVD_OK;
+}
+
+int wsvd_cache_length(wsvd_cache_t c, int32_t* len) {
+    if (!c || !len) return set_err(WSVD_ECONFIG, "null argument");
+    *len = c->len;
+    return WSVD_OK;
+}
+
+int wsvd_cache_row_bytes(wsvd_cache_t c, int32_t* rb) {
+    if (!c || !rb) return set_err(WSVD_ECONFIG, "null argument");
+    *rb = c->row_bytes;
+    return WSVD_OK;
+}
+
+int wsvd_cache_push_host(wsvd_cache_t c, const double* ck, const double* cv) {
+    if (!c || !ck || !cv) return set_err(WSVD_ECONFIG, "null argument");
+    if (c->len >= c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
+    wsvd_layer_s* L = c->L;
+    const int nh = L->d.n_heads, R = L->R;
+    if (c->cdtype == WSVD_I8) return set_err(WSVD_ECONFIG, "push_host supports F32/BF16 caches");
+    CUDA_TRY(cudaSetDevice(L->d.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    std::vector<uint8_t> row(c->row_bytes);
+    for (int b = 0; b < c->B; ++b)
+        for (int h = 0; h < nh; ++h) {
+            const int rk = L->ranks[h * 3 + 1], rv = L->ranks[h * 3 + 2];
+            for (int i = 0; i < 2 * R; ++i) {
+                const bool kpart = i < R;
+                const int j = kpart ? i : i - R;
+                double v = 0.0;
+                if (kpart && j < rk) v = ck[(static_cast<size_t>(b) * nh + h) * R + j];
+                if (!kpart && j < rv) v = cv[(static_cast<size_t>(b) * nh + h) * R + j];
+                if (c->cdtype == WSVD_F32) reinterpret_cast<float*>(row.data())[i] = static_cast<float>(v);
+                else reinterpret_cast<uint16_t*>(row.data())[i] = f32_to_bf16_bits(static_cast<float>(v));
+            }
+            const size_t off = ((static_cast<size_t>(b) * nh + h) * c->cap_alloc + c->len) * c->row_bytes;
+            CUDA_TRY(cudaMemcpy(c->data.as<uint8_t>() + off, row.data(), row.size(), cudaMemcpyHostToDevice));
+        }
+    c->len += 1;
+    CUDA_TRY(cudaMemcpy(c->d_len(), &c->len, 4, cudaMemcpyHostToDevice));
+    return WSVD_OK;
+}
+
+int wsvd_cache_read_raw(wsvd_cache_t c, int32_t b, int32_t h, void* rows_host, uint16_t* scales_host) {
+    if (!c || !rows_host) return set_err(WSVD_ECONFIG, "null argument");
+    if (b < 0 || b >= c->B || h < 0 || h >= c->L->d.n_heads) return set_err(WSVD_ESHAPE, "sequence/head out of range");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    const size_t bh = static_cast<size_t>(b) * c->L->d.n_heads + h;
+    if (c->len > 0) {
+        CUDA_TRY(cudaMemcpy(rows_host, c->data.as<uint8_t>() + bh * c->cap_alloc * c->row_bytes,
+                            static_cast<size_t>(c->len) * c->row_bytes, cudaMemcpyDeviceToHost));
+        if (scales_host && c->cdtype == WSVD_I8)
+            CUDA_TRY(cudaMemcpy(scales_host, c->scales.as<uint8_t>() + bh * c->cap_alloc * 4,
+                                static_cast<size_t>(c->len) * 4, cudaMemcpyDeviceToHost));
+    }
+    return WSVD_OK;
+}
+
+static float half_bits_to_float(uint16_t h) {
+    const uint32_t sign = (static_cast<uint32_t>(h) & 0x8000u) << 16;
+    const uint32_t e = (h >> 10) & 0x1f, m = h & 0x3ff;
+    float v;
+    if (e == 0) {
+        v = static_cast<float>(m) * 5.9604644775390625e-08f;
+        return sign ? -v : v;
+    }
+    uint32_t u = (e == 31) ? (sign | 0x7f800000u | (m << 13)) : (sign | ((e - 15 + 127) << 23) | (m << 13));
+    std::memcpy(&v, &u, 4);
+    return v;
+}
+
+int wsvd_cache_read_host(wsvd_cache_t c, int32_t b, int32_t h, double* ck, double* cv) {
+    if (!c || !ck || !cv) return set_err(WSVD_ECONFIG, "null argument");
+    const int R = c->L->R;
+    std::vector<uint8_t> rows(static_cast<size_t>(c->len) * c->row_bytes);
+    std::vector<uint16_t> sc(static_cast<size_t>(c->len) * 2);
+    int rc = wsvd_cache_read_raw(c, b, h, rows.data(), sc.data());
+    if (rc) return rc;
+    for (int t = 0; t < c->len; ++t) {
+        const uint8_t* r = rows.data() + static_cast<size_t>(t) * c->row_bytes;
+        for (int i = 0; i < 2 * R; ++i) {
+            double v;
+            if (c->cdtype == WSVD_F32) v = reinterpret_cast<const float*>(r)[i];
+            else if (c->cdtype == WSVD_BF16) {
+                uint32_t u = static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(r)[i]) << 16;
+                float f;
+                std::memcpy(&f, &u, 4);
+                v = f;
+            } else {
+                const float s = half_bits_to_float(sc[t * 2 + (i < R ? 0 : 1)]);
+                v = static_cast<double>(reinterpret_cast<const int8_t*>(r)[i]) * static_cast<double>(s);
+            }
+            if (i < R) ck[static_cast<size_t>(t) * R + i] = v;
+            else cv[static_cast<size_t>(t) * R + i - R] = v;
+        }
+    }
+    return WSVD_OK;
+}
+
+int wsvd_append_token(wsvd_cache_t c, const float* x, float* q_out, void* stream) {
+    if (!c || !x) return set_err(WSVD_ECONFIG, "null argument");
+    int rc = check_layer(c->L);
+    if (rc) return rc;
+    if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    rc = run_append(c, x, 1, q_out, c->qt.as<float>(), static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    c->len += 1;
+    return WSVD_OK;
+}
+
+int wsvd_prefill(wsvd_cache_t c, const float* x, int32_t T, void* stream) {
+    if (!c || !x) return set_err(WSVD_ECONFIG, "null argument");
+    if (T <= 0) return set_err(WSVD_ESHAPE, "prefill of zero tokens");
+    int rc = check_layer(c->L);
+    if (rc) return rc;
+    if (c->len + T > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    const int E = c->L->d.embed_dim;
+    const int tc = std::max(1, 128 / c->B);  // <= 128 token rows per projection
+    for (int t0 = 0; t0 < T; t0 += tc) {
+        const int n = std::min(tc, T - t0);
+        rc = run_append(c, x + static_cast<size_t>(t0) * c->B * E, n, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+        if (rc) return rc;
+        c->len += n;
+    }
+    return WSVD_OK;
+}
+
+int wsvd_fused_decode_step(wsvd_cache_t c, const float* q, int32_t tile_len, float* out, void* stream) {
+    if (!c || !q || !out) return set_err(WSVD_ECONFIG, "null argument");
+    if (c->len == 0) return set_err(WSVD_ESHAPE, "decode step over an empty cache");
+    if (tile_len <= 0) return set_err(WSVD_ECONFIG, "tile length must be >= 1");
+    int rc = check_layer(c->L);
+    if (rc) return rc;
+    wsvd_layer_s* L = c->L;
+    CUDA_TRY(cudaSetDevice(L->d.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(launch_absorb_query(q, c->B, L->d.n_heads, L->R, L->d.head_dim, L->B[1].p, L->b_scale[1].as<float>(),
+                                 L->bdtype, 1.4426950408889634f / std::sqrt(static_cast<float>(L->d.head_dim)),
+                                 c->qt.as<float>(), s));
+    return run_attention(c, out, s);
+}
+
+int wsvd_layer_step(wsvd_cache_t c, const float* x, float* attn_out, float* y, void* stream) {
+    if (!c || !x || !y) return set_err(WSVD_ECONFIG, "null argument");
+    int rc = check_layer(c->L);
+    if (rc) return rc;
+    if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    rc = layer_step_impl(c, x, attn_out, y, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    c->len += 1;
+    return WSVD_OK;
+}
+
+int wsvd_layer_step_graph(wsvd_cache_t c, const float* x, float* y, void* stream) {
+    if (!c || !x || !y) return set_err(WSVD_ECONFIG, "null argument");
+    int rc = check_layer(c->L);
+    if (rc) return rc;
+    if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const bool same = c->gkey.x == x && c->gkey.y == y && c->gkey.s == s;
+    if (c->gexec && same) {
+        CUDA_TRY(cudaGraphLaunch(c->gexec, c->gstream ? c->gstream : s));
+        c->len += 1;
+        return WSVD_OK;
+    }
+    if (!same || !c->gpending) {
+        // first call with these buffers: run eagerly (sizes workspaces, sets
+        // kernel attributes); the next call captures and replays
+        if (c->gexec) cudaGraphExecDestroy(c->gexec);
+        if (c->graph) cudaGraphDestroy(c->graph);
+        c->gexec = nullptr;
+        c->graph = nullptr;
+        rc = layer_step_impl(c, x, nullptr, y, s);
+        if (rc) return rc;
+        c->gkey = {x, y, s};
+        c->gpending = true;
+        c->len += 1;
+        return WSVD_OK;
+    }
+    // capture (the legacy stream cannot be captured: use an owned blocking stream)
+    cudaStream_t cs = s;
+    if (cs == nullptr) {
+        if (!c->gstream) CUDA_TRY(cudaStreamCreateWithFlags(&c->gstream, cudaStreamDefault));
+        cs = c->gstream;
+    }
+    CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    rc = layer_step_impl(c, x, nullptr, y, cs);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(cs, &g);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        return rc;
+    }
+    if (e != cudaSuccess) return set_err(WSVD_ECUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+    c->graph = g;
+    CUDA_TRY(cudaGraphInstantiate(&c->gexec, g, 0));
+    c->gpending = false;
+    CUDA_TRY(cudaGraphLaunch(c->gexec, cs));
+    c->len += 1;
+    return WSVD_OK;
+}
+
+int wsvd_layer_step_host(wsvd_cache_t c, const float* x_host, float* y_host, void* stream) {
+    if (!c || !x_host || !y_host) return set_err(WSVD_ECONFIG, "null argument");
+    wsvd_layer_s* L = c->L;
+    if (!L->Wo.p) return set_err(WSVD_ECONFIG, "layer has no O-projection (wsvd_layer_set_oproj)");
+    CUDA_TRY(cudaSetDevice(L->d.device));
+    const size_t xb = static_cast<size_t>(c->B) * L->d.embed_dim * 4;
+    const size_t yb = static_cast<size_t>(c->B) * L->e_out * 4;
+    if (c->x_dev.n < xb) CUDA_TRY(c->x_dev.alloc(xb));
+    if (c->y_dev.n < yb) CUDA_TRY(c->y_dev.alloc(yb));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaMemcpyAsync(c->x_dev.p, x_host, xb, cudaMemcpyHostToDevice, s));
+    int rc = wsvd_layer_step_graph(c, c->x_dev.as<float>(), c->y_dev.as<float>(), stream);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(y_host, c->y_dev.p, yb, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return WSVD_OK;
+}
+
+int wsvd_traffic_append(wsvd_cache_t c, uint64_t* k) {
+    if (!c || !k) return set_err(WSVD_ECONFIG, "null argument");
+    wsvd_layer_s* L = c->L;
+    const uint64_t E = L->d.embed_dim, H = L->d.head_dim, Bn = c->B;
+    k[WSVD_STREAM_QUERY] += Bn * E;  // decode.cpp:132
+    for (int h = 0; h < L->d.n_heads; ++h) {
+        const uint64_t rq = L->ranks[h * 3], rk = L->ranks[h * 3 + 1], rv = L->ranks[h * 3 + 2];
+        k[14 + WSVD_STREAM_LATENT_K] += Bn * E * rk;
+        k[7 + WSVD_STREAM_LATENT_K] += Bn * rk;
+        k[14 + WSVD_STREAM_LATENT_V] += Bn * E * rv;
+        k[7 + WSVD_STREAM_LATENT_V] += Bn * rv;
+        k[14 + WSVD_STREAM_QUERY] += Bn * (E * rq + rq * H);
+    }
+    return WSVD_OK;
+}
+
+int wsvd_traffic_fused(wsvd_cache_t c, int32_t tile_len, uint64_t* k) {
+    if (!c || !k) return set_err(WSVD_ECONFIG, "null argument");
+    if (c->len == 0) return set_err(WSVD_ESHAPE, "decode step over an empty cache");
+    if (tile_len <= 0) return set_err(WSVD_ECONFIG, "tile length must be >= 1");
+    wsvd_layer_s* L = c->L;
+    const uint64_t H = L->d.head_dim, Bn = c->B, len = c->len;
+    for (int h = 0; h < L->d.n_heads; ++h) {
+        const uint64_t rk = L->ranks[h * 3 + 1], rv = L->ranks[h * 3 + 2];
+        k[WSVD_STREAM_WEIGHTS_B] += Bn * (rk * H + rv * H);      // decode.cpp:176
+        k[WSVD_STREAM_QUERY] += Bn * H;                          // decode.cpp:177
+        k[WSVD_STREAM_LATENT_K] += Bn * len * rk;                // decode.cpp:184
+        k[WSVD_STREAM_LATENT_V] += Bn * len * rv;                // decode.cpp:185
+        k[14 + WSVD_STREAM_LATENT_K] += Bn * len * rk * H;       // decode.cpp:189
+        k[14 + WSVD_STREAM_QUERY] += Bn * len * H;               // decode.cpp:191
+        k[14 + WSVD_STREAM_LATENT_V] += Bn * len * rv;           // decode.cpp:193
+        k[14 + WSVD_STREAM_OUTPUT] += Bn * rv * H;               // decode.cpp:201
+        k[7 + WSVD_STREAM_OUTPUT] += Bn * H;                     // decode.cpp:202
+    }
+    return WSVD_OK;
+}
+
+int wsvd_nccl_unique_id(uint8_t id[128]) {
+    NcclApi& n = nccl();
+    if (!n.ok) return set_err(WSVD_ENCCL, "libnccl.so.2 not loadable");
+    const int r = n.getUniqueId(id);
+    if (r) return set_err(WSVD_ENCCL, std::string("ncclGetUniqueId: ") + (n.errStr ? n.errStr(r) : "?"));
+    return WSVD_OK;
+}
+
+int wsvd_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device, wsvd_comm_t* out) {
+    if (!id || !out) return set_err(WSVD_ECONFIG, "null argument");
+    NcclApi& n = nccl();
+    if (!n.ok) return set_err(WSVD_ENCCL, "libnccl.so.2 not loadable");
+    CUDA_TRY(cudaSetDevice(device));
+    auto init = reinterpret_cast<CommInitFn>(dlsym(n.h, "ncclCommInitRank"));
+    NcclId nid;
+    std::memcpy(nid.b, id, 128);
+    void* comm = nullptr;
+    const int r = init(&comm, nranks, nid, rank);
+    if (r) return set_err(WSVD_ENCCL, std::string("ncclCommInitRank: ") + (n.errStr ? n.errStr(r) : "?"));
+    auto* c = new wsvd_comm_s();
+    c->comm = comm;
+    c->nranks = nranks;
+    c->rank = rank;
+    *out = c;
+    return WSVD_OK;
+}
+
+int wsvd_comm_destroy(wsvd_comm_t c) {
+    if (!c) return WSVD_OK;
+    NcclApi& n = nccl();
+    if (n.ok && c->comm) n.commDestroy(c->comm);
+    delete c;
+    return WSVD_OK;
+}
+
+int wsvd_allreduce_sum_f32(wsvd_comm_t c, float* buf, int64_t count, void* stream) {
+    if (!c || !buf) return set_err(WSVD_ECONFIG, "null argument");
+    NcclApi& n = nccl();
+    if (!n.ok) return set_err(WSVD_ENCCL, "libnccl.so.2 not loadable");
+    const int r = n.allReduce(buf, buf, static_cast<size_t>(count), /*ncclFloat32*/ 7, /*ncclSum*/ 0, c->comm,
+                              static_cast<cudaStream_t>(stream));
+    if (r) return set_err(WSVD_ENCCL, std::string("ncclAllReduce: ") + (n.errStr ? n.errStr(r) : "?"));
+    return WSVD_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// kernels.h -- launch interface between the C ABI (capi.cu) and the kernels.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace wsvd_k {
+
+enum DType { F32 = 0, BF16 = 1, I8 = 2, I4 = 3 };
+
+// ---------------------------------------------------------------- GEMM --
+// Partial skinny GEMM  P[split][m][n] = sum_{k in split} X[m][k] * W[n][k]
+// (W K-major).  bf16: X fp32 -> bf16, fp32 partials.  i8 / i4: X int8,
+// int32 partials (exact).  f32: CUDA-core fp32.
+struct GemmArgs {
+    const void* W;   // [N][Kp] (bf16 / f32 / i8) or [N][Kp/2] (i4)
+    const void* X;   // fp32 [M][ldx] (f32 / bf16 modes) or int8 [M][Kp]
+    void* P;         // [splits][M][N] fp32 or int32
+    int M, N, K;     // K: valid columns of X (fp32 modes); Kp: padded K
+    int Kp, KS;      // KS: K per split (Kp % KS == 0)
+    int ldx;         // row stride of fp32 X (elements)
+    int wdtype;      // DType
+};
+int gemm_smem_bytes(int wdtype, int M, int KS);
+cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s);
+
+// Sum split partials into fp32 y [M][N] (fixed split order).
+cudaError_t launch_reduce_partials(const float* P, int splits, int M, int N, float* y,
+                                   cudaStream_t s);
+
+// ------------------------------------------------------ activation quant --
+// Per token: optional S1 rotation (FWHT over blocks of rot_blk, times
+// rot_scale), s = max|v|/127, q = clamp(roundf(v/s)); xq [M][Kp] zero-padded.
+cudaError_t launch_act_quant(const float* x, int M, int E, int Kp, int rot, int rot_blk,
+                             float rot_scale, int8_t* xq, float* sx, cudaStream_t s);
+
+// ------------------------------------------------------ append epilogue --
+struct AppendArgs {
+    const void* P;        // projection partials [splits][M][Nrows] (fp32 or int32)
+    int splits, M, Nrows;
+    int wdtype;           // DType of projection (int modes dequantise)
+    const float* a_scale; // [Nrows] per-row weight scales (int modes)
+    const float* sx;      // [M] per-token activation scales (int modes)
+    int T, B;             // tokens per sequence in this call, sequences (row m = t*B + b)
+    int nh, R, H;         // local heads, padded rank, head dim
+    // cache
+    uint8_t* cache;       // [B][nh][cap][row_bytes]
+    __half2* cscale;      // [B][nh][cap] (int8 cache)
+    int cdtype, cap, row_bytes;
+    int* d_len;           // committed length (read at start, += T by the last CTA)
+    int* done;            // CTA completion counter (self-resetting)
+    // query path (only when T == 1)
+    const void* bq;       // B_Q [nh][R][H]
+    const void* bk;       // B_K [nh][R][H]
+    const float* bq_scale;  // [nh][H] (int modes)
+    const float* bk_scale;
+    int bdtype;
+    float* q_out;         // [M][nh][H] or null
+    float* qt;            // [M][nh][R] absorbed query (log2 domain) or null
+    float qt_scale;       // log2(e) / sqrt(H)
+};
+cudaError_t launch_append_epilogue(const AppendArgs& a, cudaStream_t s);
+
+// q [B][nh][H] -> qt [B][nh][R] = qt_scale * q . B_K^T
+cudaError_t launch_absorb_query(const float* q, int B, int nh, int R, int H, const void* bk,
+                                const float* bk_scale, int bdtype, float qt_scale, float* qt,
+                                cudaStream_t s);
+
+// ------------------------------------------------------------ attention --
+struct AttnArgs {
+    const uint8_t* cache;   // [B][nh][cap][row_bytes]
+    const __half2* cscale;  // [B][nh][cap]
+    const float* qt;        // [B][nh][R]
+    const void* bv;         // B_V [nh][R][H]
+    const float* bv_scale;  // [nh][H]
+    int bdtype;
+    float* out;             // [B][nh][H]
+    float* ws;              // [B*nh][max_chunks][R+2]
+    int* counters;          // [B*nh], zero between launches (self-resetting)
+    const int* d_len;       // valid rows (device)
+    int B, nh, H, R, cap, chunk, max_chunks, cdtype, row_bytes;
+    int grid;               // persistent CTAs
+};
+int attn_smem_bytes(int cdtype, int R);
+int attn_occupancy(int cdtype, int R);  // resident CTAs per SM (0 if unsupported)
+cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s);
+
+}  // namespace wsvd_k

@@ -1,0 +1,124 @@
+"""Batched, device-resident decode layer: the performance API used by the
+benchmark and the multi-GPU path.
+
+One object holds (a head shard of) one attention layer on one GPU: the
+factored Q/K/V projections, the matching rows of W_o, and a latent cache for
+``batch`` sequences.  ``step`` is pipe::decode_factored's per-token body for
+one layer (pipeline.cpp:320-329): append the token, attend with its own
+query, O-project -- launched as one CUDA graph (projection GEMM, append
+epilogue, attention, O-proj GEMM, split reduction).
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from .decode import DeviceLayer, LayerFactors
+from .errors import ConfigError, ShapeError
+
+
+def _torch():
+    import torch
+    return torch
+
+
+class DecodeLayer:
+    def __init__(self, f: LayerFactors, w_o_rows: np.ndarray | None, batch: int, capacity: int,
+                 cache_dtype: str = "bf16", weight_dtype: str = "bf16", oproj_dtype: str = "bf16",
+                 device: int = 0, head_offset: int = 0, act_rotation: bool | None = None):
+        if cache_dtype not in ("f32", "bf16", "i8"):
+            raise ConfigError(f"unknown cache dtype '{cache_dtype}'")
+        self.device = device
+        self.batch = batch
+        self.layer = DeviceLayer(f, weight_dtype, device, act_rotation=act_rotation,
+                                 head_offset=head_offset)
+        self.e_out = None
+        if w_o_rows is not None:
+            self.layer.set_oproj(w_o_rows, oproj_dtype)
+            self.e_out = self.layer.e_out
+        h = C.c_void_p()
+        N.call("wsvd_cache_create", self.layer.h, batch, capacity, N.DTYPES[cache_dtype],
+               C.byref(h))
+        self.h = h
+        self.n_heads = self.layer.n_heads
+        self.head_dim = self.layer.head_dim
+        self.embed_dim = self.layer.embed_dim
+        self.rpad = self.layer.rpad
+        rb = C.c_int32()
+        N.call("wsvd_cache_row_bytes", self.h, C.byref(rb))
+        self.row_bytes = rb.value
+
+    def __del__(self):
+        if getattr(self, "h", None) and N._lib is not None:
+            N.lib().wsvd_cache_destroy(self.h)
+            self.h = None
+
+    @staticmethod
+    def _ptr(t):
+        return C.c_void_p(t.data_ptr())
+
+    @staticmethod
+    def _stream(stream=None):
+        torch = _torch()
+        s = stream if stream is not None else torch.cuda.current_stream()
+        return C.c_void_p(s.cuda_stream)
+
+    def length(self) -> int:
+        n = C.c_int32()
+        N.call("wsvd_cache_length", self.h, C.byref(n))
+        return n.value
+
+    def reset(self):
+        N.call("wsvd_cache_reset", self.h)
+
+    def prefill(self, x, stream=None):
+        """x: fp32 device tensor [T][batch][E] (token-major)."""
+        if x.dim() != 3 or x.shape[1] != self.batch or x.shape[2] != self.embed_dim:
+            raise ShapeError(f"prefill expects [T][{self.batch}][{self.embed_dim}], got {tuple(x.shape)}")
+        N.call("wsvd_prefill", self.h, self._ptr(x), int(x.shape[0]), self._stream(stream))
+
+    def append(self, x, q_out=None, stream=None):
+        N.call("wsvd_append_token", self.h, self._ptr(x),
+               self._ptr(q_out) if q_out is not None else None, self._stream(stream))
+
+    def attend(self, q, out, tile_len: int = 32, stream=None):
+        N.call("wsvd_fused_decode_step", self.h, self._ptr(q), tile_len, self._ptr(out),
+               self._stream(stream))
+
+    def step(self, x, y, attn_out=None, graph: bool = True, stream=None):
+        """One layer step for every sequence: x [batch][E] -> y [batch][e_out]
+        (this shard's partial O-projection)."""
+        if self.e_out is None:
+            raise ConfigError("layer built without W_o rows")
+        if graph and attn_out is None:
+            N.call("wsvd_layer_step_graph", self.h, self._ptr(x), self._ptr(y), self._stream(stream))
+        else:
+            N.call("wsvd_layer_step", self.h, self._ptr(x),
+                   self._ptr(attn_out) if attn_out is not None else None, self._ptr(y),
+                   self._stream(stream))
+
+    def step_host(self, x_host, y_host, stream=None):
+        """Same through host buffers (pinned torch tensors or numpy arrays)."""
+        def hp(t):
+            if isinstance(t, np.ndarray):
+                return C.c_void_p(t.ctypes.data)
+            return C.c_void_p(t.data_ptr())
+        N.call("wsvd_layer_step_host", self.h, hp(x_host), hp(y_host), self._stream(stream))
+
+    def read_latents(self, seq: int, head: int):
+        L, R = self.length(), self.rpad
+        ck = np.zeros((L, R))
+        cv = np.zeros((L, R))
+        N.call("wsvd_cache_read_host", self.h, seq, head, ck.ctypes.data_as(C.POINTER(C.c_double)),
+               cv.ctypes.data_as(C.POINTER(C.c_double)))
+        return ck, cv
+
+    def read_raw(self, seq: int, head: int):
+        L = self.length()
+        rows = np.zeros((L, self.row_bytes), dtype=np.uint8)
+        scales = np.zeros((L, 2), dtype=np.uint16)
+        N.call("wsvd_cache_read_raw", self.h, seq, head, C.c_void_p(rows.ctypes.data),
+               C.c_void_p(scales.ctypes.data))
+        return rows, scales

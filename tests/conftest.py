@@ -1,0 +1,22 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs an sm_100 (B200) GPU and the native library")
+    config.addinivalue_line("markers", "slow: full-size (BASELINE config) parity checks")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _oracle_built():
+    # the CPU oracle is test infrastructure; build it on first use
+    from oracle import oracle as O
+    if not os.path.exists(O.ORACLE_SO):
+        O.build()
+    yield

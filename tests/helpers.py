@@ -1,0 +1,40 @@
+"""Shared test helpers: convert between the oracle's padded layer layout and
+the reference-API LayerFactors, and the parity metric."""
+from __future__ import annotations
+
+import numpy as np
+
+from oracle import oracle as O
+from paper_2604_02570_b200.decode import HeadFactors, HeadProjection, LayerFactors, Role
+
+# north_star: floating-point attention outputs within max relative error 1e-3
+# (fp32 accumulate), measured per (sequence, head) row as max|gpu - ref| / max|ref|
+# (SURVEY.md section 7 "Tolerance definition").
+REL_TOL = 1e-3
+
+
+def to_factors(lay: O.Layer) -> LayerFactors:
+    heads = []
+    for h in range(lay.nh):
+        hf = []
+        for role in range(3):
+            r = int(lay.ranks[h, role])
+            hf.append(HeadFactors(a=lay.A[h, role, :, :r].copy(), b=lay.B[h, role, :r, :].copy(),
+                                  rank=r, head=h, role=Role(role)))
+        heads.append(HeadProjection(*hf))
+    return LayerFactors(heads=heads, embed_dim=lay.E, head_dim=lay.H)
+
+
+def rel_err_rows(gpu: np.ndarray, ref: np.ndarray) -> float:
+    """max over rows (last axis = H) of max|gpu-ref| / max|ref|."""
+    g = gpu.reshape(-1, gpu.shape[-1])
+    r = ref.reshape(-1, ref.shape[-1])
+    num = np.abs(g - r).max(axis=1)
+    den = np.maximum(np.abs(r).max(axis=1), 1e-30)
+    return float((num / den).max())
+
+
+def pad_latents(lat: np.ndarray, rmax: int) -> np.ndarray:
+    out = np.zeros((lat.shape[0], rmax))
+    out[:, : lat.shape[1]] = lat
+    return out
