@@ -1,0 +1,472 @@
+#!/usr/bin/env python
+"""Benchmark of the WSVD per-head low-rank decode layer on B200.
+
+Metric (BASELINE.json): decode-attention us/layer and tokens/s at the
+LLaVA-1.5-7B attention shape (32 heads x 128, E = 4096), per-head rank 32,
+ctx 4K, bf16 storage / fp32 accumulate (configs[1]), with the fraction of the
+HBM roofline of the dominant kernel.
+
+One step = one attention-layer decode step for every sequence
+(pipe::decode_factored's body, pipeline.cpp:320-329): latent projection of
+the new token (Q/K/V for every head), latent-cache append, fused decode
+attention over the cache, O-projection; on N > 1 GPUs the heads are sharded
+and one NCCL all-reduce sums the O-projection partials.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...
+
+Scaling is weak: global batch = 16 * N sequences, heads sharded N ways, so
+every GPU streams the same 268 MB of latent cache per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: E, nh, H, r, batch per GPU-equivalent, ctx, cache dtype, weight dtype
+    "7b-r32-b16-ctx4k-bf16": dict(E=4096, nh=32, H=128, r=32, B=16, L=4096, cache="bf16",
+                                  weights="bf16"),
+    "7b-r32-b1-ctx2k-f32": dict(E=4096, nh=32, H=128, r=32, B=1, L=2048, cache="f32",
+                                weights="f32"),
+    "7b-r32-b32-ctx4k-w8a8-i8cache": dict(E=4096, nh=32, H=128, r=32, B=32, L=4096, cache="i8",
+                                          weights="i8"),
+    "13b-r48-b64-ctx8k-w4a8-i8cache": dict(E=5120, nh=40, H=128, r=48, B=64, L=8192, cache="i8",
+                                           weights="i4"),
+}
+DEFAULT_CONFIG = "7b-r32-b16-ctx4k-bf16"
+METRIC = "WSVD decode attn µs/layer & tokens/s (LLaVA-7B shape, ctx 4K); % HBM roofline"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------ clocks ------
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, smax, reasons, power = [], [], set(), []
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+                power.append(float(parts[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        loaded = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w_max": max(power) if power else None}
+
+
+# ------------------------------------------------------- synthetic layer --
+def synthetic_layer(cfg, seed=0):
+    """Random-init factors of the config's shape (decode-bench recipe,
+    wsvd_main.cpp:360-391: A ~ N(0, 1/E), B ~ N(0, 1/r)) and W_o ~ N(0, 1/E)
+    (toymodel.cpp:81,90).  numpy PCG64 streams; no checkpoint exists offline."""
+    from paper_2604_02570_b200.decode import HeadFactors, HeadProjection, LayerFactors, Role
+    E, nh, H, r = cfg["E"], cfg["nh"], cfg["H"], cfg["r"]
+    rng = np.random.default_rng(seed)
+    heads = []
+    for h in range(nh):
+        roles = []
+        for role in range(3):
+            a = rng.standard_normal((E, r)) / math.sqrt(E)
+            b = rng.standard_normal((r, H)) / math.sqrt(r)
+            roles.append(HeadFactors(a=a, b=b, rank=r, head=h, role=Role(role)))
+        heads.append(HeadProjection(*roles))
+    f = LayerFactors(heads=heads, embed_dim=E, head_dim=H)
+    w_o = rng.standard_normal((nh * H, E)) / math.sqrt(E)
+    return f, w_o
+
+
+def algorithmic_bytes(cfg, B, nh_g, L):
+    """each byte counted once.  Returns (attention-kernel
+    bytes per launch, whole-step bytes)."""
+    E, H, r = cfg["E"], cfg["H"], cfg["r"]
+    cb = {"f32": 4, "bf16": 2, "i8": 1}[cfg["cache"]]
+    wb = {"f32": 4, "bf16": 2, "i8": 1, "i4": 0.5}[cfg["weights"]]
+    cache = B * L * nh_g * 2 * r * cb + (B * L * nh_g * 2 * 2 if cfg["cache"] == "i8" else 0)
+    bfac = nh_g * 3 * r * H * (2 if wb == 2 else (4 if wb == 4 else 1))
+    attn = cache + B * nh_g * r * 4 + nh_g * r * H * (2 if wb == 2 else 4) + B * nh_g * H * 4
+    a_w = E * nh_g * 3 * r * wb + (nh_g * 3 * r * 4 if wb < 2 else 0)
+    oproj = nh_g * H * E * 2
+    step = cache + a_w + bfac + B * E * 4 + B * nh_g * 2 * r * cb + B * nh_g * H * 4 + oproj + B * E * 4
+    return attn, step
+
+
+# ------------------------------------------------------------ our arm -----
+def run_ours(args, cfg_name, cfg):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_02570_b200 import _native as N
+    from paper_2604_02570_b200.layer import DecodeLayer
+    from paper_2604_02570_b200.sharding import NcclComm, shard_factors, shard_oproj
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N.lib()
+    B = cfg["B"] * world                       # weak scaling: 16 sequences per GPU-equivalent
+    nh_g = cfg["nh"] // world
+    E, H = cfg["E"], cfg["H"]
+    L = cfg["L"]
+    W, K = args.warmup, args.steps
+    cap = L + W + K + 64
+
+    t0 = time.time()
+    f, w_o = synthetic_layer(cfg, seed=args.seed)
+    fs = shard_factors(f, world, rank)
+    wo_s = shard_oproj(w_o, cfg["nh"], H, world, rank)
+    layer = DecodeLayer(fs, wo_s, batch=B, capacity=cap, cache_dtype=cfg["cache"],
+                        weight_dtype=cfg["weights"], oproj_dtype="bf16", device=local,
+                        head_offset=rank * nh_g)
+    dev = torch.device("cuda", local)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + args.seed)
+    # prefill L-1-W tokens per sequence on the device (untimed setup)
+    pre = L - 1 - W
+    chunk = 256
+    for t0_ in range(0, pre, chunk):
+        n = min(chunk, pre - t0_)
+        xs = torch.randn((n, B, E), generator=gen, device=dev, dtype=torch.float32)
+        layer.prefill(xs)
+    torch.cuda.synchronize()
+    log(f"[rank {rank}] setup {time.time() - t0:.1f}s, cache length {layer.length()}")
+
+    comm = NcclComm(world, rank, local) if world > 1 else None
+    xs = torch.randn((W + K + 2, B, E), generator=gen, device=dev, dtype=torch.float32)
+    y = torch.empty((B, E), device=dev, dtype=torch.float32)
+    out = torch.empty((B, nh_g, H), device=dev, dtype=torch.float32)
+    stream = torch.cuda.current_stream()
+
+    x_in = torch.empty((B, E), device=dev, dtype=torch.float32)
+
+    def step(i):
+        # the step's token arrives in the layer's (graph-captured) input buffer
+        x_in.copy_(xs[i], non_blocking=True)
+        layer.step(x_in, y)
+        if comm is not None:
+            comm.allreduce_(y)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    for i in range(W):
+        step(i)
+    torch.cuda.synchronize()
+    # soak: keep the GPU under the same load (the attention kernel, no append)
+    # while the clock sampler collects samples around the timed region
+    t_s = time.time()
+    while time.time() - t_s < args.soak_ms / 1e3:
+        for _ in range(50):
+            layer.attention_only(out)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for j in range(K):
+        step(W + j)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = ev0.elapsed_time(ev1)
+    clocks = sampler.stop()
+    L_mid = layer.length() - K // 2
+    ms_t = torch.tensor([ms_total], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_total = float(ms_t.item())
+    ms_step = ms_total / K
+    value = B / (ms_step / 1e3)
+
+    # ---- dominant kernel alone: decode attention (same stream, CUDA events)
+    R = 20
+    for _ in range(3):
+        layer.attention_only(out)
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    for _ in range(R):
+        layer.attention_only(out)
+    a1.record(stream)
+    torch.cuda.synchronize()
+    attn_ms = a0.elapsed_time(a1) / R
+    attn_bytes, step_bytes = algorithmic_bytes(cfg, B, nh_g, layer.length())
+    peak, peak_kind = measured_peak()
+    achieved = attn_bytes / (attn_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "attn_traffic.json")
+    if os.path.exists(tp):
+        try:
+            with open(tp) as fh:
+                traffic = json.load(fh).get(cfg_name)
+        except Exception:
+            traffic = None
+
+    # ---- end to end through the public API with host buffers
+    xh = torch.empty((B, E), dtype=torch.float32).pin_memory()
+    yh = torch.empty((B, E), dtype=torch.float32).pin_memory()
+    xh.copy_(xs[0].cpu())
+    xd = torch.empty((B, E), device=dev, dtype=torch.float32)
+    yd = torch.empty((B, E), device=dev, dtype=torch.float32)
+    Ke = max(3, min(K, 20))
+    e2e_ms = None
+    if layer.length() + Ke + 4 < cap:
+        def e2e_step():
+            if comm is None:
+                layer.step_host(xh.numpy(), yh.numpy())
+            else:
+                xd.copy_(xh, non_blocking=True)
+                layer.step(xd, yd)
+                comm.allreduce_(yd)
+                yh.copy_(yd, non_blocking=True)
+                stream.synchronize()
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t_e = time.perf_counter()
+        for _ in range(Ke):
+            e2e_step()
+        torch.cuda.synchronize()
+        e2e_ms = (time.perf_counter() - t_e) * 1e3 / Ke
+        et = torch.tensor([e2e_ms], device=dev)
+        if world > 1:
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        e2e_ms = float(et.item())
+
+    res = None
+    if rank == 0:
+        res = {
+            "metric": METRIC,
+            "value": round(value, 1),
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": K,
+            "warmup": W,
+            "ms_per_step": round(ms_step, 5),
+            "us_per_layer": round(ms_step * 1e3, 2),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": {"bf16": "bf16 storage / fp32 accumulate", "f32": "f32",
+                      "i8": "int8 (W8A8, int32 accumulate)", "i4": "int4 weights / int8 act"}[cfg["weights"]],
+            "data": "synthetic (random-init factors, decode-bench recipe; random tokens)",
+            "config": {"workload": cfg_name, "embed_dim": E, "heads": cfg["nh"], "heads_per_gpu": nh_g,
+                       "head_dim": H, "rank": cfg["r"], "global_batch": B, "ctx": L_mid,
+                       "ctx_range": [L + 0, layer.length()], "cache_dtype": cfg["cache"],
+                       "weight_dtype": cfg["weights"], "parallelism": f"heads/{world}",
+                       "step": "append(x.A_qkv) + fused decode attention + O-proj"
+                               + (" + NCCL all-reduce" if world > 1 else ""),
+                       "l2": f"inputs larger than L2: {attn_bytes / 1e6:.0f} MB latent cache per GPU per step",
+                       "graph": "one CUDA graph per layer step"},
+            "roofline": {"bound": "hbm", "kernel": "decode_attn_kernel", "achieved": round(achieved, 1),
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic,
+                         "attn_us": round(attn_ms * 1e3, 2), "algorithmic_bytes": int(attn_bytes),
+                         "step_algorithmic_bytes": int(step_bytes),
+                         "step_frac": round(step_bytes / (ms_step / 1e3) / 1e9 / peak, 4)},
+            "clocks": clocks,
+            "gpu_launches": 5 * K + (K if cfg["weights"] in ("i8", "i4") else 0),
+            "e2e": {"value": round(B / (e2e_ms / 1e3), 1) if e2e_ms else None, "unit": "tokens/s",
+                    "ms_per_step": round(e2e_ms, 4) if e2e_ms else None,
+                    "h2d_bytes_per_step": B * E * 4, "d2h_bytes_per_step": B * E * 4,
+                    "api": "wsvd_layer_step_host (C ABI)" if world == 1 else "DecodeLayer.step + NCCL"},
+        }
+    del layer
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return res
+
+
+# ------------------------------------------------------- CPU baselines ----
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_reference_rate(cfg, B, steps, warmup, threads, L=None):
+    """The reference's own fused_decode_step + append_token (oracle/_ref, compiled
+    from the reference sources) on the host cores; returns (tokens/s, kind, detail)."""
+    from oracle import oracle as O
+    L = L or cfg["L"]
+    if O.ref_available():
+        R = O.ref()
+        h = R.ref_baseline_create(cfg["E"], cfg["H"], cfg["nh"], cfg["r"], B, L, 32, 0, threads)
+        if not h:
+            raise RuntimeError(R.ref_last_error().decode())
+        for _ in range(warmup):
+            R.ref_baseline_step(h, threads)
+        ms = [R.ref_baseline_step(h, threads) for _ in range(steps)]
+        R.ref_baseline_destroy(h)
+        kind = "reference"
+    else:
+        # the oracle port (same algorithm, plain C), batched over (sequence, head)
+        lay = O.bench_layer(cfg["E"], cfg["H"], cfg["nh"], cfg["r"])
+        cap = L + warmup + steps + 2
+        ck = np.random.default_rng(0).standard_normal((B, cfg["nh"], cap, cfg["r"]))
+        cv = np.random.default_rng(1).standard_normal((B, cfg["nh"], cap, cfg["r"]))
+        ms = []
+        length = L - 1
+        for i in range(warmup + steps):
+            x = np.random.default_rng(2 + i).standard_normal((B, cfg["E"]))
+            t = time.perf_counter()
+            q = O.batched_append(lay, ck, cv, length, x, threads)
+            O.batched_decode(lay, ck, cv, length + 1, q, 32, threads)
+            length += 1
+            if i >= warmup:
+                ms.append((time.perf_counter() - t) * 1e3)
+        kind = "port"
+    med = statistics.median(ms)
+    return B / (med / 1e3), kind, med
+
+
+def run_reference_arm(args, cfg_name, cfg):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return None
+    threads = cpu_threads()
+    B = cfg["B"] * world
+    rate, kind, med = cpu_reference_rate(cfg, B, args.steps, args.warmup, threads)
+    return {
+        "metric": METRIC, "value": round(rate, 3), "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(med, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (decode-bench recipe factors; N(0,1) latent prefill)",
+        "impl": "reference",
+        "config": {"workload": cfg_name, "embed_dim": cfg["E"], "heads": cfg["nh"],
+                   "head_dim": cfg["H"], "rank": cfg["r"], "global_batch": B, "ctx": cfg["L"],
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": round(rate, 3), "unit": "tokens/s", "cores": threads, "kind": kind,
+                         "sample": f"full workload: {B} sequences x {cfg['nh']} heads, ctx {cfg['L']}, "
+                                   f"append_token + fused_decode_step per (sequence, head), fp64"},
+        "e2e": {"value": round(rate, 3), "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--soak-ms", type=float, default=1500.0,
+                    help="untimed attention load before the timed region while clocks are sampled")
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-seqs", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+    cfg = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        res = run_reference_arm(args, args.config, cfg)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+
+    res = run_ours(args, args.config, cfg)
+    if res is None:
+        return
+    if args.gpus == 1 and not args.no_cpu_baseline:
+        threads = cpu_threads()
+        try:
+            bs = args.cpu_sample_seqs
+            rate, kind, med = cpu_reference_rate(cfg, bs, 2, 1, threads)
+            res["cpu_baseline"] = {
+                "value": round(rate, 3), "unit": "tokens/s", "cores": threads, "kind": kind,
+                "sample": f"{bs} sequences x {cfg['nh']} heads at ctx {cfg['L']} (same per-sequence "
+                          f"work as the workload; tokens/s = sequences / step time), median of 2 steps, fp64",
+                "ms_per_step": round(med, 2)}
+        except Exception as e:  # the baseline is reported, never the target
+            res["cpu_baseline"] = {"value": None, "unit": "tokens/s", "cores": threads,
+                                   "kind": "unavailable", "sample": str(e)[:200]}
+    print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

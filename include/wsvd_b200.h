@@ -161,6 +161,10 @@ int wsvd_prefill(wsvd_cache_t cache, const float* x, int32_t T, void* stream);
  * the same result up to reassociation, as in the reference. */
 int wsvd_fused_decode_step(wsvd_cache_t cache, const float* q, int32_t tile_len, float* out,
                            void* stream);
+/* The attention kernel alone, with the absorbed query of the most recent
+ * wsvd_append_token / wsvd_fused_decode_step on this cache (no append):
+ * out [batch][n_heads][H].  Used to time the dominant kernel in isolation. */
+int wsvd_decode_attention(wsvd_cache_t cache, float* out, void* stream);
 /* One attention-layer decode step for every sequence (pipeline.cpp:320-329):
  * append x, attend with that token's own query, O-project this shard's
  * heads.  y [batch][e_out] fp32 = this shard's partial sum (complete when

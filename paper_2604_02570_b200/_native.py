@@ -52,6 +52,7 @@ SIGNATURES = {
     "wsvd_append_token": (C.c_int, [_vp, _fp, _fp, _vp]),
     "wsvd_prefill": (C.c_int, [_vp, _fp, _i32, _vp]),
     "wsvd_fused_decode_step": (C.c_int, [_vp, _fp, _i32, _fp, _vp]),
+    "wsvd_decode_attention": (C.c_int, [_vp, _fp, _vp]),
     "wsvd_layer_step": (C.c_int, [_vp, _fp, _fp, _fp, _vp]),
     "wsvd_layer_step_host": (C.c_int, [_vp, _fp, _fp, _vp]),
     "wsvd_layer_step_graph": (C.c_int, [_vp, _fp, _fp, _vp]),

@@ -127,7 +127,9 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
 
     // ---- cache append: row [C_K | C_V] at position pos
     const size_t bh = static_cast<size_t>(b) * a.nh + h;
-    uint8_t* row = a.cache + (bh * a.cap + pos) * a.row_bytes;
+    // rows live inside the (sequence, head) region with the 16-byte XOR swizzle
+    uint8_t* region = a.cache + bh * a.cap * a.row_bytes;
+    const uint32_t row0 = static_cast<uint32_t>(pos) * a.row_bytes;
     if (a.cdtype == I8) {
         // per (token, head, role) scale: f16(max|c| / 127), 1 when it is 0
         const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -146,17 +148,17 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
                 hs = __float2half_rn(1.f);
                 s = 1.f;
             }
-            int8_t* dst = reinterpret_cast<int8_t*>(row) + warp * R;
             for (int i = lane; i < R; i += 32)
-                dst[i] = static_cast<int8_t>(fminf(fmaxf(roundf(__fdiv_rn(src[i], s)), -127.f), 127.f));
+                reinterpret_cast<int8_t*>(region)[cache_swz(row0 + warp * R + i)] =
+                    static_cast<int8_t>(fminf(fmaxf(roundf(__fdiv_rn(src[i], s)), -127.f), 127.f));
             if (lane == 0) reinterpret_cast<__half*>(a.cscale + bh * a.cap + pos)[warp] = hs;
         }
     } else if (a.cdtype == BF16) {
-        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(row);
-        for (int i = threadIdx.x; i < 2 * R; i += kEpThreads) dst[i] = __float2bfloat16_rn(c[R + i]);
+        for (int i = threadIdx.x; i < 2 * R; i += kEpThreads)
+            *reinterpret_cast<__nv_bfloat16*>(region + cache_swz(row0 + 2 * i)) = __float2bfloat16_rn(c[R + i]);
     } else {
-        float* dst = reinterpret_cast<float*>(row);
-        for (int i = threadIdx.x; i < 2 * R; i += kEpThreads) dst[i] = c[R + i];
+        for (int i = threadIdx.x; i < 2 * R; i += kEpThreads)
+            *reinterpret_cast<float*>(region + cache_swz(row0 + 4 * i)) = c[R + i];
     }
 
     // ---- query: q_h = c_Q . B_Q (decode.cpp:140), then the absorbed key side
@@ -185,6 +187,19 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
             __threadfence();
         }
     }
+}
+
+// rows [n][row_bytes] (logical order) -> cache row `pos` of regions 0..n-1
+__global__ void push_rows_kernel(const uint8_t* __restrict__ rows, int n, uint8_t* cache, int cap,
+                                 int row_bytes, int pos) {
+    const int units = row_bytes / 16;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n * units) return;
+    const int r = i / units, u = i - r * units;
+    uint8_t* region = cache + static_cast<size_t>(r) * cap * row_bytes;
+    const uint32_t off = static_cast<uint32_t>(pos) * row_bytes + u * 16;
+    *reinterpret_cast<uint4*>(region + cache_swz(off)) =
+        *reinterpret_cast<const uint4*>(rows + static_cast<size_t>(r) * row_bytes + u * 16);
 }
 
 __global__ void __launch_bounds__(kEpThreads) absorb_query_kernel(const float* __restrict__ q, int nh,
@@ -218,6 +233,13 @@ cudaError_t launch_append_epilogue(const AppendArgs& a, cudaStream_t s) {
     const int smem = (3 * a.R + a.H) * 4;
     dim3 grid(a.nh, a.M);
     append_epilogue_kernel<<<grid, kEpThreads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_push_rows(const uint8_t* rows, int n, uint8_t* cache, int cap, int row_bytes,
+                             int pos, cudaStream_t s) {
+    const int total = n * (row_bytes / 16);
+    push_rows_kernel<<<(total + 255) / 256, 256, 0, s>>>(rows, n, cache, cap, row_bytes, pos);
     return cudaGetLastError();
 }
 

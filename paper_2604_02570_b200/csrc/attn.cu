@@ -5,7 +5,7 @@
 // at L*r*H MACs per head.  Scores only need q . key_j, so this kernel uses
 // the algebraically identical absorbed query qt = q . B_K^T (r values,
 // computed once per (sequence, head) by the append epilogue or
-// launch_absorb_query) and streams the latent rows once:
+// launch_absorb_query) and streams every latent row exactly once:
 //
 //   s_j   = qt . C_K[j]                      (log2 domain, 1/sqrt(H) folded in)
 //   state = online softmax over s_j with the accumulator in latent-V space
@@ -15,17 +15,28 @@
 // Results equal the reference up to floating-point reassociation.
 //
 // HBM layout: cache[b][h][t][ C_K(R) | C_V(R) ] (one row per token, R = padded
-// rank), int8 rows carry a half2 (s_K, s_V) scale per token in a parallel
-// array.  Work is split into units (sequence, head, chunk of `chunk` tokens);
-// a persistent grid walks the units round-robin.  Per CTA, one thread keeps a
-// ring of TMA bulk copies (cp.async.bulk + mbarrier complete_tx) of
-// 128-token stages in flight across unit boundaries while 4 warps consume:
-// one token per thread per stage, warp-uniform running max, per-lane
-// accumulators.  At a unit's end the CTA reduces its 128 partial states and
-// either finalises (single chunk) or publishes a partial (m, l, acc[R]); the
-// last CTA to finish a (sequence, head) merges the partials in chunk order
-// (SoftmaxState::merge, decode.cpp:59-75) and applies B_V -- the split-KV
-// combine is fused, deterministic and needs no second launch.
+// rank), XOR-swizzled in 16-byte units (cache_swz, common.cuh); int8 rows carry
+// a half2 (s_K, s_V) per token in a parallel array.  Work units are
+// (sequence, head, chunk of `chunk` tokens); a persistent grid of one CTA per
+// SM walks them round-robin.  Warp specialisation: one producer warp keeps a
+// ring of TMA bulk copies (cp.async.bulk, completion via mbarrier complete_tx)
+// of 256-token stages in flight across unit boundaries -- including the
+// unit's absorbed query row -- while 8 consumer warps drain them and hand
+// slots back through `empty` mbarriers; no CTA-wide barrier sits in the
+// streaming loop.
+//
+// bf16 caches (the production format) run both contractions of a 16-token
+// group on the tensor cores with mma.sync m16n8k16: scores = K_tile . [qt_hi |
+// qt_lo] and acc += V_tile^T . [p_hi | p_lo], where x_hi = bf16(x) and
+// x_lo = bf16(x - x_hi) keep ~16 significant bits of the fp32 query and
+// probabilities (the cache operand is exact bf16, products and sums are fp32).
+// fp32 and int8 caches use a CUDA-core path (one token per thread).
+//
+// At a unit's end every consumer warp publishes its own partial state
+// (m, l, acc[R]) -- no CTA-wide or grid-wide synchronisation anywhere in the
+// streaming kernel.  A small combine kernel then merges each (sequence, head)'s
+// partials in a fixed order (SoftmaxState::merge, decode.cpp:59-75) and
+// applies B_V once; results are run-to-run deterministic.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -35,8 +46,10 @@ namespace wsvd_k {
 
 namespace {
 
-constexpr int kThreads = 128;
-constexpr int kStageTok = 128;
+constexpr int kConsumerWarps = 8;
+constexpr int kConsumers = 32 * kConsumerWarps;
+constexpr int kThreads = kConsumers + 32;  // + one producer warp
+constexpr int kStageTok = kConsumers;      // 256 tokens per stage
 
 template <int CD, int R>
 struct Cfg {
@@ -45,23 +58,23 @@ struct Cfg {
     static constexpr int PART = R * EB;        // bytes of the K (and V) half
     static constexpr int NC = PART / 16;       // chunks per half
     static constexpr int ROWB = 2 * PART;
-    static constexpr bool POW2 = (NC & (NC - 1)) == 0;
-    // per-lane rotation of the chunk order keeps ld.shared.v4 at <= 2-way bank
-    // conflicts for rows that are multiples of 128 B (or 64 B)
-    static constexpr bool ROT = POW2 && NC > 1 && (ROWB % 64 == 0);
-    static constexpr int ROT_SHIFT = ROWB >= 128 ? 0 : 1;
+    static constexpr bool MMA = (CD == BF16);
+    static constexpr int ROWS = kStageTok * ROWB;
     static constexpr int SC = (CD == I8) ? 4 * kStageTok : 0;
-    static constexpr int STAGE = kStageTok * ROWB + SC;
+    static constexpr int QT_OFF = ROWS + SC;   // absorbed query of the unit (first stage)
+    static constexpr int STAGE = QT_OFF + 256;
     static constexpr int RSTRIDE = R + 4;      // floats per lane row of the reduction scratch
-    static constexpr int RED = 4 * 32 * RSTRIDE * 4;
-    static constexpr int BUDGET = 110 * 1024;
-    static constexpr int ST_RAW = (BUDGET - RED - 2048) / STAGE;
-    static constexpr int STAGES = ST_RAW > 8 ? 8 : (ST_RAW < 2 ? 2 : ST_RAW);
+    static constexpr int RED = MMA ? 0 : kConsumerWarps * 32 * RSTRIDE * 4;
+    static constexpr int BUDGET = 222 * 1024;
+    static constexpr int ST_RAW = (BUDGET - RED - 4096) / STAGE;
+    static constexpr int STAGES = ST_RAW > 8 ? 8 : ST_RAW;
     static constexpr int BAR_OFF = STAGES * STAGE;
-    static constexpr int RED_OFF = BAR_OFF + 128;
-    static constexpr int MISC_OFF = RED_OFF + RED;                  // wpart[4][R+2], vt[R]
-    static constexpr int SMEM = MISC_OFF + (4 * (R + 2) + R + 8) * 4;
+    static constexpr int RED_OFF = BAR_OFF + 256;
+    static constexpr int MISC_OFF = RED_OFF + RED;
+    static constexpr bool OK = ST_RAW >= 2;         // f32 rows of R > 32 do not fit two stages
+    static constexpr int SMEM = OK ? MISC_OFF : 0;
     static_assert(PART % 16 == 0, "latent half must be a multiple of 16 bytes");
+    static_assert(R * 4 <= 256, "query row must fit the stage's query area");
 };
 
 WSVD_DEV float ex2(float x) {
@@ -103,6 +116,14 @@ WSVD_DEV float load_b(const void* b, int bdtype, size_t idx) {
     return static_cast<float>(reinterpret_cast<const int8_t*>(b)[idx]);
 }
 
+// x -> (bf16(x), bf16(x - bf16(x))) as raw 16-bit patterns
+WSVD_DEV void split_bf16(float x, uint32_t& hi, uint32_t& lo) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    const __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
+    hi = *reinterpret_cast<const uint16_t*>(&h);
+    lo = *reinterpret_cast<const uint16_t*>(&l);
+}
+
 struct Unit {
     int bh, chunk, t0, ntok;
 };
@@ -116,16 +137,27 @@ WSVD_DEV Unit unit_geom(int u, int nch, int chunk, int len) {
     return g;
 }
 
+// ----------------------------------------------------------------------------
+// Consumer state of one warp over one unit, tensor-core variant (bf16 cache).
+// Per 16-token group g16: D_s(16 x 8) = K(16 x R) . Q(R x 8), Q's columns
+// 0/1 = qt_hi/qt_lo, so a lane with t = lane%4 == 0 holds the scores of tokens
+// g and g+8 (g = lane/4) as d0+d1 and d2+d3.  P(16 tok x 8) has columns 0/1 =
+// p_hi/p_lo; acc(R x 8) += V^T(R x 16) . P accumulates in MMA D fragments.
+template <int R>
+struct MmaState {
+    static constexpr int KR = R / 16;
+    uint32_t qf[KR][2];  // B fragments of [qt_hi | qt_lo]
+    float acc[KR][4];    // D fragments of V^T . P
+};
+
 template <int CD, int R>
-__global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const AttnArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs a) {
     using C = Cfg<CD, R>;
     constexpr int NC = C::NC, EPC = C::EPC;
     extern __shared__ __align__(128) uint8_t smem[];
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    uint64_t* empty = full + C::STAGES;
     float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
-    float* wpart = reinterpret_cast<float*>(smem + C::MISC_OFF);  // [4][R+2]
-    float* vt = wpart + 4 * (R + 2);                               // [R]
-    int* sflag = reinterpret_cast<int*>(vt + R);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int len = *a.d_len;
@@ -134,223 +166,318 @@ __global__ void __launch_bounds__(kThreads, 2) decode_attn_kernel(const AttnArgs
     const int n_units = a.B * a.nh * nch;
     const size_t cap = static_cast<size_t>(a.cap);
 
+    // Zero the stage ring once: rows past a stage's valid end are read by the
+    // MMAs (times p = 0) and must hold finite values.
+    for (int i = tid; i < C::STAGES * C::STAGE / 16; i += kThreads)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (tid == 0) {
-        for (int i = 0; i < C::STAGES; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < C::STAGES; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], kConsumerWarps);
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
-    // ---------------- producer cursor (thread 0 only)
-    int pu = blockIdx.x, ps = 0, pslot = 0;
-    const uint64_t pol = policy_evict_first();
-    auto issue_next = [&]() {
-        // load the next stage of this CTA's unit sequence into pslot
-        if (pu >= n_units) return;
-        const Unit g = unit_geom(pu, nch, a.chunk, len);
-        const int t = g.t0 + ps * kStageTok;
-        const int rows = min(kStageTok, g.ntok - ps * kStageTok);
-        uint8_t* dst = smem + pslot * C::STAGE;
-        const uint32_t rbytes = static_cast<uint32_t>(rows * C::ROWB);
-        uint32_t sbytes = 0;
-        if (CD == I8) sbytes = static_cast<uint32_t>((rows * 4 + 15) & ~15);
-        mbar_arrive_expect_tx(&bars[pslot], rbytes + sbytes);
-        const uint8_t* src = a.cache + (static_cast<size_t>(g.bh) * cap + t) * C::ROWB;
-        tma_bulk_g2s_stream(dst, src, rbytes, &bars[pslot], pol);
-        if (CD == I8) {
-            const __half2* ssrc = a.cscale + static_cast<size_t>(g.bh) * cap + t;
-            tma_bulk_g2s_stream(dst + kStageTok * C::ROWB, ssrc, sbytes, &bars[pslot], pol);
+    // ======================================================== producer warp
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int slot = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const Unit g = unit_geom(u, nch, a.chunk, len);
+                const uint8_t* src = a.cache + (static_cast<size_t>(g.bh) * cap + g.t0) * C::ROWB;
+                const __half2* ssrc = a.cscale + static_cast<size_t>(g.bh) * cap + g.t0;
+                for (int s = 0; s * kStageTok < g.ntok; ++s) {
+                    const int rows = min(kStageTok, g.ntok - s * kStageTok);
+                    // whole 16-byte units; the swizzle only permutes within 1 KB blocks,
+                    // so copy the covering blocks (rows past the end are masked)
+                    const uint32_t rbytes = static_cast<uint32_t>(min(kStageTok * C::ROWB, ((rows * C::ROWB + 1023) / 1024) * 1024));
+                    const uint32_t sbytes = (CD == I8) ? static_cast<uint32_t>((rows * 4 + 15) & ~15) : 0u;
+                    const uint32_t qbytes = (s == 0) ? static_cast<uint32_t>(R * 4) : 0u;
+                    mbar_wait(&empty[slot], phase ^ 1u);
+                    uint8_t* dst = smem + slot * C::STAGE;
+                    mbar_arrive_expect_tx(&full[slot], rbytes + sbytes + qbytes);
+                    tma_bulk_g2s_stream(dst, src + static_cast<size_t>(s) * kStageTok * C::ROWB, rbytes,
+                                        &full[slot], pol);
+                    if (CD == I8)
+                        tma_bulk_g2s_stream(dst + C::ROWS, ssrc + s * kStageTok, sbytes, &full[slot], pol);
+                    if (s == 0)
+                        tma_bulk_g2s(dst + C::QT_OFF, a.qt + static_cast<size_t>(g.bh) * R, qbytes, &full[slot]);
+                    if (++slot == C::STAGES) {
+                        slot = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
         }
-        pslot = (pslot + 1 == C::STAGES) ? 0 : pslot + 1;
-        if (++ps * kStageTok >= g.ntok) {
-            ps = 0;
-            pu += gridDim.x;
-        }
-    };
-    if (tid == 0)
-        for (int i = 0; i < C::STAGES; ++i) issue_next();
+        return;
+    }
 
-    // ---------------- per-lane chunk rotation
-    const int rot = C::ROT ? ((lane >> C::ROT_SHIFT) & (NC - 1)) : 0;
-    uint32_t koff[NC];
-#pragma unroll
-    for (int c = 0; c < NC; ++c) koff[c] = static_cast<uint32_t>(((c + rot) % NC) * 16);
-
-    int cslot = 0;
+    // ====================================================== consumer warps
+    const int g8 = lane >> 2, t4 = lane & 3;
+    int slot = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const Unit g = unit_geom(u, nch, a.chunk, len);
-
-        // absorbed query chunks in this lane's rotated order
-        float qr[NC][EPC];
-        const float* qsrc = a.qt + static_cast<size_t>(g.bh) * R;
-#pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            const float4* p4 = reinterpret_cast<const float4*>(qsrc + (koff[c] / 16) * EPC);
-#pragma unroll
-            for (int e = 0; e < EPC / 4; ++e) {
-                const float4 v = __ldg(p4 + e);
-                qr[c][4 * e] = v.x; qr[c][4 * e + 1] = v.y;
-                qr[c][4 * e + 2] = v.z; qr[c][4 * e + 3] = v.w;
-            }
-        }
-        float acc[NC][EPC];
-#pragma unroll
-        for (int c = 0; c < NC; ++c)
-#pragma unroll
-            for (int e = 0; e < EPC; ++e) acc[c][e] = 0.f;
         float m_w = -INFINITY, l = 0.f;
-
         const int ns = (g.ntok + kStageTok - 1) / kStageTok;
-        for (int s = 0; s < ns; ++s) {
-            mbar_wait(&bars[cslot], phase);
-            const uint8_t* st = smem + cslot * C::STAGE;
-            const int rows = min(kStageTok, g.ntok - s * kStageTok);
-            const bool valid = tid < rows;
-            const uint32_t row = smem_u32(st) + static_cast<uint32_t>(tid * C::ROWB);
+        float wacc[2 * (R / 16 > 0 ? R / 16 : 1)];  // MMA path: this lane's acc rows (t4 == 0)
 
-            float sk = 1.f, sv = 1.f;
-            if (CD == I8) {
-                const __half2 sc = reinterpret_cast<const __half2*>(st + kStageTok * C::ROWB)[tid];
-                sk = __low2float(sc);
-                sv = __high2float(sc);
+        if constexpr (C::MMA) {
+            constexpr int KR = R / 16;
+            MmaState<R> st;
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) st.acc[kk][i] = 0.f;
+            for (int s = 0; s < ns; ++s) {
+                mbar_wait(&full[slot], phase);
+                const uint8_t* sp = smem + slot * C::STAGE;
+                const uint32_t sbase = smem_u32(sp);
+                if (s == 0) {
+                    const float* q = reinterpret_cast<const float*>(sp + C::QT_OFF);
+#pragma unroll
+                    for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const int k0 = kk * 16 + 2 * t4 + 8 * j;
+                            uint32_t h0, l0, h1, l1;
+                            split_bf16(q[k0], h0, l0);
+                            split_bf16(q[k0 + 1], h1, l1);
+                            st.qf[kk][j] = (g8 == 0) ? (h0 | (h1 << 16)) : (g8 == 1 ? (l0 | (l1 << 16)) : 0u);
+                        }
+                }
+                const int rows = min(kStageTok, g.ntok - s * kStageTok);
+                // ---- scores of the warp's 2 groups of 16 tokens
+                float sc[2][2];
+#pragma unroll
+                for (int grp = 0; grp < 2; ++grp) {
+                    const int tb = warp * 32 + grp * 16;
+                    float d[4] = {0.f, 0.f, 0.f, 0.f};
+                    const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+                    for (int kk = 0; kk < KR; ++kk) {
+                        uint32_t a0, a1, a2, a3;
+                        const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
+                        ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
+                        mma_bf16_16816(d, a0, a1, a2, a3, st.qf[kk][0], st.qf[kk][1]);
+                    }
+                    const bool v0 = (t4 == 0) && (tb + g8 < rows);
+                    const bool v1 = (t4 == 0) && (tb + g8 + 8 < rows);
+                    sc[grp][0] = v0 ? d[0] + d[1] : -INFINITY;
+                    sc[grp][1] = v1 ? d[2] + d[3] : -INFINITY;
+                }
+                // ---- online softmax, warp-uniform running max (exp2 domain)
+                const float wm = warp_max(fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])));
+                if (wm > m_w) {
+                    const float f = ex2(m_w - wm);
+                    l *= f;
+#pragma unroll
+                    for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) st.acc[kk][i] *= f;
+                    m_w = wm;
+                }
+#pragma unroll
+                for (int grp = 0; grp < 2; ++grp) {
+                    const int tb = warp * 32 + grp * 16;
+                    const float p0 = (sc[grp][0] == -INFINITY) ? 0.f : ex2(sc[grp][0] - m_w);
+                    const float p1 = (sc[grp][1] == -INFINITY) ? 0.f : ex2(sc[grp][1] - m_w);
+                    l += p0 + p1;
+                    uint32_t h0, l0, h1, l1;
+                    split_bf16(p0, h0, l0);
+                    split_bf16(p1, h1, l1);
+                    const uint32_t hi2 = h0 | (h1 << 16), lo2 = l0 | (l1 << 16);
+                    // P fragment: lane (g8 in {0,1}, t4) needs p of tokens 2t4, 2t4+1 (+8)
+                    const int s0 = 8 * t4, s1 = 8 * t4 + 4;
+                    const uint32_t xh = __shfl_sync(0xffffffffu, hi2, s0), yh = __shfl_sync(0xffffffffu, hi2, s1);
+                    const uint32_t xl = __shfl_sync(0xffffffffu, lo2, s0), yl = __shfl_sync(0xffffffffu, lo2, s1);
+                    const uint32_t x = (g8 == 0) ? xh : xl, y = (g8 == 0) ? yh : yl;
+                    const uint32_t b0 = (g8 < 2) ? __byte_perm(x, y, 0x5410) : 0u;
+                    const uint32_t b1 = (g8 < 2) ? __byte_perm(x, y, 0x7632) : 0u;
+                    const int stok = tb + (lane & 7) + ((lane >> 4) & 1) * 8;
+#pragma unroll
+                    for (int mm = 0; mm < KR; ++mm) {
+                        uint32_t a0, a1, a2, a3;
+                        const uint32_t off = static_cast<uint32_t>(stok * C::ROWB + C::PART + (mm * 2 + ((lane >> 3) & 1)) * 16);
+                        ldsm_x4_trans(sbase + cache_swz(off), a0, a1, a2, a3);
+                        mma_bf16_16816(st.acc[mm], a0, a1, a2, a3, b0, b1);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                if (++slot == C::STAGES) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
             }
-            // ---- score: qt . C_K[t]
-            float sacc[2] = {0.f, 0.f};
 #pragma unroll
-            for (int c = 0; c < NC; ++c) {
-                float f[EPC];
-                chunk_to_f32<CD>(lds128(row + koff[c]), f);
-#pragma unroll
-                for (int e = 0; e < EPC; ++e) sacc[e & 1] = fmaf(qr[c][e], f[e], sacc[e & 1]);
+            for (int mm = 0; mm < KR; ++mm) {
+                wacc[2 * mm] = st.acc[mm][0] + st.acc[mm][1];      // r = mm*16 + g8
+                wacc[2 * mm + 1] = st.acc[mm][2] + st.acc[mm][3];  // r = mm*16 + g8 + 8
             }
-            const float sc = valid ? (sacc[0] + sacc[1]) * sk : -INFINITY;
-
-            // ---- online softmax, warp-uniform running max (exp2 domain)
-            const float wm = warp_max(sc);
-            if (wm > m_w) {
-                const float f = ex2(m_w - wm);
-                l *= f;
+            const float lsum = warp_sum(l);
+            float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kConsumerWarps + warp) * (R + 2);
+            if (t4 == 0) {
 #pragma unroll
-                for (int c = 0; c < NC; ++c)
-#pragma unroll
-                    for (int e = 0; e < EPC; ++e) acc[c][e] *= f;
-                m_w = wm;
+                for (int mm = 0; mm < KR; ++mm) {
+                    wsp[mm * 16 + g8] = wacc[2 * mm];
+                    wsp[mm * 16 + g8 + 8] = wacc[2 * mm + 1];
+                }
             }
-            const float p = valid ? ex2(sc - m_w) : 0.f;
-            l += p;
-            // ---- latent-V accumulate (rows past the stage end hold stale smem)
-            if (valid) {
-                const float pv = p * sv;
+            if (lane == 0) {
+                wsp[R] = m_w;
+                wsp[R + 1] = lsum;
+            }
+        } else {
+            // ------------------------------------------ CUDA-core path (f32, int8)
+            float qr[NC][EPC];
+            float acc[NC][EPC];
+#pragma unroll
+            for (int c = 0; c < NC; ++c)
+#pragma unroll
+                for (int e = 0; e < EPC; ++e) acc[c][e] = 0.f;
+            for (int s = 0; s < ns; ++s) {
+                mbar_wait(&full[slot], phase);
+                const uint8_t* sp = smem + slot * C::STAGE;
+                if (s == 0) {
+                    const float* q = reinterpret_cast<const float*>(sp + C::QT_OFF);
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+#pragma unroll
+                        for (int e = 0; e < EPC; ++e) qr[c][e] = q[c * EPC + e];
+                }
+                const int rows = min(kStageTok, g.ntok - s * kStageTok);
+                const bool valid = tid < rows;
+                const uint32_t sbase = smem_u32(sp);
+                const uint32_t rlog = static_cast<uint32_t>(tid * C::ROWB);
+                float sk = 1.f, sv = 1.f;
+                if (CD == I8) {
+                    const __half2 scv = reinterpret_cast<const __half2*>(sp + C::ROWS)[tid];
+                    sk = __low2float(scv);
+                    sv = __high2float(scv);
+                }
+                float sacc[2] = {0.f, 0.f};
 #pragma unroll
                 for (int c = 0; c < NC; ++c) {
                     float f[EPC];
-                    chunk_to_f32<CD>(lds128(row + C::PART + koff[c]), f);
+                    chunk_to_f32<CD>(lds128(sbase + cache_swz(rlog + c * 16)), f);
 #pragma unroll
-                    for (int e = 0; e < EPC; ++e) acc[c][e] = fmaf(pv, f[e], acc[c][e]);
+                    for (int e = 0; e < EPC; ++e) sacc[e & 1] = fmaf(qr[c][e], f[e], sacc[e & 1]);
+                }
+                const float scv = valid ? (sacc[0] + sacc[1]) * sk : -INFINITY;
+                const float wm = warp_max(scv);
+                if (wm > m_w) {
+                    const float f = ex2(m_w - wm);
+                    l *= f;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c)
+#pragma unroll
+                        for (int e = 0; e < EPC; ++e) acc[c][e] *= f;
+                    m_w = wm;
+                }
+                if (valid) {
+                    const float p = ex2(scv - m_w);
+                    l += p;
+                    const float pv = p * sv;
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) {
+                        float f[EPC];
+                        chunk_to_f32<CD>(lds128(sbase + cache_swz(rlog + C::PART + c * 16)), f);
+#pragma unroll
+                        for (int e = 0; e < EPC; ++e) acc[c][e] = fmaf(pv, f[e], acc[c][e]);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[slot]);
+                if (++slot == C::STAGES) {
+                    slot = 0;
+                    phase ^= 1u;
                 }
             }
-
-            __syncthreads();  // slot fully consumed
-            if (tid == 0) issue_next();
-            cslot = (cslot + 1 == C::STAGES) ? 0 : cslot + 1;
-            if (cslot == 0) phase ^= 1u;
-        }
-
-        // ---- reduce 32 lanes: transpose through shared memory
-        float* wr = red + warp * 32 * C::RSTRIDE;
+            // reduce 32 lanes through a shared-memory transpose
+            float* wr = red + warp * 32 * C::RSTRIDE;
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
+            for (int c = 0; c < NC; ++c)
 #pragma unroll
-            for (int e = 0; e < EPC; e += 4) {
-                float4 v = make_float4(acc[c][e], acc[c][e + 1], acc[c][e + 2], acc[c][e + 3]);
-                *reinterpret_cast<float4*>(wr + lane * C::RSTRIDE + (koff[c] / 16) * EPC + e) = v;
-            }
-        const float lsum = warp_sum(l);
-        __syncwarp();
-        for (int j = lane; j < R; j += 32) {
-            float s = 0.f;
+                for (int e = 0; e < EPC; e += 4)
+                    *reinterpret_cast<float4*>(wr + lane * C::RSTRIDE + c * EPC + e) =
+                        make_float4(acc[c][e], acc[c][e + 1], acc[c][e + 2], acc[c][e + 3]);
+            const float lsum = warp_sum(l);
+            float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kConsumerWarps + warp) * (R + 2);
+            for (int j = lane; j < R; j += 32) {
+                float sum = 0.f;
 #pragma unroll 8
-            for (int r = 0; r < 32; ++r) s += wr[r * C::RSTRIDE + j];
-            wpart[warp * (R + 2) + j] = s;
-        }
-        if (lane == 0) {
-            wpart[warp * (R + 2) + R] = m_w;
-            wpart[warp * (R + 2) + R + 1] = lsum;
-        }
-        __syncthreads();
-
-        // ---- merge the 4 warps
-        float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, wpart[w * (R + 2) + R]);
-        float fw[4], L = 0.f;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            const float mw = wpart[w * (R + 2) + R];
-            fw[w] = (mw == -INFINITY) ? 0.f : ex2(mw - M);
-            L = fmaf(wpart[w * (R + 2) + R + 1], fw[w], L);
-        }
-        float accj = 0.f;
-        if (tid < R) {
-#pragma unroll
-            for (int w = 0; w < 4; ++w) accj = fmaf(wpart[w * (R + 2) + tid], fw[w], accj);
-        }
-
-        bool finalize = true;
-        if (nch > 1) {
-            float* wsu = a.ws + (static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * (R + 2);
-            if (tid < R) wsu[tid] = accj;
-            if (tid == R) wsu[R] = M;
-            if (tid == R + 1) wsu[R + 1] = L;
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) *sflag = (atomicAdd(&a.counters[g.bh], 1) == nch - 1);
-            __syncthreads();
-            finalize = *sflag != 0;
-            if (finalize) {
-                __threadfence();
-                const float* wsb = a.ws + static_cast<size_t>(g.bh) * a.max_chunks * (R + 2);
-                M = -INFINITY;
-                for (int c = 0; c < nch; ++c) M = fmaxf(M, __ldcg(wsb + c * (R + 2) + R));
-                L = 0.f;
-                accj = 0.f;
-                for (int c = 0; c < nch; ++c) {
-                    const float f = ex2(__ldcg(wsb + c * (R + 2) + R) - M);
-                    L = fmaf(__ldcg(wsb + c * (R + 2) + R + 1), f, L);
-                    if (tid < R) accj = fmaf(__ldcg(wsb + c * (R + 2) + tid), f, accj);
-                }
-                if (tid == 0) a.counters[g.bh] = 0;
+                for (int r = 0; r < 32; ++r) sum += wr[r * C::RSTRIDE + j];
+                wsp[j] = sum;
             }
-        }
-        if (finalize) {
-            // latent output, then one B_V up-projection (decode.cpp:198-203)
-            if (tid < R) vt[tid] = accj / L;
-            __syncthreads();
-            const int h = g.bh % a.nh;
-            const size_t bvo = static_cast<size_t>(h) * R * a.H;
-            for (int col = tid; col < a.H; col += kThreads) {
-                float o = 0.f;
-                for (int j = 0; j < R; ++j) o = fmaf(vt[j], load_b(a.bv, a.bdtype, bvo + j * a.H + col), o);
-                if (a.bdtype == I8) o *= a.bv_scale[h * a.H + col];
-                a.out[static_cast<size_t>(g.bh) * a.H + col] = o;
+            if (lane == 0) {
+                wsp[R] = m_w;
+                wsp[R + 1] = lsum;
             }
+            __syncwarp();  // scratch reuse by the next unit
         }
-        __syncthreads();  // scratch reuse by the next unit
+        (void)wacc;
+        // each warp published its own partial (m, l, acc[R]); no CTA-wide sync
+    }
+}
+
+// Split-KV combine (SoftmaxState::merge, decode.cpp:59-75, over the chunk x
+// warp partials in a fixed order) and the single B_V up-projection per head
+// (decode.cpp:198-203).  One CTA per (sequence, head).
+__global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a, int parts_per_chunk) {
+    extern __shared__ float vt[];  // [R]
+    const int bh = blockIdx.x, tid = threadIdx.x, R = a.R;
+    const int len = *a.d_len;
+    if (len <= 0) return;
+    const int nch = (len + a.chunk - 1) / a.chunk;
+    const int np = nch * parts_per_chunk;
+    const float* wsb = a.ws + static_cast<size_t>(bh) * a.max_chunks * parts_per_chunk * (R + 2);
+    float M = -INFINITY;
+    for (int p = 0; p < np; ++p) M = fmaxf(M, wsb[p * (R + 2) + R]);
+    float L = 0.f, acc = 0.f;
+    for (int p = 0; p < np; ++p) {
+        const float m = wsb[p * (R + 2) + R];
+        if (m == -INFINITY) continue;  // a warp that saw no token of its chunk
+        const float f = ex2(m - M);
+        L = fmaf(wsb[p * (R + 2) + R + 1], f, L);
+        if (tid < R) acc = fmaf(wsb[p * (R + 2) + tid], f, acc);
+    }
+    if (tid < R) vt[tid] = acc / L;
+    __syncthreads();
+    const int h = bh % a.nh;
+    const size_t bvo = static_cast<size_t>(h) * R * a.H;
+    for (int col = tid; col < a.H; col += blockDim.x) {
+        float o = 0.f;
+#pragma unroll 8
+        for (int j = 0; j < R; ++j) o = fmaf(vt[j], load_b(a.bv, a.bdtype, bvo + j * a.H + col), o);
+        if (a.bdtype == I8) o *= a.bv_scale[h * a.H + col];
+        a.out[static_cast<size_t>(bh) * a.H + col] = o;
     }
 }
 
 template <int CD, int R>
 cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
     using C = Cfg<CD, R>;
-    auto k = decode_attn_kernel<CD, R>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    if constexpr (!C::OK) {
+        return cudaErrorInvalidValue;
+    } else {
+        auto k = decode_attn_kernel<CD, R>;
+        static bool attr_set = false;
+        if (!attr_set) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            if (e != cudaSuccess) return e;
+            attr_set = true;
+        }
+        k<<<a.grid, kThreads, C::SMEM, s>>>(a);
+        cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        attr_set = true;
+        attn_combine_kernel<<<a.B * a.nh, 128, R * 4, s>>>(a, kConsumerWarps);
+        return cudaGetLastError();
     }
-    k<<<a.grid, kThreads, C::SMEM, s>>>(a);
-    return cudaGetLastError();
 }
 
 template <int CD>
@@ -386,12 +513,10 @@ int attn_smem_bytes(int cdtype, int R) {
     return 0;
 }
 
+int attn_parts_per_chunk() { return kConsumerWarps; }
+
 int attn_occupancy(int cdtype, int R) {
-    const int sm = attn_smem_bytes(cdtype, R);
-    if (sm <= 0) return 0;
-    int occ = (227 * 1024) / (sm + 1024);
-    if (occ > 2) occ = 2;  // __launch_bounds__(128, 2)
-    return occ < 1 ? 1 : occ;
+    return attn_smem_bytes(cdtype, R) > 0 ? 1 : 0;  // persistent: one CTA per SM
 }
 
 cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s) {

@@ -41,6 +41,9 @@ int set_err(int code, const std::string& msg) {
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
 
+// host copy of cache_swz (common.cuh): the 16-byte XOR swizzle of cache rows
+uint32_t wsvd_dev_swz(uint32_t a) { return a ^ (((a >> 7) & 7u) << 4); }
+
 struct DevBuf {
     void* p = nullptr;
     size_t n = 0;
@@ -623,7 +626,7 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4);
     if (e == cudaSuccess) e = c->ctrl.alloc(64);
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
-    if (e == cudaSuccess) e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh * c->max_chunks * (L->R + 2) * 4);
+    if (e == cudaSuccess) e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh * c->max_chunks * attn_parts_per_chunk() * (L->R + 2) * 4);
     if (e == cudaSuccess) e = c->attn_cnt.alloc(static_cast<size_t>(batch) * nh * 4);
     if (e == cudaSuccess) e = c->attn_out.alloc(static_cast<size_t>(batch) * nh * H * 4);
     if (e != cudaSuccess) {
@@ -691,22 +694,27 @@ int wsvd_cache_push_host(wsvd_cache_t c, const double* ck, const double* cv) {
     if (c->cdtype == WSVD_I8) return set_err(WSVD_ECONFIG, "push_host supports F32/BF16 caches");
     CUDA_TRY(cudaSetDevice(L->d.device));
     CUDA_TRY(cudaDeviceSynchronize());
-    std::vector<uint8_t> row(c->row_bytes);
+    const int n = c->B * nh;
+    std::vector<uint8_t> rows(static_cast<size_t>(n) * c->row_bytes);
     for (int b = 0; b < c->B; ++b)
         for (int h = 0; h < nh; ++h) {
             const int rk = L->ranks[h * 3 + 1], rv = L->ranks[h * 3 + 2];
+            uint8_t* row = rows.data() + (static_cast<size_t>(b) * nh + h) * c->row_bytes;
             for (int i = 0; i < 2 * R; ++i) {
                 const bool kpart = i < R;
                 const int j = kpart ? i : i - R;
                 double v = 0.0;
                 if (kpart && j < rk) v = ck[(static_cast<size_t>(b) * nh + h) * R + j];
                 if (!kpart && j < rv) v = cv[(static_cast<size_t>(b) * nh + h) * R + j];
-                if (c->cdtype == WSVD_F32) reinterpret_cast<float*>(row.data())[i] = static_cast<float>(v);
-                else reinterpret_cast<uint16_t*>(row.data())[i] = f32_to_bf16_bits(static_cast<float>(v));
+                if (c->cdtype == WSVD_F32) reinterpret_cast<float*>(row)[i] = static_cast<float>(v);
+                else reinterpret_cast<uint16_t*>(row)[i] = f32_to_bf16_bits(static_cast<float>(v));
             }
-            const size_t off = ((static_cast<size_t>(b) * nh + h) * c->cap_alloc + c->len) * c->row_bytes;
-            CUDA_TRY(cudaMemcpy(c->data.as<uint8_t>() + off, row.data(), row.size(), cudaMemcpyHostToDevice));
         }
+    DevBuf tmp;
+    CUDA_TRY(tmp.alloc(rows.size()));
+    CUDA_TRY(cudaMemcpy(tmp.p, rows.data(), rows.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(launch_push_rows(tmp.as<uint8_t>(), n, c->data.as<uint8_t>(), c->cap_alloc, c->row_bytes, c->len, nullptr));
+    CUDA_TRY(cudaDeviceSynchronize());
     c->len += 1;
     CUDA_TRY(cudaMemcpy(c->d_len(), &c->len, 4, cudaMemcpyHostToDevice));
     return WSVD_OK;
@@ -719,8 +727,15 @@ int wsvd_cache_read_raw(wsvd_cache_t c, int32_t b, int32_t h, void* rows_host, u
     CUDA_TRY(cudaDeviceSynchronize());
     const size_t bh = static_cast<size_t>(b) * c->L->d.n_heads + h;
     if (c->len > 0) {
-        CUDA_TRY(cudaMemcpy(rows_host, c->data.as<uint8_t>() + bh * c->cap_alloc * c->row_bytes,
-                            static_cast<size_t>(c->len) * c->row_bytes, cudaMemcpyDeviceToHost));
+        // copy the covering 1 KB swizzle blocks, then undo the 16-byte XOR swizzle
+        const size_t used = static_cast<size_t>(c->len) * c->row_bytes;
+        const size_t span = std::min((used + 1023) / 1024 * 1024, static_cast<size_t>(c->cap_alloc) * c->row_bytes);
+        std::vector<uint8_t> raw(span);
+        CUDA_TRY(cudaMemcpy(raw.data(), c->data.as<uint8_t>() + bh * c->cap_alloc * c->row_bytes, span,
+                            cudaMemcpyDeviceToHost));
+        uint8_t* out = static_cast<uint8_t*>(rows_host);
+        for (size_t u = 0; u < used / 16; ++u)
+            std::memcpy(out + u * 16, raw.data() + wsvd_dev_swz(static_cast<uint32_t>(u * 16)), 16);
         if (scales_host && c->cdtype == WSVD_I8)
             CUDA_TRY(cudaMemcpy(scales_host, c->scales.as<uint8_t>() + bh * c->cap_alloc * 4,
                                 static_cast<size_t>(c->len) * 4, cudaMemcpyDeviceToHost));
@@ -812,6 +827,13 @@ int wsvd_fused_decode_step(wsvd_cache_t c, const float* q, int32_t tile_len, flo
                                  L->bdtype, 1.4426950408889634f / std::sqrt(static_cast<float>(L->d.head_dim)),
                                  c->qt.as<float>(), s));
     return run_attention(c, out, s);
+}
+
+int wsvd_decode_attention(wsvd_cache_t c, float* out, void* stream) {
+    if (!c || !out) return set_err(WSVD_ECONFIG, "null argument");
+    if (c->len == 0) return set_err(WSVD_ESHAPE, "decode step over an empty cache");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    return run_attention(c, out, static_cast<cudaStream_t>(stream));
 }
 
 int wsvd_layer_step(wsvd_cache_t c, const float* x, float* attn_out, float* y, void* stream) {

@@ -37,6 +37,16 @@ WSVD_DEV void unpack_s4x8(uint32_t w, uint32_t& lo4, uint32_t& hi4) {
     hi4 = __byte_perm(even, odd, 0x7362);   // e2 o2 e3 o3 -> elements 4..7
 }
 
+// ---------------------------------------------------------- cache swizzle
+// Latent-cache rows are stored with the 128-byte XOR swizzle applied to the
+// byte offset inside each (sequence, head) region: 16-byte unit u of every
+// 1024-byte block moves to u ^ (block row).  A 1-D TMA bulk copy brings it to
+// shared memory unchanged, where 8 consecutive 128-byte rows then hit 8
+// distinct bank groups (conflict-free ldmatrix and 16-byte loads).
+__host__ __device__ __forceinline__ uint32_t cache_swz(uint32_t a) {
+    return a ^ (((a >> 7) & 7u) << 4);
+}
+
 // ------------------------------------------------------------ warp reduce
 WSVD_DEV float warp_max(float v) {
 #pragma unroll
@@ -66,6 +76,15 @@ WSVD_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+
+WSVD_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// named barrier over a subset of the CTA's warps (id 0 is __syncthreads)
+WSVD_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 WSVD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -130,6 +149,18 @@ WSVD_DEV void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a
         "{%8,%9}, {%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+WSVD_DEV void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+WSVD_DEV void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
 }
 
 // D(16x8 s32) += A(16x32 s8, row) * B(32x8 s8, col)

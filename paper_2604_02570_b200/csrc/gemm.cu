@@ -306,7 +306,9 @@ int w_stride_h(int b) { return b + ((64 - (b & 127)) & 127); }
 }  // namespace
 
 int gemm_smem_bytes(int wdtype, int M, int KS) {
-    const int Mp = ((M + 15) / 16) * 16;
+    // rows staged = the kernel's MT bucket (1, 2, 4 or 8 tiles of 16)
+    const int mt = (M + 15) / 16;
+    const int Mp = 16 * (mt <= 2 ? mt : (mt <= 4 ? 4 : 8));
     switch (wdtype) {
         case BF16: return kRowsPerCta * w_stride_h(KS * 2) + Mp * (KS * 2 + GT<BF16>::XPAD) + 16;
         case I8: return kRowsPerCta * w_stride_h(KS) + Mp * (KS + GT<I8>::XPAD) + 16;

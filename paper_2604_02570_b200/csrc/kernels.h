@@ -62,6 +62,10 @@ struct AppendArgs {
 };
 cudaError_t launch_append_epilogue(const AppendArgs& a, cudaStream_t s);
 
+// host-provided rows [n][row_bytes] -> row `pos` of cache regions 0..n-1 (swizzled)
+cudaError_t launch_push_rows(const uint8_t* rows, int n, uint8_t* cache, int cap, int row_bytes,
+                             int pos, cudaStream_t s);
+
 // q [B][nh][H] -> qt [B][nh][R] = qt_scale * q . B_K^T
 cudaError_t launch_absorb_query(const float* q, int B, int nh, int R, int H, const void* bk,
                                 const float* bk_scale, int bdtype, float qt_scale, float* qt,
@@ -84,6 +88,7 @@ struct AttnArgs {
 };
 int attn_smem_bytes(int cdtype, int R);
 int attn_occupancy(int cdtype, int R);  // resident CTAs per SM (0 if unsupported)
+int attn_parts_per_chunk();             // warp partials published per unit
 cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s);
 
 }  // namespace wsvd_k

@@ -87,6 +87,10 @@ class DecodeLayer:
         N.call("wsvd_fused_decode_step", self.h, self._ptr(q), tile_len, self._ptr(out),
                self._stream(stream))
 
+    def attention_only(self, out, stream=None):
+        """The attention kernel alone (absorbed query of the last append)."""
+        N.call("wsvd_decode_attention", self.h, self._ptr(out), self._stream(stream))
+
     def step(self, x, y, attn_out=None, graph: bool = True, stream=None):
         """One layer step for every sequence: x [batch][E] -> y [batch][e_out]
         (this shard's partial O-projection)."""
