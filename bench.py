@@ -160,7 +160,7 @@ def algorithmic_bytes(cfg, B, nh_g, L):
     bfac = nh_g * 3 * r * H * (2 if wb == 2 else (4 if wb == 4 else 1))
     attn = cache + B * nh_g * r * 4 + nh_g * r * H * (2 if wb == 2 else 4) + B * nh_g * H * 4
     a_w = E * nh_g * 3 * r * wb + (nh_g * 3 * r * 4 if wb < 2 else 0)
-    oproj = nh_g * H * E * 2
+    oproj = nh_g * r * E * 2  # W'_o = B_V . W_o (V path folded into the O-projection)
     step = cache + a_w + bfac + B * E * 4 + B * nh_g * 2 * r * cb + B * nh_g * H * 4 + oproj + B * E * 4
     return attn, step
 

@@ -82,6 +82,7 @@ WSVD_DEV void absorb(const float* q_s, int R, int H, const void* bk, const float
     const size_t base = static_cast<size_t>(h) * R * H;
     for (int i = warp; i < R; i += nw) {
         float acc = 0.f;
+#pragma unroll 4
         for (int j = lane; j < H; j += 32) {
             float b = bload(bk, bdtype, base + static_cast<size_t>(i) * H + j);
             if (bdtype == I8) b *= bk_scale[h * H + j];
@@ -113,12 +114,15 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
         if (a.wdtype == I8 || a.wdtype == I4) {
             int acc = 0;
             const int* P = reinterpret_cast<const int*>(a.P);
-            for (int s = 0; s < a.splits; ++s) acc += P[s * stride + o];
+#pragma unroll 8
+            for (int s = 0; s < a.splits; ++s) acc += __ldcg(P + s * stride + o);
             val = __fmul_rn(__fmul_rn(static_cast<float>(acc), a.sx[m]), a.a_scale[nrow0 + i]);
         } else {
+            // fixed split order: deterministic
             float acc = 0.f;
             const float* P = reinterpret_cast<const float*>(a.P);
-            for (int s = 0; s < a.splits; ++s) acc += P[s * stride + o];
+#pragma unroll 8
+            for (int s = 0; s < a.splits; ++s) acc += __ldcg(P + s * stride + o);
             val = acc;
         }
         c[i] = val;
@@ -161,22 +165,36 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
             *reinterpret_cast<float*>(region + cache_swz(row0 + 4 * i)) = c[R + i];
     }
 
-    // ---- query: q_h = c_Q . B_Q (decode.cpp:140), then the absorbed key side
-    if (a.q_out != nullptr || a.qt != nullptr) {
+    // ---- query
+    if (a.q_out != nullptr) {
+        // reference API: q_h = c_Q . B_Q (decode.cpp:140) is returned; then the
+        // absorbed key side qt = scale * q_h . B_K^T
         const size_t bq0 = static_cast<size_t>(h) * R * H;
         for (int j = threadIdx.x; j < H; j += kEpThreads) {
             float acc = 0.f;
+#pragma unroll 16
             for (int i = 0; i < R; ++i) acc = fmaf(c[i], bload(a.bq, a.bdtype, bq0 + static_cast<size_t>(i) * H + j), acc);
             if (a.bdtype == I8) acc *= a.bq_scale[h * H + j];
             qh[j] = acc;
-            if (a.q_out) a.q_out[(static_cast<size_t>(m) * a.nh + h) * H + j] = acc;
+            a.q_out[(static_cast<size_t>(m) * a.nh + h) * H + j] = acc;
         }
         __syncthreads();
         if (a.qt) absorb(qh, R, H, a.bk, a.bk_scale, a.bdtype, h, a.qt_scale,
                          a.qt + (static_cast<size_t>(m) * a.nh + h) * R);
+    } else if (a.qt != nullptr) {
+        // layer step: q_h is never materialised; qt = c_Q . M_QK with
+        // M_QK = scale * B_Q . B_K^T (R x R, folded on the host in fp64)
+        const float* mq = a.mqk + static_cast<size_t>(h) * R * R;
+        for (int i = threadIdx.x; i < R; i += kEpThreads) {
+            float acc = 0.f;
+#pragma unroll 16
+            for (int j = 0; j < R; ++j) acc = fmaf(c[j], __ldg(mq + j * R + i), acc);
+            a.qt[(static_cast<size_t>(m) * a.nh + h) * R + i] = acc;
+        }
     }
 
     // ---- commit: the last CTA advances the length by T
+    if (!a.commit) return;
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();

@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
     float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int len = *a.d_len;
+    const int len = *a.d_len + a.len_add;
     if (len <= 0) return;
     const int nch = (len + a.chunk - 1) / a.chunk;
     const int n_units = a.B * a.nh * nch;
@@ -429,24 +429,33 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
 // warp partials in a fixed order) and the single B_V up-projection per head
 // (decode.cpp:198-203).  One CTA per (sequence, head).
 __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a, int parts_per_chunk) {
-    extern __shared__ float vt[];  // [R]
+    extern __shared__ float sm[];  // parts [np][R+2], then vt [R]
     const int bh = blockIdx.x, tid = threadIdx.x, R = a.R;
-    const int len = *a.d_len;
+    const int len = *a.d_len + a.len_add;
     if (len <= 0) return;
     const int nch = (len + a.chunk - 1) / a.chunk;
     const int np = nch * parts_per_chunk;
+    float* part = sm;
+    float* vt = sm + a.max_chunks * parts_per_chunk * (R + 2);
+    // stage every partial of this (sequence, head) with coalesced loads
     const float* wsb = a.ws + static_cast<size_t>(bh) * a.max_chunks * parts_per_chunk * (R + 2);
+    for (int i = tid; i < np * (R + 2); i += blockDim.x) part[i] = __ldcg(wsb + i);
+    __syncthreads();
     float M = -INFINITY;
-    for (int p = 0; p < np; ++p) M = fmaxf(M, wsb[p * (R + 2) + R]);
+    for (int p = 0; p < np; ++p) M = fmaxf(M, part[p * (R + 2) + R]);
     float L = 0.f, acc = 0.f;
     for (int p = 0; p < np; ++p) {
-        const float m = wsb[p * (R + 2) + R];
+        const float m = part[p * (R + 2) + R];
         if (m == -INFINITY) continue;  // a warp that saw no token of its chunk
         const float f = ex2(m - M);
-        L = fmaf(wsb[p * (R + 2) + R + 1], f, L);
-        if (tid < R) acc = fmaf(wsb[p * (R + 2) + tid], f, acc);
+        L = fmaf(part[p * (R + 2) + R + 1], f, L);
+        if (tid < R) acc = fmaf(part[p * (R + 2) + tid], f, acc);
     }
-    if (tid < R) vt[tid] = acc / L;
+    if (tid < R) {
+        vt[tid] = acc / L;
+        if (a.vlat) a.vlat[static_cast<size_t>(bh) * R + tid] = acc / L;
+    }
+    if (a.out == nullptr) return;  // the layer step folds B_V into W_o
     __syncthreads();
     const int h = bh % a.nh;
     const size_t bvo = static_cast<size_t>(h) * R * a.H;
@@ -475,7 +484,14 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
         k<<<a.grid, kThreads, C::SMEM, s>>>(a);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;
-        attn_combine_kernel<<<a.B * a.nh, 128, R * 4, s>>>(a, kConsumerWarps);
+        const int csmem = (a.max_chunks * kConsumerWarps * (R + 2) + R) * 4;
+        static int cattr = 0;
+        if (csmem > cattr) {
+            e = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
+            if (e != cudaSuccess) return e;
+            cattr = csmem;
+        }
+        attn_combine_kernel<<<a.B * a.nh, 128, csmem, s>>>(a, kConsumerWarps);
         return cudaGetLastError();
     }
 }

@@ -44,6 +44,21 @@ int round_up(int v, int m) { return (v + m - 1) / m * m; }
 // host copy of cache_swz (common.cuh): the 16-byte XOR swizzle of cache rows
 uint32_t wsvd_dev_swz(uint32_t a) { return a ^ (((a >> 7) & 7u) << 4); }
 
+// W-tiles (gemm.cu): rows [nrows][row_bytes] -> [nrows/16][row_bytes/ksb][16][ksb],
+// the 16-byte units of odd rows XOR 4.  nrows must be a multiple of 16.
+void pack_wtiles(const uint8_t* rows, int nrows, int row_bytes, int ksb, uint8_t* out) {
+    const int splits = row_bytes / ksb, units = ksb / 16;
+    for (int r = 0; r < nrows; ++r) {
+        const int tile = r / 16, rr = r % 16;
+        for (int s = 0; s < splits; ++s)
+            for (int u = 0; u < units; ++u) {
+                const size_t dst = ((static_cast<size_t>(tile) * splits + s) * 16 + rr) * ksb +
+                                   static_cast<size_t>(u ^ ((rr & 1) << 2)) * 16;
+                std::memcpy(out + dst, rows + static_cast<size_t>(r) * row_bytes + static_cast<size_t>(s) * ksb + u * 16, 16);
+            }
+    }
+}
+
 struct DevBuf {
     void* p = nullptr;
     size_t n = 0;
@@ -198,7 +213,11 @@ struct wsvd_layer_s {
     float rot_scale = 1.f;
     // O-projection
     int e_out = 0, o_dtype = BF16, oKp = 0;
-    DevBuf Wo;                        // [e_out][oKp]
+    int ks = 512, oks = 1024;         // K split of the projection / O-projection W-tiles
+    DevBuf Wo;                        // [e_out][oKp] rows of W'_o = B_V . W_o (K = nh*R)
+    std::vector<double> b_host[3];    // [nh][R][H] device B values per role (for host folds)
+    DevBuf mqk;                       // [nh][R][R] qt_scale * B_Q . B_K^T (fp32)
+    bool mqk_ready = false;
 };
 
 struct GraphKey {
@@ -212,7 +231,7 @@ struct wsvd_cache_s {
     int B = 0, cap = 0, cap_alloc = 0, cdtype = BF16, row_bytes = 0;
     int len = 0;                      // host mirror of *d_len
     DevBuf data, scales, ctrl;        // ctrl: [0]=d_len, [1]=done
-    DevBuf qt, q_tmp, attn_ws, attn_cnt, attn_out;
+    DevBuf qt, q_tmp, attn_ws, attn_cnt, vlat;
     DevBuf P, xq, sx;                 // projection workspace
     int P_M = 0;                      // rows the projection workspace holds
     DevBuf oP, y_tmp;                 // O-proj partials
@@ -249,25 +268,13 @@ int check_layer(wsvd_layer_t l) {
     return WSVD_OK;
 }
 
-int choose_ks(int wdtype, int M, int N, int Kp, int sms) {
-    // Largest split that keeps >= ~4 CTAs per SM in flight and fits 2 CTAs/SM.
-    int best = 256;
-    for (int ks : {256, 512, 1024, 2048}) {
-        if (Kp % ks) continue;
-        if (gemm_smem_bytes(wdtype, M, ks) > 100 * 1024) break;
-        const long ctas = static_cast<long>((N + 63) / 64) * (Kp / ks);
-        if (ctas < 4L * sms && ks != 256) break;
-        best = ks;
-    }
-    if (Kp % best) best = 128;
-    return best;
-}
-
 // projection of M token rows (fp32 x [M][E]) into the partial workspace
 int run_projection(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* splits_out) {
     wsvd_layer_s* L = c->L;
     const int wd = L->d.weight_dtype;
-    const int ks = (wd == F32) ? std::min(L->Kp, 1024) : choose_ks(wd, M, L->Nrows, L->Kp, c->sms);
+    const int ks = L->ks;
+    if (!gemm_fits(wd, M, ks))
+        return set_err(WSVD_ECONFIG, std::to_string(M) + " token rows do not fit the projection kernel");
     const int splits = L->Kp / ks;
     const size_t need = static_cast<size_t>(splits) * M * L->Nrows * 4;
     if (c->P.n < need) CUDA_TRY(c->P.alloc(need));
@@ -281,6 +288,7 @@ int run_projection(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* 
     g.KS = ks;
     g.ldx = L->d.embed_dim;
     g.wdtype = wd;
+    g.grid = c->sms;
     if (wd == I8 || wd == I4) {
         if (c->xq.n < static_cast<size_t>(M) * L->Kp) CUDA_TRY(c->xq.alloc(static_cast<size_t>(M) * L->Kp));
         if (c->sx.n < static_cast<size_t>(M) * 4) CUDA_TRY(c->sx.alloc(static_cast<size_t>(M) * 4));
@@ -295,9 +303,34 @@ int run_projection(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* 
     return WSVD_OK;
 }
 
-int run_append(wsvd_cache_s* c, const float* x, int T, float* q_out, float* qt, cudaStream_t s) {
+// M_QK[h] = qt_scale * B_Q[h] . B_K[h]^T (R x R, fp64 -> fp32) from the device's B values
+int ensure_mqk(wsvd_layer_s* L) {
+    if (L->mqk_ready) return WSVD_OK;
+    const int nh = L->d.n_heads, R = L->R, H = L->d.head_dim;
+    const double scale = 1.4426950408889634 / std::sqrt(static_cast<double>(H));
+    std::vector<float> m(static_cast<size_t>(nh) * R * R);
+    for (int h = 0; h < nh; ++h)
+        for (int j = 0; j < R; ++j)
+            for (int i = 0; i < R; ++i) {
+                const double* bq = L->b_host[0].data() + (static_cast<size_t>(h) * R + j) * H;
+                const double* bk = L->b_host[1].data() + (static_cast<size_t>(h) * R + i) * H;
+                double acc = 0.0;
+                for (int d = 0; d < H; ++d) acc += bq[d] * bk[d];
+                m[(static_cast<size_t>(h) * R + j) * R + i] = static_cast<float>(acc * scale);
+            }
+    if (!L->mqk.p) CUDA_TRY(L->mqk.alloc(m.size() * 4));
+    CUDA_TRY(cudaMemcpy(L->mqk.p, m.data(), m.size() * 4, cudaMemcpyHostToDevice));
+    L->mqk_ready = true;
+    return WSVD_OK;
+}
+
+int run_append(wsvd_cache_s* c, const float* x, int T, float* q_out, float* qt, int commit, cudaStream_t s) {
     wsvd_layer_s* L = c->L;
     const int M = T * c->B;
+    if (qt && !q_out) {
+        const int rc0 = ensure_mqk(L);
+        if (rc0) return rc0;
+    }
     int splits = 0;
     int rc = run_projection(c, x, M, s, &splits);
     if (rc) return rc;
@@ -329,11 +362,15 @@ int run_append(wsvd_cache_s* c, const float* x, int T, float* q_out, float* qt, 
     a.q_out = q_out;
     a.qt = qt;
     a.qt_scale = 1.4426950408889634f / std::sqrt(static_cast<float>(L->d.head_dim));
+    a.mqk = L->mqk.as<float>();
+    a.commit = commit;
     CUDA_TRY(launch_append_epilogue(a, s));
     return WSVD_OK;
 }
 
-int run_attention(wsvd_cache_s* c, float* out, cudaStream_t s) {
+// out: per-head outputs (B_V applied) or null; vlat: latent outputs or null;
+// len_add: rows appended by this step but not yet committed to *d_len
+int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStream_t s) {
     wsvd_layer_s* L = c->L;
     AttnArgs a{};
     a.cache = c->data.as<uint8_t>();
@@ -343,9 +380,11 @@ int run_attention(wsvd_cache_s* c, float* out, cudaStream_t s) {
     a.bv_scale = L->b_scale[2].as<float>();
     a.bdtype = L->bdtype;
     a.out = out;
+    a.vlat = vlat;
     a.ws = c->attn_ws.as<float>();
     a.counters = c->attn_cnt.as<int>();
     a.d_len = c->d_len();
+    a.len_add = len_add;
     a.B = c->B;
     a.nh = L->d.n_heads;
     a.H = L->d.head_dim;
@@ -360,18 +399,25 @@ int run_attention(wsvd_cache_s* c, float* out, cudaStream_t s) {
     return WSVD_OK;
 }
 
-int run_oproj(wsvd_cache_s* c, const float* attn, float* y, cudaStream_t s) {
+// y = vlat . (B_V W_o): the V-path up-projection folded into the output
+// projection (SPEC section 3.4, "B_Vh is fused into the output projection").
+int run_oproj(wsvd_cache_s* c, const float* vlat, float* y, int* commit_len, cudaStream_t s) {
     wsvd_layer_s* L = c->L;
     if (!L->Wo.p) return set_err(WSVD_ECONFIG, "layer has no O-projection (wsvd_layer_set_oproj)");
-    const int K = L->d.n_heads * L->d.head_dim;
-    const int ks = (L->o_dtype == F32) ? std::min(L->oKp, 1024) : choose_ks(L->o_dtype, c->B, L->e_out, L->oKp, c->sms);
+    const int K = L->d.n_heads * L->R;
+    // the folded O-projection is short (K = nh*R <= 1024 at 7B): one K split,
+    // each 16-row tile is one work item and the GEMM writes y directly
+    const int ks = L->oks;
+    if (!gemm_fits(L->o_dtype, c->B, ks))
+        return set_err(WSVD_ECONFIG, "batch of " + std::to_string(c->B) + " does not fit the O-projection kernel");
     const int splits = L->oKp / ks;
     const size_t need = static_cast<size_t>(splits) * c->B * L->e_out * 4;
     if (c->oP.n < need) CUDA_TRY(c->oP.alloc(need));
     GemmArgs g{};
     g.W = L->Wo.p;
-    g.X = attn;
-    g.P = c->oP.p;
+    g.X = vlat;
+    g.P = splits == 1 ? static_cast<void*>(y) : c->oP.p;
+    g.commit_len = commit_len;
     g.M = c->B;
     g.N = L->e_out;
     g.K = K;
@@ -379,18 +425,20 @@ int run_oproj(wsvd_cache_s* c, const float* attn, float* y, cudaStream_t s) {
     g.KS = ks;
     g.ldx = K;
     g.wdtype = L->o_dtype;
+    g.grid = c->sms;
     CUDA_TRY(launch_gemm(g, s));
-    CUDA_TRY(launch_reduce_partials(c->oP.as<float>(), splits, c->B, L->e_out, y, s));
+    if (splits > 1) CUDA_TRY(launch_reduce_partials(c->oP.as<float>(), splits, c->B, L->e_out, y, s));
     return WSVD_OK;
 }
 
+// append (row written, length not yet committed) -> attention over len + 1
+// -> combine -> folded O-projection, whose first thread commits the length
 int layer_step_impl(wsvd_cache_s* c, const float* x, float* attn_out, float* y, cudaStream_t s) {
-    float* attn = attn_out ? attn_out : c->attn_out.as<float>();
-    int rc = run_append(c, x, 1, nullptr, c->qt.as<float>(), s);
+    int rc = run_append(c, x, 1, nullptr, c->qt.as<float>(), 0, s);
     if (rc) return rc;
-    rc = run_attention(c, attn, s);
+    rc = run_attention(c, attn_out, c->vlat.as<float>(), 1, s);
     if (rc) return rc;
-    return run_oproj(c, attn, y, s);
+    return run_oproj(c, c->vlat.as<float>(), y, c->d_len(), s);
 }
 
 }  // namespace
@@ -433,9 +481,11 @@ int wsvd_layer_create(const wsvd_layer_desc* desc, const int32_t* ranks, wsvd_la
     L->d = d;
     L->R = R;
     L->Kp = round_up(d.embed_dim, 256);
+    L->ks = (L->Kp % 512 == 0) ? 512 : 256;
     L->Nrows = d.n_heads * 3 * R;
     L->ranks.assign(ranks, ranks + d.n_heads * 3);
     L->have.assign(d.n_heads * 3, 0);
+    for (auto& bh : L->b_host) bh.assign(static_cast<size_t>(d.n_heads) * R * d.head_dim, 0.0);
     L->bdtype = (d.weight_dtype == WSVD_I4) ? I8 : d.weight_dtype;
     if (d.act_rotation) {
         const size_t blk = rot_block(static_cast<size_t>(d.embed_dim));
@@ -506,6 +556,13 @@ static int upload_head(wsvd_layer_t L, int head, int role, const std::vector<int
         }
         if (as) ascale[i] = static_cast<float>((*as)[i]);
     }
+    if (wd != WSVD_F32) {
+        // W-tiles: this head-role's R rows are R/16 whole tiles at byte offset n0 * rb
+        std::vector<uint8_t> tiled(rows.size());
+        pack_wtiles(rows.data(), R, static_cast<int>(rb), wd == WSVD_I4 ? L->ks / 2 : L->ks * (wd == WSVD_BF16 ? 2 : 1),
+                    tiled.data());
+        rows.swap(tiled);
+    }
     CUDA_TRY(cudaMemcpy(L->A.as<uint8_t>() + n0 * rb, rows.data(), rows.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(L->a_scale.as<float>() + n0, ascale.data(), R * 4, cudaMemcpyHostToDevice));
     // ---- B: [head][R][H]
@@ -522,6 +579,26 @@ static int upload_head(wsvd_layer_t L, int head, int role, const std::vector<int
         }
     if (bs)
         for (int j = 0; j < H; ++j) bsc[j] = static_cast<float>((*bs)[j]);
+    {
+        // host copy of the device's B values, for the host-side folds
+        // (B_Q . B_K^T for the absorbed query, B_V . W_o for the O-projection)
+        for (int i = 0; i < R; ++i)
+            for (int j = 0; j < H; ++j) {
+                const size_t o = static_cast<size_t>(i) * H + j;
+                double v = 0.0;
+                if (L->bdtype == F32) v = reinterpret_cast<const float*>(bh.data())[o];
+                else if (L->bdtype == BF16) {
+                    const uint32_t u = static_cast<uint32_t>(reinterpret_cast<const uint16_t*>(bh.data())[o]) << 16;
+                    float f;
+                    std::memcpy(&f, &u, 4);
+                    v = f;
+                } else {
+                    v = static_cast<double>(reinterpret_cast<const int8_t*>(bh.data())[o]) * static_cast<double>(bsc[j]);
+                }
+                L->b_host[role][(static_cast<size_t>(head) * R + i) * H + j] = v;
+            }
+    }
+    L->mqk_ready = false;
     CUDA_TRY(cudaMemcpy(L->B[role].as<uint8_t>() + static_cast<size_t>(head) * R * H * bel, bh.data(), bh.size(),
                         cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(L->b_scale[role].as<float>() + static_cast<size_t>(head) * H, bsc.data(), H * 4,
@@ -574,20 +651,45 @@ int wsvd_layer_set_oproj(wsvd_layer_t L, const double* w, int32_t e_out, int32_t
     if (!L || !w) return set_err(WSVD_ECONFIG, "null argument");
     if (e_out <= 0) return set_err(WSVD_ESHAPE, "e_out must be positive");
     if (dtype != WSVD_F32 && dtype != WSVD_BF16) return set_err(WSVD_ECONFIG, "O-projection dtype must be F32 or BF16");
+    if (!L->have[2]) return set_err(WSVD_ECONFIG, "upload the V factors before the O-projection");
+    for (size_t i = 0; i < L->have.size(); i += 3)
+        if (!L->have[i + 2]) return set_err(WSVD_ECONFIG, "upload the V factors before the O-projection");
     CUDA_TRY(cudaSetDevice(L->d.device));
-    const int K = L->d.n_heads * L->d.head_dim;
+    // W'_o = blockdiag_h(B_Vh) . W_o  ((n_heads*R) x e_out): the latent attention
+    // output is projected straight to the model width (SPEC section 3.4)
+    const int nh = L->d.n_heads, H = L->d.head_dim, R = L->R;
+    const int K = nh * R;
     L->e_out = e_out;
     L->o_dtype = dtype;
     L->oKp = round_up(K, 256);
+    L->oks = L->oKp <= 1024 ? L->oKp : ((L->oKp % 512 == 0) ? 512 : 256);
+    if (dtype == WSVD_F32) L->oks = std::min(L->oKp, 1024);
+    const int e_pad = round_up(e_out, 16);  // whole W-tiles
     const size_t el = dtype == WSVD_F32 ? 4 : 2;
-    std::vector<uint8_t> rows(static_cast<size_t>(e_out) * L->oKp * el, 0);
+    std::vector<double> fold(static_cast<size_t>(K) * e_out, 0.0);
+    for (int h = 0; h < nh; ++h)
+        for (int i = 0; i < R; ++i) {
+            double* dst = fold.data() + (static_cast<size_t>(h) * R + i) * e_out;
+            for (int j = 0; j < H; ++j) {
+                const double bv = L->b_host[2][(static_cast<size_t>(h) * R + i) * H + j];
+                if (bv == 0.0) continue;
+                const double* src = w + (static_cast<size_t>(h) * H + j) * e_out;
+                for (int e = 0; e < e_out; ++e) dst[e] += bv * src[e];
+            }
+        }
+    std::vector<uint8_t> rows(static_cast<size_t>(e_pad) * L->oKp * el, 0);
     for (int e = 0; e < e_out; ++e)
         for (int k = 0; k < K; ++k) {
-            const double v = w[static_cast<size_t>(k) * e_out + e];
+            const double v = fold[static_cast<size_t>(k) * e_out + e];
             const size_t o = static_cast<size_t>(e) * L->oKp + k;
             if (dtype == WSVD_F32) reinterpret_cast<float*>(rows.data())[o] = static_cast<float>(v);
             else reinterpret_cast<uint16_t*>(rows.data())[o] = f32_to_bf16_bits(static_cast<float>(v));
         }
+    if (dtype == WSVD_BF16) {
+        std::vector<uint8_t> tiled(rows.size());
+        pack_wtiles(rows.data(), e_pad, L->oKp * 2, L->oks * 2, tiled.data());
+        rows.swap(tiled);
+    }
     CUDA_TRY(L->Wo.alloc(rows.size()));
     CUDA_TRY(cudaMemcpy(L->Wo.p, rows.data(), rows.size(), cudaMemcpyHostToDevice));
     return WSVD_OK;
@@ -628,7 +730,8 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     if (e == cudaSuccess) e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh * c->max_chunks * attn_parts_per_chunk() * (L->R + 2) * 4);
     if (e == cudaSuccess) e = c->attn_cnt.alloc(static_cast<size_t>(batch) * nh * 4);
-    if (e == cudaSuccess) e = c->attn_out.alloc(static_cast<size_t>(batch) * nh * H * 4);
+    if (e == cudaSuccess) e = c->vlat.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
+    (void)H;
     if (e != cudaSuccess) {
         delete c;
         return set_err(WSVD_ECUDA, std::string("cache allocation: ") + cudaGetErrorString(e));
@@ -790,7 +893,7 @@ int wsvd_append_token(wsvd_cache_t c, const float* x, float* q_out, void* stream
     if (rc) return rc;
     if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
     CUDA_TRY(cudaSetDevice(c->L->d.device));
-    rc = run_append(c, x, 1, q_out, c->qt.as<float>(), static_cast<cudaStream_t>(stream));
+    rc = run_append(c, x, 1, q_out, c->qt.as<float>(), 1, static_cast<cudaStream_t>(stream));
     if (rc) return rc;
     c->len += 1;
     return WSVD_OK;
@@ -807,7 +910,7 @@ int wsvd_prefill(wsvd_cache_t c, const float* x, int32_t T, void* stream) {
     const int tc = std::max(1, 128 / c->B);  // <= 128 token rows per projection
     for (int t0 = 0; t0 < T; t0 += tc) {
         const int n = std::min(tc, T - t0);
-        rc = run_append(c, x + static_cast<size_t>(t0) * c->B * E, n, nullptr, nullptr, static_cast<cudaStream_t>(stream));
+        rc = run_append(c, x + static_cast<size_t>(t0) * c->B * E, n, nullptr, nullptr, 1, static_cast<cudaStream_t>(stream));
         if (rc) return rc;
         c->len += n;
     }
@@ -826,14 +929,14 @@ int wsvd_fused_decode_step(wsvd_cache_t c, const float* q, int32_t tile_len, flo
     CUDA_TRY(launch_absorb_query(q, c->B, L->d.n_heads, L->R, L->d.head_dim, L->B[1].p, L->b_scale[1].as<float>(),
                                  L->bdtype, 1.4426950408889634f / std::sqrt(static_cast<float>(L->d.head_dim)),
                                  c->qt.as<float>(), s));
-    return run_attention(c, out, s);
+    return run_attention(c, out, nullptr, 0, s);
 }
 
 int wsvd_decode_attention(wsvd_cache_t c, float* out, void* stream) {
     if (!c || !out) return set_err(WSVD_ECONFIG, "null argument");
     if (c->len == 0) return set_err(WSVD_ESHAPE, "decode step over an empty cache");
     CUDA_TRY(cudaSetDevice(c->L->d.device));
-    return run_attention(c, out, static_cast<cudaStream_t>(stream));
+    return run_attention(c, out, nullptr, 0, static_cast<cudaStream_t>(stream));
 }
 
 int wsvd_layer_step(wsvd_cache_t c, const float* x, float* attn_out, float* y, void* stream) {

@@ -3,16 +3,20 @@
 //   latent projection  C[m][n] = x_m . A_all[:, n]   (append_token's vec_mat
 //                      calls x.A_K, x.A_V, x.A_Q, decode.cpp:137-139, for every
 //                      head at once: N = n_heads * 3 * R columns)
-//   O-projection       y[m][e] = heads_row_m . W_o[:, e]   (pipeline.cpp:329)
+//   O-projection       y[m][e] = vlat_m . W'_o[:, e], W'_o = B_V . W_o
+//                      (pipeline.cpp:323-329 with the V up-projection folded in)
 //
-// Weights are stored K-major (one contiguous row of E values per output
-// column) so a warp streams 16 weight rows with fully used 32-byte sectors.
+// Weight layout in HBM ("W-tiles"): every (16-row tile, K split) work item is
+// one contiguous block [16 rows][KS] -- rows are output columns, K-major --
+// with the 16-byte units of odd rows XOR-ed by 4 so that the MMA fragment
+// loads are bank-conflict free.  One TMA bulk copy moves one work item.
+//
 // The MMA's M side is the weight rows and its N side the tokens ("swap AB"),
 // so a decode batch of 16 tokens exactly fills two m16n8 tiles.  The k order
 // inside each 32/64/128-wide block is permuted identically for the weight
 // (A) and token (B) fragments, which lets every lane load its fragment with
 // one 16-byte load per row; a contraction does not care about k order.
-// Partial sums of each K split go to P[split][m][n]; the consumer sums the
+// Partial sums of each K split go to P[split][m][n]; consumers sum the
 // splits in a fixed order, so results are run-to-run deterministic.  Integer
 // modes accumulate in int32 and are bit-exact.
 #include "common.cuh"
@@ -24,8 +28,7 @@ namespace wsvd_k {
 
 namespace {
 
-constexpr int kGemmThreads = 128;  // 4 warps x 16 weight rows
-constexpr int kRowsPerCta = 64;
+constexpr int kXThreads = 128;  // threads that stage the token slice
 
 template <int WT>
 struct GT;
@@ -34,201 +37,265 @@ struct GT<BF16> {
     static constexpr int KB = 32;      // k per block (two k16 MMA steps)
     static constexpr int XB = 2;       // bytes per X element in smem
     static constexpr int XPAD = 64;    // row pad: stride == 64 mod 128 -> conflict-free
-    static constexpr int U = 8;        // blocks in flight per lane
 };
 template <>
 struct GT<I8> {
     static constexpr int KB = 64;
     static constexpr int XB = 1;
     static constexpr int XPAD = 64;
-    static constexpr int U = 8;
 };
 template <>
 struct GT<I4> {
     static constexpr int KB = 128;
     static constexpr int XB = 1;
     static constexpr int XPAD = 16;    // 32-byte X reads per lane
-    static constexpr int U = 4;
 };
 
 template <int WT>
-WSVD_DEV int x_stride(int KS) {
+__host__ __device__ __forceinline__ int x_stride(int KS) {
     return KS * GT<WT>::XB + GT<WT>::XPAD;
 }
 
-// Stage X[:, k0:k0+KS] into shared memory (bf16 or int8), zero-padded to Mp rows.
+// Stage X[:, k0:k0+KS] into shared memory (bf16 or int8), zero-padded to Mp
+// rows.  Loads are issued in batches of 8 per thread before any is consumed,
+// so staging costs one memory latency per batch rather than one per item.
 template <int WT>
 WSVD_DEV void stage_x(const GemmArgs& a, uint8_t* xs, int k0, int Mp) {
     const int stride = x_stride<WT>(a.KS);
+    constexpr int BATCH = 8;
     if (WT == BF16) {
         const float* X = reinterpret_cast<const float*>(a.X);
         const int per_row = a.KS / 8;  // 8 elements per thread-item
-        for (int i = threadIdx.x; i < Mp * per_row; i += kGemmThreads) {
-            const int m = i / per_row, kk = (i - m * per_row) * 8;
-            const int k = k0 + kk;
-            uint4 o = make_uint4(0, 0, 0, 0);
-            if (m < a.M) {
-                const float* src = X + static_cast<size_t>(m) * a.ldx + k;
-                float v[8];
-                if (k + 8 <= a.K && (a.ldx % 4) == 0) {
-                    const float4 p0 = *reinterpret_cast<const float4*>(src);
-                    const float4 p1 = *reinterpret_cast<const float4*>(src + 4);
-                    v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w;
-                    v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
-                } else {
+        const int n = Mp * per_row;
+        const bool vec = (a.ldx % 4) == 0;
+        for (int i0 = threadIdx.x; i0 < n; i0 += kXThreads * BATCH) {
+            float4 p[BATCH][2];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) v[j] = (k + j < a.K) ? src[j] : 0.f;
+            for (int u = 0; u < BATCH; ++u) {
+                const int i = i0 + u * kXThreads;
+                const int m = i / per_row, kk = (i - m * per_row) * 8;
+                const int k = k0 + kk;
+                p[u][0] = p[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (i < n && m < a.M) {
+                    const float* src = X + static_cast<size_t>(m) * a.ldx + k;
+                    if (k + 8 <= a.K && vec) {
+                        p[u][0] = __ldg(reinterpret_cast<const float4*>(src));
+                        p[u][1] = __ldg(reinterpret_cast<const float4*>(src + 4));
+                    } else {
+                        float v[8];
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) v[j] = (k + j < a.K) ? src[j] : 0.f;
+                        p[u][0] = make_float4(v[0], v[1], v[2], v[3]);
+                        p[u][1] = make_float4(v[4], v[5], v[6], v[7]);
+                    }
                 }
-                o.x = pack_bf16x2(v[0], v[1]); o.y = pack_bf16x2(v[2], v[3]);
-                o.z = pack_bf16x2(v[4], v[5]); o.w = pack_bf16x2(v[6], v[7]);
             }
-            *reinterpret_cast<uint4*>(xs + m * stride + kk * 2) = o;
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int i = i0 + u * kXThreads;
+                if (i >= n) break;
+                const int m = i / per_row, kk = (i - m * per_row) * 8;
+                uint4 o;
+                o.x = pack_bf16x2(p[u][0].x, p[u][0].y); o.y = pack_bf16x2(p[u][0].z, p[u][0].w);
+                o.z = pack_bf16x2(p[u][1].x, p[u][1].y); o.w = pack_bf16x2(p[u][1].z, p[u][1].w);
+                *reinterpret_cast<uint4*>(xs + m * stride + kk * 2) = o;
+            }
         }
     } else {
         const int8_t* X = reinterpret_cast<const int8_t*>(a.X);
         const int per_row = a.KS / 16;
-        for (int i = threadIdx.x; i < Mp * per_row; i += kGemmThreads) {
-            const int m = i / per_row, kk = (i - m * per_row) * 16;
-            uint4 o = make_uint4(0, 0, 0, 0);
-            if (m < a.M) o = *reinterpret_cast<const uint4*>(X + static_cast<size_t>(m) * a.Kp + k0 + kk);
-            *reinterpret_cast<uint4*>(xs + m * stride + kk) = o;
+        const int n = Mp * per_row;
+        for (int i0 = threadIdx.x; i0 < n; i0 += kXThreads * BATCH) {
+            uint4 o[BATCH];
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int i = i0 + u * kXThreads;
+                const int m = i / per_row, kk = (i - m * per_row) * 16;
+                o[u] = make_uint4(0, 0, 0, 0);
+                if (i < n && m < a.M)
+                    o[u] = __ldg(reinterpret_cast<const uint4*>(X + static_cast<size_t>(m) * a.Kp + k0 + kk));
+            }
+#pragma unroll
+            for (int u = 0; u < BATCH; ++u) {
+                const int i = i0 + u * kXThreads;
+                if (i >= n) break;
+                const int m = i / per_row, kk = (i - m * per_row) * 16;
+                *reinterpret_cast<uint4*>(xs + m * stride + kk) = o[u];
+            }
         }
     }
 }
 
-template <int WT>
-WSVD_DEV int w_row_bytes(int KS) {
-    return WT == I4 ? KS / 2 : KS * (WT == BF16 ? 2 : 1);
-}
-// smem pitch of a staged weight row: == 64 (mod 128) so the 8 lanes of a
-// shared-memory phase (2 rows x 4 x 16 B) hit distinct banks
-template <int WT>
-WSVD_DEV int w_stride(int KS) {
-    const int b = w_row_bytes<WT>(KS);
-    return b + ((64 - (b & 127)) & 127);
-}
+// ---------------------------------------------------------------------------
+// Persistent streaming GEMM.  CTAs are assigned split-aligned: CTA c works on
+// K split c % splits and a contiguous run of 16-row tiles, so it stages one
+// token slice.  A producer warp streams each work item (one W-tile block) into
+// a ring of shared-memory slots with one TMA bulk copy per item (completion on
+// the slot's mbarrier); consumer warp w takes items w, w+4, ... and runs the
+// MMAs straight from the slot.  One CTA per SM, deep bytes-in-flight, no wave
+// quantisation.
+constexpr int kStreamConsumers = 4;
+constexpr int kStreamThreads = 32 * (kStreamConsumers + 1);
 
-// One CTA: 64 weight rows x one K split.  Thread 0 streams the 64 rows of
-// the split into shared memory with TMA bulk copies (one per row, completion
-// on one mbarrier) while all threads convert/stage the token slice; then
-// 4 warps run the MMAs out of shared memory.
 template <int WT, int MT>
-__global__ void __launch_bounds__(kGemmThreads) skinny_mma_kernel(const GemmArgs a) {
+struct StreamCfg {
+    static constexpr int XROWS = MT * 16;
+    __host__ __device__ static int ksb(int KS) { return WT == I4 ? KS / 2 : KS * (WT == BF16 ? 2 : 1); }
+    __host__ __device__ static int item_bytes(int KS) { return 16 * ksb(KS); }
+    __host__ __device__ static int xbytes(int KS) { return XROWS * x_stride<WT>(KS); }
+    __host__ __device__ static int stages(int KS) {
+        const int budget = 222 * 1024 - xbytes(KS) - 256;
+        int s = budget / item_bytes(KS);
+        return s > 8 ? 8 : s;
+    }
+    __host__ __device__ static int smem(int KS) { return stages(KS) * item_bytes(KS) + xbytes(KS) + 256; }
+};
+
+template <int WT, int MT>
+__global__ void __launch_bounds__(kStreamThreads, 1) skinny_stream_kernel(const GemmArgs a) {
     using G = GT<WT>;
+    using S = StreamCfg<WT, MT>;
     extern __shared__ __align__(128) uint8_t smem[];
-    const int split = blockIdx.y;
-    const int k0 = split * a.KS;
-    const int Mp = MT * 16;
-    const int wrb = w_row_bytes<WT>(a.KS);
-    const int wst = w_stride<WT>(a.KS);
-    uint8_t* ws = smem;                                     // [64][wst]
-    uint8_t* xs = smem + kRowsPerCta * wst;                 // [Mp][xstride]
-    uint64_t* bar = reinterpret_cast<uint64_t*>(xs + Mp * x_stride<WT>(a.KS));
-    const int nc0 = blockIdx.x * kRowsPerCta;
-    const int nrows = min(kRowsPerCta, a.N - nc0);
+    const int KS = a.KS;
+    const int nst = S::stages(KS);
+    const int ksb = S::ksb(KS), xst = x_stride<WT>(KS);
+    const int ibytes = S::item_bytes(KS);
+    uint8_t* ring = smem;
+    uint8_t* xbuf = smem + nst * ibytes;
+    uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + S::xbytes(KS));
+    uint64_t* empty = full + 8;
+
+    if (a.commit_len && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.commit_len, 1);
+    const int splits = a.Kp / KS;
+    const int cps = gridDim.x / splits;  // CTAs per split
+    const int s = blockIdx.x % splits, j = blockIdx.x / splits;
+    if (j >= cps) return;
+    const int tiles = (a.N + 15) / 16;
+    const int lo = static_cast<int>(static_cast<long>(j) * tiles / cps);
+    const int hi = static_cast<int>(static_cast<long>(j + 1) * tiles / cps);
+    if (lo >= hi) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
+        for (int i = 0; i < nst; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
         fence_mbar_init();
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const size_t full_row = static_cast<size_t>(WT == I4 ? a.Kp / 2 : a.Kp * (WT == BF16 ? 2 : 1));
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(a.W) + static_cast<size_t>(nc0) * full_row +
-                             static_cast<size_t>(WT == I4 ? k0 / 2 : k0 * (WT == BF16 ? 2 : 1));
-        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nrows * wrb));
-        for (int r = 0; r < nrows; ++r) tma_bulk_g2s(ws + r * wst, src + r * full_row, wrb, bar);
-    }
-    stage_x<WT>(a, xs, k0, Mp);
-    __syncthreads();
-    mbar_wait(bar, 0);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == kStreamConsumers) {
+        // ------------------------------------------------ producer warp
+        if (lane == 0) {
+            const uint8_t* W = reinterpret_cast<const uint8_t*>(a.W);
+            for (int tile = lo; tile < hi; ++tile) {
+                const int k = tile - lo, slot = k % nst;
+                const uint32_t ph = static_cast<uint32_t>(k / nst) & 1u;
+                mbar_wait(&empty[slot], ph ^ 1u);
+                mbar_arrive_expect_tx(&full[slot], static_cast<uint32_t>(ibytes));
+                tma_bulk_g2s(ring + slot * ibytes, W + (static_cast<size_t>(tile) * splits + s) * ibytes, ibytes,
+                             &full[slot]);
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------ consumers
+    stage_x<WT>(a, xbuf, s * KS, S::XROWS);
+    named_bar_sync(1, 32 * kStreamConsumers);
+
     const int g = lane >> 2, t = lane & 3;
-    if (warp * 16 >= nrows) return;
-    const int stride = x_stride<WT>(a.KS);
-    const uint32_t wa_lo = smem_u32(ws) + static_cast<uint32_t>((warp * 16 + g) * wst + t * 16);
-    const uint32_t wa_hi = wa_lo + static_cast<uint32_t>(8 * wst);
-    const uint32_t xbase = smem_u32(xs) + static_cast<uint32_t>(g * stride) +
+    const uint32_t swz = static_cast<uint32_t>((g & 1) << 2);  // unit ^= 4 on odd rows
+    const uint32_t xbase = smem_u32(xbuf) + static_cast<uint32_t>(g * xst) +
                            static_cast<uint32_t>(WT == I4 ? t * 32 : t * 16);
-    constexpr int KBB = (WT == I4) ? G::KB / 2 : G::KB * (WT == BF16 ? 2 : 1);  // weight bytes per block
-
-    float facc[MT][2][4];
-    int iacc[MT][2][4];
+    const int nblk = KS / G::KB;
+    for (int tile = lo + warp; tile < hi; tile += kStreamConsumers) {
+        const int k = tile - lo, slot = k % nst;
+        const uint32_t ph = static_cast<uint32_t>(k / nst) & 1u;
+        mbar_wait(&full[slot], ph);
+        const uint32_t rb = smem_u32(ring + slot * ibytes);
+        const uint32_t row_lo = rb + static_cast<uint32_t>(g * ksb);
+        const uint32_t row_hi = row_lo + static_cast<uint32_t>(8 * ksb);
+        float facc[MT][2][4];
+        int iacc[MT][2][4];
 #pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
+            for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                facc[mt][hh][i] = 0.f;
-                iacc[mt][hh][i] = 0;
-            }
-
-    const int nblk = a.KS / G::KB;
+                for (int i = 0; i < 4; ++i) {
+                    facc[mt][hh][i] = 0.f;
+                    iacc[mt][hh][i] = 0;
+                }
 #pragma unroll 2
-    for (int b = 0; b < nblk; ++b) {
-        const uint4 wl = lds128(wa_lo + b * KBB);
-        const uint4 wh = lds128(wa_hi + b * KBB);
-        const uint32_t xk = static_cast<uint32_t>(b * G::KB * G::XB);
-        uint32_t la[8], ha[8];
-        if (WT == I4) {
-            unpack_s4x8(wl.x, la[0], la[1]); unpack_s4x8(wl.y, la[2], la[3]);
-            unpack_s4x8(wl.z, la[4], la[5]); unpack_s4x8(wl.w, la[6], la[7]);
-            unpack_s4x8(wh.x, ha[0], ha[1]); unpack_s4x8(wh.y, ha[2], ha[3]);
-            unpack_s4x8(wh.z, ha[4], ha[5]); unpack_s4x8(wh.w, ha[6], ha[7]);
-        }
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt) {
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-                const uint32_t xa = xbase + static_cast<uint32_t>((mt * 16 + hh * 8) * stride) + xk;
-                if (WT == BF16) {
-                    const uint4 xv = lds128(xa);
-                    mma_bf16_16816(facc[mt][hh], wl.x, wh.x, wl.y, wh.y, xv.x, xv.y);
-                    mma_bf16_16816(facc[mt][hh], wl.z, wh.z, wl.w, wh.w, xv.z, xv.w);
-                } else if (WT == I8) {
-                    const uint4 xv = lds128(xa);
-                    mma_s8_16832(iacc[mt][hh], wl.x, wh.x, wl.y, wh.y, xv.x, xv.y);
-                    mma_s8_16832(iacc[mt][hh], wl.z, wh.z, wl.w, wh.w, xv.z, xv.w);
-                } else {
-                    const uint4 x0 = lds128(xa), x1 = lds128(xa + 16);
-                    mma_s8_16832(iacc[mt][hh], la[0], ha[0], la[1], ha[1], x0.x, x0.y);
-                    mma_s8_16832(iacc[mt][hh], la[2], ha[2], la[3], ha[3], x0.z, x0.w);
-                    mma_s8_16832(iacc[mt][hh], la[4], ha[4], la[5], ha[5], x1.x, x1.y);
-                    mma_s8_16832(iacc[mt][hh], la[6], ha[6], la[7], ha[7], x1.z, x1.w);
-                }
+        for (int b = 0; b < nblk; ++b) {
+            // this lane's 16-byte unit of block b: logical unit 4b + t
+            const uint32_t uoff = ((static_cast<uint32_t>(4 * b + t)) ^ swz) * 16;
+            const uint4 wl = lds128(row_lo + uoff);
+            const uint4 wh = lds128(row_hi + uoff);
+            const uint32_t xk = static_cast<uint32_t>(b * G::KB * G::XB);
+            uint32_t la[8], ha[8];
+            if (WT == I4) {
+                unpack_s4x8(wl.x, la[0], la[1]); unpack_s4x8(wl.y, la[2], la[3]);
+                unpack_s4x8(wl.z, la[4], la[5]); unpack_s4x8(wl.w, la[6], la[7]);
+                unpack_s4x8(wh.x, ha[0], ha[1]); unpack_s4x8(wh.y, ha[2], ha[3]);
+                unpack_s4x8(wh.z, ha[4], ha[5]); unpack_s4x8(wh.w, ha[6], ha[7]);
             }
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh) {
+                    const uint32_t xa = xbase + static_cast<uint32_t>((mt * 16 + hh * 8) * xst) + xk;
+                    if (WT == BF16) {
+                        const uint4 xv = lds128(xa);
+                        mma_bf16_16816(facc[mt][hh], wl.x, wh.x, wl.y, wh.y, xv.x, xv.y);
+                        mma_bf16_16816(facc[mt][hh], wl.z, wh.z, wl.w, wh.w, xv.z, xv.w);
+                    } else if (WT == I8) {
+                        const uint4 xv = lds128(xa);
+                        mma_s8_16832(iacc[mt][hh], wl.x, wh.x, wl.y, wh.y, xv.x, xv.y);
+                        mma_s8_16832(iacc[mt][hh], wl.z, wh.z, wl.w, wh.w, xv.z, xv.w);
+                    } else {
+                        const uint4 x0 = lds128(xa), x1 = lds128(xa + 16);
+                        mma_s8_16832(iacc[mt][hh], la[0], ha[0], la[1], ha[1], x0.x, x0.y);
+                        mma_s8_16832(iacc[mt][hh], la[2], ha[2], la[3], ha[3], x0.z, x0.w);
+                        mma_s8_16832(iacc[mt][hh], la[4], ha[4], la[5], ha[5], x1.x, x1.y);
+                        mma_s8_16832(iacc[mt][hh], la[6], ha[6], la[7], ha[7], x1.z, x1.w);
+                    }
+                }
         }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        // D fragment: (row g | g+8, token 2t | 2t+1) of each m16n8 tile
+        const size_t pbase = static_cast<size_t>(s) * a.M * a.N;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int n = tile * 16 + g + ((i & 2) ? 8 : 0);
+                    const int m = mt * 16 + hh * 8 + 2 * t + (i & 1);
+                    if (n < a.N && m < a.M) {
+                        const size_t o = pbase + static_cast<size_t>(m) * a.N + n;
+                        if (WT == BF16) reinterpret_cast<float*>(a.P)[o] = facc[mt][hh][i];
+                        else reinterpret_cast<int*>(a.P)[o] = iacc[mt][hh][i];
+                    }
+                }
     }
-
-    // D fragment: (row g | g+8, token 2t | 2t+1) of each m16n8 tile
-    const int n0 = nc0 + warp * 16;
-    const size_t pbase = static_cast<size_t>(split) * a.M * a.N;
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-        for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int n = n0 + g + ((i & 2) ? 8 : 0);
-                const int m = mt * 16 + hh * 8 + 2 * t + (i & 1);
-                if (n < a.N && m < a.M) {
-                    const size_t o = pbase + static_cast<size_t>(m) * a.N + n;
-                    if (WT == BF16) reinterpret_cast<float*>(a.P)[o] = facc[mt][hh][i];
-                    else reinterpret_cast<int*>(a.P)[o] = iacc[mt][hh][i];
-                }
-            }
 }
 
-// fp32 weights (config 1): CUDA-core GEMV, one warp per weight row at a time.
+// fp32 weights (config 1): CUDA-core GEMV over the plain [N][Kp] layout, one
+// warp per weight row at a time.
 constexpr int kF32Rows = 32;
-__global__ void __launch_bounds__(kGemmThreads) skinny_f32_kernel(const GemmArgs a) {
+constexpr int kF32Threads = 128;
+__global__ void __launch_bounds__(kF32Threads) skinny_f32_kernel(const GemmArgs a) {
     extern __shared__ __align__(16) float xsf[];
     const int split = blockIdx.y;
+    if (a.commit_len && blockIdx.x == 0 && split == 0 && threadIdx.x == 0) atomicAdd(a.commit_len, 1);
     const int k0 = split * a.KS;
     const float* X = reinterpret_cast<const float*>(a.X);
-    for (int i = threadIdx.x; i < a.M * a.KS; i += kGemmThreads) {
+    for (int i = threadIdx.x; i < a.M * a.KS; i += kF32Threads) {
         const int m = i / a.KS, kk = i - m * a.KS;
         const int k = k0 + kk;
         xsf[i] = (k < a.K) ? X[static_cast<size_t>(m) * a.ldx + k] : 0.f;
@@ -257,65 +324,65 @@ __global__ void __launch_bounds__(kGemmThreads) skinny_f32_kernel(const GemmArgs
             }
 #pragma unroll
             for (int mm = 0; mm < 8; ++mm) {
-                const float s = warp_sum(acc[mm]);
+                const float sum = warp_sum(acc[mm]);
                 if (lane == 0 && m0 + mm < a.M)
-                    reinterpret_cast<float*>(a.P)[(static_cast<size_t>(split) * a.M + m0 + mm) * a.N + n] = s;
+                    reinterpret_cast<float*>(a.P)[(static_cast<size_t>(split) * a.M + m0 + mm) * a.N + n] = sum;
             }
         }
     }
 }
 
 template <int WT, int MT>
-cudaError_t launch_mma(const GemmArgs& a, cudaStream_t s) {
-    const int smem = gemm_smem_bytes(WT, a.M, a.KS);
-    auto k = skinny_mma_kernel<WT, MT>;
+cudaError_t launch_stream(const GemmArgs& a, cudaStream_t s) {
+    using S = StreamCfg<WT, MT>;
+    if (S::stages(a.KS) < 2) return cudaErrorInvalidConfiguration;
+    const int smem = S::smem(a.KS);
+    auto k = skinny_stream_kernel<WT, MT>;
     static int attr_smem = 0;
     if (smem > attr_smem) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr_smem = smem;
     }
-    dim3 grid((a.N + kRowsPerCta - 1) / kRowsPerCta, a.Kp / a.KS);
-    k<<<grid, kGemmThreads, smem, s>>>(a);
+    const int splits = a.Kp / a.KS;
+    const int grid = splits <= a.grid ? (a.grid / splits) * splits : splits;
+    k<<<grid, kStreamThreads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int WT>
 cudaError_t launch_wt(const GemmArgs& a, cudaStream_t s) {
-    const int mt = (a.M + 15) / 16;
-    switch (mt) {
-        case 1: return launch_mma<WT, 1>(a, s);
-        case 2: return launch_mma<WT, 2>(a, s);
-        case 3: case 4: return launch_mma<WT, 4>(a, s);
-        case 5: case 6: case 7: case 8: return launch_mma<WT, 8>(a, s);
+    switch ((a.M + 15) / 16) {
+        case 1: return launch_stream<WT, 1>(a, s);
+        case 2: return launch_stream<WT, 2>(a, s);
+        case 3: case 4: return launch_stream<WT, 4>(a, s);
+        case 5: case 6: case 7: case 8: return launch_stream<WT, 8>(a, s);
     }
-    return cudaErrorInvalidValue;  // M > 128: caller tiles over M
+    return cudaErrorInvalidValue;  // M > 128: the caller tiles over M
 }
 
 __global__ void reduce_partials_kernel(const float* __restrict__ P, int splits, int MN,
                                        float* __restrict__ y) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= MN) return;
-    float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += P[static_cast<size_t>(k) * MN + i];
-    y[i] = s;
+    float sum = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < splits; ++k) sum += __ldcg(P + static_cast<size_t>(k) * MN + i);
+    y[i] = sum;
 }
-
-int w_stride_h(int b) { return b + ((64 - (b & 127)) & 127); }
 
 }  // namespace
 
-int gemm_smem_bytes(int wdtype, int M, int KS) {
-    // rows staged = the kernel's MT bucket (1, 2, 4 or 8 tiles of 16)
+bool gemm_fits(int wdtype, int M, int KS) {
     const int mt = (M + 15) / 16;
-    const int Mp = 16 * (mt <= 2 ? mt : (mt <= 4 ? 4 : 8));
+    auto st = [&](auto cfg) { return decltype(cfg)::stages(KS) >= 2; };
     switch (wdtype) {
-        case BF16: return kRowsPerCta * w_stride_h(KS * 2) + Mp * (KS * 2 + GT<BF16>::XPAD) + 16;
-        case I8: return kRowsPerCta * w_stride_h(KS) + Mp * (KS + GT<I8>::XPAD) + 16;
-        case I4: return kRowsPerCta * w_stride_h(KS / 2) + Mp * (KS + GT<I4>::XPAD) + 16;
-        case F32: return M * KS * 4;
+        case BF16: return mt <= 1 ? st(StreamCfg<BF16, 1>{}) : mt <= 2 ? st(StreamCfg<BF16, 2>{}) : mt <= 4 ? st(StreamCfg<BF16, 4>{}) : st(StreamCfg<BF16, 8>{});
+        case I8: return mt <= 1 ? st(StreamCfg<I8, 1>{}) : mt <= 2 ? st(StreamCfg<I8, 2>{}) : mt <= 4 ? st(StreamCfg<I8, 4>{}) : st(StreamCfg<I8, 8>{});
+        case I4: return mt <= 1 ? st(StreamCfg<I4, 1>{}) : mt <= 2 ? st(StreamCfg<I4, 2>{}) : mt <= 4 ? st(StreamCfg<I4, 4>{}) : st(StreamCfg<I4, 8>{});
+        case F32: return M * KS * 4 <= 200 * 1024;
     }
-    return 0;
+    return false;
 }
 
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s) {
@@ -324,7 +391,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s) {
         case I8: return launch_wt<I8>(a, s);
         case I4: return launch_wt<I4>(a, s);
         case F32: {
-            const int smem = gemm_smem_bytes(F32, a.M, a.KS);
+            const int smem = a.M * a.KS * 4;
             static int attr_smem = 0;
             if (smem > attr_smem) {
                 cudaError_t e = cudaFuncSetAttribute(skinny_f32_kernel,
@@ -333,7 +400,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s) {
                 attr_smem = smem;
             }
             dim3 grid((a.N + kF32Rows - 1) / kF32Rows, a.Kp / a.KS);
-            skinny_f32_kernel<<<grid, kGemmThreads, smem, s>>>(a);
+            skinny_f32_kernel<<<grid, kF32Threads, smem, s>>>(a);
             return cudaGetLastError();
         }
     }

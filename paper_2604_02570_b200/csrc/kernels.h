@@ -13,16 +13,21 @@ enum DType { F32 = 0, BF16 = 1, I8 = 2, I4 = 3 };
 // Partial skinny GEMM  P[split][m][n] = sum_{k in split} X[m][k] * W[n][k]
 // (W K-major).  bf16: X fp32 -> bf16, fp32 partials.  i8 / i4: X int8,
 // int32 partials (exact).  f32: CUDA-core fp32.
+// bf16 / i8 / i4 weights are W-tiles: [N/16][Kp/KS][16][KS bytes-of-row],
+// 16-byte units of odd rows XOR 4 (see pack in capi.cu); f32 is plain [N][Kp].
 struct GemmArgs {
-    const void* W;   // [N][Kp] (bf16 / f32 / i8) or [N][Kp/2] (i4)
+    const void* W;   // W-tiles (bf16 / i8 / i4) or [N][Kp] (f32)
     const void* X;   // fp32 [M][ldx] (f32 / bf16 modes) or int8 [M][Kp]
     void* P;         // [splits][M][N] fp32 or int32
     int M, N, K;     // K: valid columns of X (fp32 modes); Kp: padded K
     int Kp, KS;      // KS: K per split (Kp % KS == 0)
     int ldx;         // row stride of fp32 X (elements)
     int wdtype;      // DType
+    int grid;        // SM count: the streaming kernel runs floor(grid/splits)*splits CTAs
+    int* commit_len; // non-null: one thread adds 1 to it (the layer step's length commit)
 };
-int gemm_smem_bytes(int wdtype, int M, int KS);
+// true when M token rows with split KS fit the streaming kernel's shared memory
+bool gemm_fits(int wdtype, int M, int KS);
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s);
 
 // Sum split partials into fp32 y [M][N] (fixed split order).
@@ -59,6 +64,8 @@ struct AppendArgs {
     float* q_out;         // [M][nh][H] or null
     float* qt;            // [M][nh][R] absorbed query (log2 domain) or null
     float qt_scale;       // log2(e) / sqrt(H)
+    const float* mqk;     // [nh][R][R] qt_scale * B_Q . B_K^T (used when q_out is null)
+    int commit;           // 1: the last CTA advances *d_len by T
 };
 cudaError_t launch_append_epilogue(const AppendArgs& a, cudaStream_t s);
 
@@ -79,10 +86,12 @@ struct AttnArgs {
     const void* bv;         // B_V [nh][R][H]
     const float* bv_scale;  // [nh][H]
     int bdtype;
-    float* out;             // [B][nh][H]
-    float* ws;              // [B*nh][max_chunks][R+2]
+    float* out;             // [B][nh][H] (null: latent output only)
+    float* vlat;            // [B][nh][R] latent output acc/denom (may be null)
+    float* ws;              // [B*nh][max_chunks][warps][R+2]
     int* counters;          // [B*nh], zero between launches (self-resetting)
-    const int* d_len;       // valid rows (device)
+    const int* d_len;       // committed rows (device); the kernel attends over *d_len + len_add
+    int len_add;            // 1 when the step's own row is appended but not yet committed
     int B, nh, H, R, cap, chunk, max_chunks, cdtype, row_bytes;
     int grid;               // persistent CTAs
 };
