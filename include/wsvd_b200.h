@@ -177,6 +177,15 @@ int wsvd_layer_step_host(wsvd_cache_t cache, const float* x_host, float* y_host,
  * calls with the same arguments replay it (1 launch instead of ~5). */
 int wsvd_layer_step_graph(wsvd_cache_t cache, const float* x, float* y, void* stream);
 
+/* ----------------------------------------------------- host utilities ---
+ * The reference weight quantiser (quant::quantize_weight, quant.cpp:99-119):
+ * per-column symmetric round-to-nearest (ties away from zero), clip ratio
+ * searched over 0.50..1.00 (first minimum wins), zero columns get scale 1.
+ * w row-major rows x cols fp64 -> q int8 (values in +-(2^(bits-1)-1)),
+ * scales[cols], *clip.  Host only; what wsvd_layer_set_head uses for I8/I4. */
+int wsvd_quantize_weight(const double* w, int64_t rows, int64_t cols, int32_t bits, int8_t* q,
+                         double* scales, double* clip);
+
 /* ----------------------------------------------------- traffic counters --
  * Closed-form TrafficCounter increments (decode.cpp:132-149, 176-203;
  * test_decode.cpp:229-292) for one call on this cache, ADDED to counter21

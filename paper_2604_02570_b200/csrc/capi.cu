@@ -1019,6 +1019,22 @@ int wsvd_layer_step_host(wsvd_cache_t c, const float* x_host, float* y_host, voi
     return WSVD_OK;
 }
 
+int wsvd_quantize_weight(const double* w, int64_t rows, int64_t cols, int32_t bits, int8_t* q,
+                         double* scales, double* clip) {
+    if (!w || !q || !scales) return set_err(WSVD_ECONFIG, "null argument");
+    if (bits != 4 && bits != 8) return set_err(WSVD_ECONFIG, "bit width must be 4 or 8");
+    if (rows <= 0 || cols <= 0) return set_err(WSVD_ESHAPE, "empty matrix");
+    for (int64_t i = 0; i < rows * cols; ++i)
+        if (!std::isfinite(w[i])) return set_err(WSVD_ENUMERIC, "quantize input: non-finite entry");
+    std::vector<double> wv(w, w + rows * cols), s;
+    std::vector<int8_t> qv;
+    const double c = quantize_weight_ref(wv, static_cast<size_t>(rows), static_cast<size_t>(cols), bits, qv, s);
+    std::memcpy(q, qv.data(), qv.size());
+    std::memcpy(scales, s.data(), s.size() * sizeof(double));
+    if (clip) *clip = c;
+    return WSVD_OK;
+}
+
 int wsvd_traffic_append(wsvd_cache_t c, uint64_t* k) {
     if (!c || !k) return set_err(WSVD_ECONFIG, "null argument");
     wsvd_layer_s* L = c->L;
