@@ -31,6 +31,8 @@ __global__ void __launch_bounds__(kAqThreads) act_quant_kernel(const float* __re
     extern __shared__ float v[];  // [E]
     __shared__ float wmax[kAqThreads / 32];
     const int m = blockIdx.x;
+    griddep_wait();
+    griddep_launch_dependents();
     const float* xm = x + static_cast<size_t>(m) * E;
     for (int i = threadIdx.x; i < E; i += kAqThreads) v[i] = xm[i];
     if (rot) {
@@ -103,6 +105,8 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
     const int h = blockIdx.x, m = blockIdx.y;
     const int b = m % a.B, tpos = m / a.B;  // rows are token-major: m = tpos * B + b
     const int R = a.R, H = a.H;
+    griddep_wait();
+    griddep_launch_dependents();
     const int pos = *a.d_len + tpos;
 
     // ---- latents: fixed-order sum of the K-split partials (+ dequant)
@@ -226,6 +230,8 @@ __global__ void __launch_bounds__(kEpThreads) absorb_query_kernel(const float* _
                                                                   float scale, float* qt) {
     extern __shared__ float qs[];
     const int h = blockIdx.x, b = blockIdx.y;
+    griddep_wait();
+    griddep_launch_dependents();
     const size_t o = (static_cast<size_t>(b) * nh + h);
     for (int j = threadIdx.x; j < H; j += kEpThreads) qs[j] = q[o * H + j];
     __syncthreads();
@@ -243,15 +249,13 @@ cudaError_t launch_act_quant(const float* x, int M, int E, int Kp, int rot, int 
         if (e != cudaSuccess) return e;
         attr_smem = smem;
     }
-    act_quant_kernel<<<M, kAqThreads, smem, s>>>(x, E, Kp, rot, rot_blk, rot_scale, xq, sx);
-    return cudaGetLastError();
+    return launch_pdl(act_quant_kernel, dim3(M), dim3(kAqThreads), smem, s, x, E, Kp, rot, rot_blk, rot_scale,
+                      xq, sx);
 }
 
 cudaError_t launch_append_epilogue(const AppendArgs& a, cudaStream_t s) {
     const int smem = (3 * a.R + a.H) * 4;
-    dim3 grid(a.nh, a.M);
-    append_epilogue_kernel<<<grid, kEpThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(append_epilogue_kernel, dim3(a.nh, a.M), dim3(kEpThreads), smem, s, a);
 }
 
 cudaError_t launch_push_rows(const uint8_t* rows, int n, uint8_t* cache, int cap, int row_bytes,
@@ -264,9 +268,8 @@ cudaError_t launch_push_rows(const uint8_t* rows, int n, uint8_t* cache, int cap
 cudaError_t launch_absorb_query(const float* q, int B, int nh, int R, int H, const void* bk,
                                 const float* bk_scale, int bdtype, float qt_scale, float* qt,
                                 cudaStream_t s) {
-    dim3 grid(nh, B);
-    absorb_query_kernel<<<grid, kEpThreads, H * 4, s>>>(q, nh, R, H, bk, bk_scale, bdtype, qt_scale, qt);
-    return cudaGetLastError();
+    return launch_pdl(absorb_query_kernel, dim3(nh, B), dim3(kEpThreads), H * 4, s, q, nh, R, H, bk, bk_scale,
+                      bdtype, qt_scale, qt);
 }
 
 }  // namespace wsvd_k

@@ -128,6 +128,19 @@ struct Unit {
     int bh, chunk, t0, ntok;
 };
 
+// Split of one (sequence, head) into chunks for this launch.  a.chunk > 0
+// fixes the chunk length (tests); otherwise up to a.max_chunks chunks of equal
+// length (a multiple of 32 tokens), so every unit carries real work.
+WSVD_DEV void chunking(const AttnArgs& a, int len, int& nch, int& chunk) {
+    if (a.chunk > 0) {
+        chunk = a.chunk;
+    } else {
+        const int n = max(1, min(a.max_chunks, (len + 31) / 32));
+        chunk = (((len + n - 1) / n) + 31) & ~31;
+    }
+    nch = (len + chunk - 1) / chunk;
+}
+
 WSVD_DEV Unit unit_geom(int u, int nch, int chunk, int len) {
     Unit g;
     g.bh = u / nch;
@@ -160,14 +173,11 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
     float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int len = *a.d_len + a.len_add;
-    if (len <= 0) return;
-    const int nch = (len + a.chunk - 1) / a.chunk;
-    const int n_units = a.B * a.nh * nch;
     const size_t cap = static_cast<size_t>(a.cap);
 
     // Zero the stage ring once: rows past a stage's valid end are read by the
-    // MMAs (times p = 0) and must hold finite values.
+    // MMAs (times p = 0) and must hold finite values.  This prologue overlaps
+    // the previous kernel (programmatic dependent launch).
     for (int i = tid; i < C::STAGES * C::STAGE / 16; i += kThreads)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -179,6 +189,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
         fence_mbar_init();
     }
     __syncthreads();
+    griddep_wait();  // the appended row, qt and the length come from the predecessor
+    griddep_launch_dependents();
+    const int len = *a.d_len + a.len_add;
+    if (len <= 0) return;
+    int nch, chunk;
+    chunking(a, len, nch, chunk);
+    const int n_units = a.B * a.nh * nch;
 
     // ======================================================== producer warp
     if (warp == kConsumerWarps) {
@@ -187,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
             int slot = 0;
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const Unit g = unit_geom(u, nch, a.chunk, len);
+                const Unit g = unit_geom(u, nch, chunk, len);
                 const uint8_t* src = a.cache + (static_cast<size_t>(g.bh) * cap + g.t0) * C::ROWB;
                 const __half2* ssrc = a.cscale + static_cast<size_t>(g.bh) * cap + g.t0;
                 for (int s = 0; s * kStageTok < g.ntok; ++s) {
@@ -221,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
     int slot = 0;
     uint32_t phase = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-        const Unit g = unit_geom(u, nch, a.chunk, len);
+        const Unit g = unit_geom(u, nch, chunk, len);
         float m_w = -INFINITY, l = 0.f;
         const int ns = (g.ntok + kStageTok - 1) / kStageTok;
         float wacc[2 * (R / 16 > 0 ? R / 16 : 1)];  // MMA path: this lane's acc rows (t4 == 0)
@@ -431,9 +448,12 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
 __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a, int parts_per_chunk) {
     extern __shared__ float sm[];  // parts [np][R+2], then vt [R]
     const int bh = blockIdx.x, tid = threadIdx.x, R = a.R;
+    griddep_wait();
+    griddep_launch_dependents();
     const int len = *a.d_len + a.len_add;
     if (len <= 0) return;
-    const int nch = (len + a.chunk - 1) / a.chunk;
+    int nch, chunk;
+    chunking(a, len, nch, chunk);
     const int np = nch * parts_per_chunk;
     float* part = sm;
     float* vt = sm + a.max_chunks * parts_per_chunk * (R + 2);
@@ -481,8 +501,7 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
             if (e != cudaSuccess) return e;
             attr_set = true;
         }
-        k<<<a.grid, kThreads, C::SMEM, s>>>(a);
-        cudaError_t e = cudaGetLastError();
+        cudaError_t e = launch_pdl(k, dim3(a.grid), dim3(kThreads), C::SMEM, s, a);
         if (e != cudaSuccess) return e;
         const int csmem = (a.max_chunks * kConsumerWarps * (R + 2) + R) * 4;
         static int cattr = 0;
@@ -491,8 +510,8 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
             if (e != cudaSuccess) return e;
             cattr = csmem;
         }
-        attn_combine_kernel<<<a.B * a.nh, 128, csmem, s>>>(a, kConsumerWarps);
-        return cudaGetLastError();
+        return launch_pdl(attn_combine_kernel, dim3(a.B * a.nh), dim3(128), csmem, s, a,
+                          static_cast<int>(kConsumerWarps));
     }
 }
 

@@ -715,14 +715,16 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     CUDA_TRY(cudaGetDeviceProperties(&p, L->d.device));
     c->sms = p.multiProcessorCount;
     c->grid = c->sms * attn_occupancy(cache_dtype, L->R);
-    // chunk: ~16 units per CTA at full capacity, multiple of 128 tokens
-    long units_target = static_cast<long>(c->grid) * 16;
-    long tok = static_cast<long>(c->cap_alloc) * batch * nh;
-    int chunk = static_cast<int>(round_up(static_cast<int>(std::max(1L, tok / units_target)), 128));
-    chunk = std::max(128, std::min(chunk, 8192));
-    if (const char* env = getenv("WSVD_ATTN_CHUNK")) chunk = std::max(128, round_up(atoi(env), 128));
-    c->chunk = chunk;
-    c->max_chunks = (c->cap_alloc + chunk - 1) / chunk;
+    // split-KV: each (sequence, head) is cut into up to max_chunks equal chunks
+    // per launch (attn.cu chunking()), ~12 units per persistent CTA
+    c->chunk = 0;
+    int units = 4;  // target units per persistent CTA (measured best: 2 chunks at B16 ctx4K)
+    if (const char* env = getenv("WSVD_ATTN_UNITS")) units = std::max(1, atoi(env));
+    c->max_chunks = std::max(1, std::min(64, (units * c->grid + batch * nh - 1) / (batch * nh)));
+    if (const char* env = getenv("WSVD_ATTN_CHUNK")) {  // fixed chunk length (tests)
+        c->chunk = std::max(32, round_up(atoi(env), 32));
+        c->max_chunks = (c->cap_alloc + c->chunk - 1) / c->chunk;
+    }
     const size_t rows = static_cast<size_t>(batch) * nh * c->cap_alloc;
     cudaError_t e = c->data.alloc(rows * c->row_bytes);
     if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4);

@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 #define WSVD_DEV __device__ __forceinline__
 
 namespace wsvd_dev {
@@ -35,6 +38,32 @@ WSVD_DEV void unpack_s4x8(uint32_t w, uint32_t& lo4, uint32_t& hi4) {
     odd = __vsub4(odd ^ 0x08080808u, 0x08080808u);
     lo4 = __byte_perm(even, odd, 0x5140);   // e0 o0 e1 o1 -> elements 0..3
     hi4 = __byte_perm(even, odd, 0x7362);   // e2 o2 e3 o3 -> elements 4..7
+}
+
+// --------------------------------------- programmatic dependent launch (PDL)
+// Every kernel of the step is launched with programmatic stream serialisation:
+// it may start while its predecessor drains, runs its independent prologue,
+// then griddep_wait()s before touching the predecessor's outputs, and only
+// after that lets its own dependents launch (so a kernel never overlaps
+// anything older than its immediate predecessor).
+WSVD_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+WSVD_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    static const bool off = std::getenv("WSVD_NO_PDL") != nullptr;  // A/B switch for profiling
+    cfg.numAttrs = off ? 0 : 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // ---------------------------------------------------------- cache swizzle

@@ -165,7 +165,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1) skinny_stream_kernel(const 
     uint64_t* full = reinterpret_cast<uint64_t*>(xbuf + S::xbytes(KS));
     uint64_t* empty = full + 8;
 
-    if (a.commit_len && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.commit_len, 1);
     const int splits = a.Kp / KS;
     const int cps = gridDim.x / splits;  // CTAs per split
     const int s = blockIdx.x % splits, j = blockIdx.x / splits;
@@ -202,6 +201,11 @@ __global__ void __launch_bounds__(kStreamThreads, 1) skinny_stream_kernel(const 
     }
 
     // ------------------------------------------------ consumers
+    // the weight stream above needs nothing from the previous kernel; the
+    // token slice, the partial outputs and the length commit do
+    griddep_wait();
+    griddep_launch_dependents();
+    if (a.commit_len && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.commit_len, 1);
     stage_x<WT>(a, xbuf, s * KS, S::XROWS);
     named_bar_sync(1, 32 * kStreamConsumers);
 
@@ -292,6 +296,8 @@ constexpr int kF32Threads = 128;
 __global__ void __launch_bounds__(kF32Threads) skinny_f32_kernel(const GemmArgs a) {
     extern __shared__ __align__(16) float xsf[];
     const int split = blockIdx.y;
+    griddep_wait();
+    griddep_launch_dependents();
     if (a.commit_len && blockIdx.x == 0 && split == 0 && threadIdx.x == 0) atomicAdd(a.commit_len, 1);
     const int k0 = split * a.KS;
     const float* X = reinterpret_cast<const float*>(a.X);
@@ -346,8 +352,7 @@ cudaError_t launch_stream(const GemmArgs& a, cudaStream_t s) {
     }
     const int splits = a.Kp / a.KS;
     const int grid = splits <= a.grid ? (a.grid / splits) * splits : splits;
-    k<<<grid, kStreamThreads, smem, s>>>(a);
-    return cudaGetLastError();
+    return launch_pdl(k, dim3(grid), dim3(kStreamThreads), smem, s, a);
 }
 
 template <int WT>
@@ -363,6 +368,8 @@ cudaError_t launch_wt(const GemmArgs& a, cudaStream_t s) {
 
 __global__ void reduce_partials_kernel(const float* __restrict__ P, int splits, int MN,
                                        float* __restrict__ y) {
+    griddep_wait();
+    griddep_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= MN) return;
     float sum = 0.f;
@@ -400,8 +407,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s) {
                 attr_smem = smem;
             }
             dim3 grid((a.N + kF32Rows - 1) / kF32Rows, a.Kp / a.KS);
-            skinny_f32_kernel<<<grid, kF32Threads, smem, s>>>(a);
-            return cudaGetLastError();
+            return launch_pdl(skinny_f32_kernel, grid, dim3(kF32Threads), smem, s, a);
         }
     }
     return cudaErrorInvalidValue;
@@ -410,8 +416,7 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s) {
 cudaError_t launch_reduce_partials(const float* P, int splits, int M, int N, float* y,
                                    cudaStream_t s) {
     const int MN = M * N;
-    reduce_partials_kernel<<<(MN + 255) / 256, 256, 0, s>>>(P, splits, MN, y);
-    return cudaGetLastError();
+    return launch_pdl(reduce_partials_kernel, dim3((MN + 255) / 256), dim3(256), 0, s, P, splits, MN, y);
 }
 
 }  // namespace wsvd_k

@@ -1,0 +1,20 @@
+#!/usr/bin/env bash
+# Round-end evidence on one B200 (run under gpurun from the repo root):
+#   bench line (ours + reference arm), per-launch device times, ncu full
+#   captures of the dominant kernel and the projection GEMM.
+set -u
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.limit --format=csv > gpurun_out/gpu.txt
+python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
+python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+python tools/timing.py > gpurun_out/timing.txt 2>&1
+# prefill = 1024 kernel launches matching the filter; then the timed decode steps
+FILTER='regex:skinny_stream|append_epilogue|decode_attn|attn_combine|reduce_partials|act_quant'
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k "$FILTER" -s 1024 -c 40 --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:decode_attn -s 3 -c 1 \
+    -o gpurun_out/attn_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:skinny_stream -s 513 -c 1 \
+    -o gpurun_out/gemm_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
+ls -la gpurun_out
