@@ -177,6 +177,13 @@ int wsvd_layer_step_host(wsvd_cache_t cache, const float* x_host, float* y_host,
  * calls with the same arguments replay it (1 launch instead of ~5). */
 int wsvd_layer_step_graph(wsvd_cache_t cache, const float* x, float* y, void* stream);
 
+/* Copies internal per-step buffers of the last append to the host, for
+ * bit-exact parity checks of the integer path: what = 0 quantised tokens
+ * int8 [rows][Kp]; 1 token scales fp32 [rows]; 2 projection accumulators
+ * summed over K splits, int32 (I8/I4) or fp32, [rows][n_heads*3*rpad];
+ * 3 absorbed queries fp32 [batch][n_heads][rpad].  *bytes is in/out. */
+int wsvd_cache_debug_copy(wsvd_cache_t cache, int32_t what, void* host, int64_t* bytes);
+
 /* ----------------------------------------------------- host utilities ---
  * The reference weight quantiser (quant::quantize_weight, quant.cpp:99-119):
  * per-column symmetric round-to-nearest (ties away from zero), clip ratio

@@ -56,6 +56,7 @@ SIGNATURES = {
     "wsvd_layer_step": (C.c_int, [_vp, _fp, _fp, _fp, _vp]),
     "wsvd_layer_step_host": (C.c_int, [_vp, _fp, _fp, _vp]),
     "wsvd_layer_step_graph": (C.c_int, [_vp, _fp, _fp, _vp]),
+    "wsvd_cache_debug_copy": (C.c_int, [_vp, _i32, _vp, C.POINTER(C.c_int64)]),
     "wsvd_quantize_weight": (C.c_int, [C.POINTER(C.c_double), _i64, _i64, _i32, _i8p,
                                        C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "wsvd_traffic_append": (C.c_int, [_vp, _u64p]),

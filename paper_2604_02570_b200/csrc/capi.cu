@@ -233,7 +233,7 @@ struct wsvd_cache_s {
     DevBuf data, scales, ctrl;        // ctrl: [0]=d_len, [1]=done
     DevBuf qt, q_tmp, attn_ws, attn_cnt, vlat;
     DevBuf P, xq, sx;                 // projection workspace
-    int P_M = 0;                      // rows the projection workspace holds
+    int P_M = 0, P_splits = 0;        // rows / K splits of the last projection
     DevBuf oP, y_tmp;                 // O-proj partials
     DevBuf x_dev, y_dev;              // staging for the host-buffer step
     int chunk = 512, max_chunks = 1, grid = 148;
@@ -300,6 +300,8 @@ int run_projection(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* 
     }
     CUDA_TRY(launch_gemm(g, s));
     *splits_out = splits;
+    c->P_M = M;
+    c->P_splits = splits;
     return WSVD_OK;
 }
 
@@ -1019,6 +1021,51 @@ int wsvd_layer_step_host(wsvd_cache_t c, const float* x_host, float* y_host, voi
     CUDA_TRY(cudaMemcpyAsync(y_host, c->y_dev.p, yb, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
     return WSVD_OK;
+}
+
+int wsvd_cache_debug_copy(wsvd_cache_t c, int32_t what, void* host, int64_t* bytes) {
+    if (!c || !host || !bytes) return set_err(WSVD_ECONFIG, "null argument");
+    wsvd_layer_s* L = c->L;
+    CUDA_TRY(cudaSetDevice(L->d.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    const int M = c->P_M;
+    if (what == 0 || what == 1) {
+        const DevBuf& b = what == 0 ? c->xq : c->sx;
+        const size_t n = what == 0 ? static_cast<size_t>(M) * L->Kp : static_cast<size_t>(M) * 4;
+        if (!b.p || n > b.n) return set_err(WSVD_ECONFIG, "no quantised activations (not an I8/I4 layer?)");
+        if (*bytes < static_cast<int64_t>(n)) return set_err(WSVD_ESHAPE, "host buffer too small");
+        CUDA_TRY(cudaMemcpy(host, b.p, n, cudaMemcpyDeviceToHost));
+        *bytes = static_cast<int64_t>(n);
+        return WSVD_OK;
+    }
+    if (what == 2) {
+        const size_t per = static_cast<size_t>(M) * L->Nrows;
+        if (*bytes < static_cast<int64_t>(per * 4)) return set_err(WSVD_ESHAPE, "host buffer too small");
+        std::vector<uint8_t> all(per * 4 * c->P_splits);
+        CUDA_TRY(cudaMemcpy(all.data(), c->P.p, all.size(), cudaMemcpyDeviceToHost));
+        const bool ints = L->d.weight_dtype == WSVD_I8 || L->d.weight_dtype == WSVD_I4;
+        for (size_t i = 0; i < per; ++i) {
+            if (ints) {
+                int32_t s = 0;
+                for (int k = 0; k < c->P_splits; ++k) s += reinterpret_cast<const int32_t*>(all.data())[k * per + i];
+                static_cast<int32_t*>(host)[i] = s;
+            } else {
+                float s = 0.f;
+                for (int k = 0; k < c->P_splits; ++k) s += reinterpret_cast<const float*>(all.data())[k * per + i];
+                static_cast<float*>(host)[i] = s;
+            }
+        }
+        *bytes = static_cast<int64_t>(per * 4);
+        return WSVD_OK;
+    }
+    if (what == 3) {
+        const size_t n = static_cast<size_t>(c->B) * L->d.n_heads * L->R * 4;
+        if (*bytes < static_cast<int64_t>(n)) return set_err(WSVD_ESHAPE, "host buffer too small");
+        CUDA_TRY(cudaMemcpy(host, c->qt.p, n, cudaMemcpyDeviceToHost));
+        *bytes = static_cast<int64_t>(n);
+        return WSVD_OK;
+    }
+    return set_err(WSVD_ECONFIG, "unknown debug buffer");
 }
 
 int wsvd_quantize_weight(const double* w, int64_t rows, int64_t cols, int32_t bits, int8_t* q,

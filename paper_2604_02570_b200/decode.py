@@ -139,7 +139,11 @@ class DeviceLayer:
     """Device copy of (a head shard of) one layer's factors: wsvd_layer_t."""
 
     def __init__(self, f: LayerFactors, weight_dtype: str = "f32", device: int = 0,
-                 act_rotation: bool | None = None, head_offset: int = 0):
+                 act_rotation: bool | None = None, head_offset: int = 0, quantized=None):
+        """quantized: optional per head, per role (q, k, v) tuples
+        (a_q int8 E x r, a_scales r, b_q int8 r x H, b_scales H) -- already
+        rotated factors as quant::QuantizedFactors holds them (quant.hpp:98-107);
+        f then only supplies the geometry."""
         if not f.heads:
             raise ShapeError("latent cache over zero heads")
         if weight_dtype not in N.DTYPES:
@@ -163,6 +167,18 @@ class DeviceLayer:
         self.h = h
         for hi, p in enumerate(f.heads):
             for role, hf in enumerate((p.q, p.k, p.v)):
+                if quantized is not None:
+                    aq, as_, bq, bs = quantized[hi][role]
+                    aq = np.ascontiguousarray(aq, dtype=np.int8)
+                    bq = np.ascontiguousarray(bq, dtype=np.int8)
+                    as_ = np.ascontiguousarray(as_, dtype=np.float64)
+                    bs = np.ascontiguousarray(bs, dtype=np.float64)
+                    N.call("wsvd_layer_set_head_quantized", self.h, hi, role,
+                           aq.ctypes.data_as(C.POINTER(C.c_int8)),
+                           as_.ctypes.data_as(C.POINTER(C.c_double)),
+                           bq.ctypes.data_as(C.POINTER(C.c_int8)),
+                           bs.ctypes.data_as(C.POINTER(C.c_double)))
+                    continue
                 a = np.ascontiguousarray(hf.a, dtype=np.float64)
                 b = np.ascontiguousarray(hf.b, dtype=np.float64)
                 if a.shape != (f.embed_dim, hf.rank) or b.shape != (hf.rank, f.head_dim):

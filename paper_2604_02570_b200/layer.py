@@ -27,13 +27,14 @@ def _torch():
 class DecodeLayer:
     def __init__(self, f: LayerFactors, w_o_rows: np.ndarray | None, batch: int, capacity: int,
                  cache_dtype: str = "bf16", weight_dtype: str = "bf16", oproj_dtype: str = "bf16",
-                 device: int = 0, head_offset: int = 0, act_rotation: bool | None = None):
+                 device: int = 0, head_offset: int = 0, act_rotation: bool | None = None,
+                 quantized=None):
         if cache_dtype not in ("f32", "bf16", "i8"):
             raise ConfigError(f"unknown cache dtype '{cache_dtype}'")
         self.device = device
         self.batch = batch
         self.layer = DeviceLayer(f, weight_dtype, device, act_rotation=act_rotation,
-                                 head_offset=head_offset)
+                                 head_offset=head_offset, quantized=quantized)
         self.e_out = None
         if w_o_rows is not None:
             self.layer.set_oproj(w_o_rows, oproj_dtype)
@@ -118,6 +119,19 @@ class DecodeLayer:
         N.call("wsvd_cache_read_host", self.h, seq, head, ck.ctypes.data_as(C.POINTER(C.c_double)),
                cv.ctypes.data_as(C.POINTER(C.c_double)))
         return ck, cv
+
+    def debug_copy(self, what: str) -> np.ndarray:
+        """Internal buffers of the last append (see wsvd_cache_debug_copy)."""
+        code = {"xq": 0, "sx": 1, "acc": 2, "qt": 3}[what]
+        nbytes = C.c_int64(1 << 30)
+        buf = np.empty(1 << 28, dtype=np.uint8)
+        N.call("wsvd_cache_debug_copy", self.h, code, C.c_void_p(buf.ctypes.data), C.byref(nbytes))
+        raw = buf[: nbytes.value].copy()
+        if what == "xq":
+            return raw.view(np.int8)
+        if what == "acc":
+            return raw.view(np.int32 if self.layer.weight_dtype in ("i8", "i4") else np.float32)
+        return raw.view(np.float32)
 
     def read_raw(self, seq: int, head: int):
         L = self.length()
