@@ -488,6 +488,8 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a, int
     }
 }
 
+int g_combine_smem_attr = 0;
+
 template <int CD, int R>
 cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
     using C = Cfg<CD, R>;
@@ -504,11 +506,10 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
         cudaError_t e = launch_pdl(k, dim3(a.grid), dim3(kThreads), C::SMEM, s, a);
         if (e != cudaSuccess) return e;
         const int csmem = (a.max_chunks * kConsumerWarps * (R + 2) + R) * 4;
-        static int cattr = 0;
-        if (csmem > cattr) {
+        if (csmem > g_combine_smem_attr) {  // one (non-template) kernel: track its attribute globally
             e = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
             if (e != cudaSuccess) return e;
-            cattr = csmem;
+            g_combine_smem_attr = csmem;
         }
         return launch_pdl(attn_combine_kernel, dim3(a.B * a.nh), dim3(128), csmem, s, a,
                           static_cast<int>(kConsumerWarps));

@@ -483,7 +483,7 @@ int wsvd_layer_create(const wsvd_layer_desc* desc, const int32_t* ranks, wsvd_la
     L->d = d;
     L->R = R;
     L->Kp = round_up(d.embed_dim, 256);
-    L->ks = (L->Kp % 512 == 0) ? 512 : 256;
+    L->ks = (L->Kp % 512 == 0 && d.weight_dtype != WSVD_F32) ? 512 : 256;
     L->Nrows = d.n_heads * 3 * R;
     L->ranks.assign(ranks, ranks + d.n_heads * 3);
     L->have.assign(d.n_heads * 3, 0);
