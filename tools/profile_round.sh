@@ -15,6 +15,6 @@ ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum 
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:decode_attn -s 3 -c 1 \
     -o gpurun_out/attn_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:skinny_stream -s 513 -c 1 \
+ncu --set full --clock-control none --import-source on -k regex:skinny_stream -s 512 -c 1 \
     -o gpurun_out/gemm_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
 ls -la gpurun_out
