@@ -145,6 +145,10 @@ int wsvd_cache_read_host(wsvd_cache_t cache, int32_t b, int32_t head, double* ck
 /* raw device rows of sequence b, head h: rows [len][row_bytes] and (I8 only)
  * fp16 scale pairs [len][2]; for bit-exact checks. */
 int wsvd_cache_row_bytes(wsvd_cache_t cache, int32_t* row_bytes);
+/* How wsvd_layer_step(_graph/_host) runs for this cache: *fused = 1 when the
+ * whole step is the single persistent kernel of step.cu (bf16, rank 32,
+ * batch <= 32), 0 for the multi-kernel path; *launches = kernels per step. */
+int wsvd_cache_step_info(wsvd_cache_t cache, int32_t* fused, int32_t* launches);
 int wsvd_cache_read_raw(wsvd_cache_t cache, int32_t b, int32_t head, void* rows_host,
                         uint16_t* scales_host);
 

@@ -40,18 +40,21 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 using namespace wsvd_dev;
 
 namespace wsvd_k {
 
 namespace {
 
-constexpr int kConsumerWarps = 8;
-constexpr int kConsumers = 32 * kConsumerWarps;
-constexpr int kThreads = kConsumers + 32;  // + one producer warp
-constexpr int kStageTok = kConsumers;      // 256 tokens per stage
+constexpr int kStageTok = 256;   // tokens per pipeline stage
+constexpr int kMaxWarps = 16;    // most consumer warps of any variant (partials per chunk)
+constexpr int kDefaultVariant = 0;
 
-template <int CD, int R>
+// V (tensor-core variants, bf16 cache): bit 0 = transposed score tile,
+// bit 1 = 16 consumer warps (else 8)
+template <int CD, int R, int V = 0>
 struct Cfg {
     static constexpr int EB = (CD == F32) ? 4 : (CD == BF16 ? 2 : 1);
     static constexpr int EPC = 16 / EB;        // elements per 16-byte chunk
@@ -59,12 +62,17 @@ struct Cfg {
     static constexpr int NC = PART / 16;       // chunks per half
     static constexpr int ROWB = 2 * PART;
     static constexpr bool MMA = (CD == BF16);
+    // tensor-core consumers: 16 warps x one 16-token group per stage (latency
+    // hiding: 4 warps per SM sub-partition); CUDA-core consumers: one token per thread
+    static constexpr int NW = (MMA && (V & 2)) ? 16 : 8;
+    static constexpr int THREADS = 32 * NW + 32;  // + one producer warp
+    static constexpr int GPW = kStageTok / (16 * NW);  // 16-token groups per warp per stage
     static constexpr int ROWS = kStageTok * ROWB;
     static constexpr int SC = (CD == I8) ? 4 * kStageTok : 0;
     static constexpr int QT_OFF = ROWS + SC;   // absorbed query of the unit (first stage)
     static constexpr int STAGE = QT_OFF + 256;
     static constexpr int RSTRIDE = R + 4;      // floats per lane row of the reduction scratch
-    static constexpr int RED = MMA ? 0 : kConsumerWarps * 32 * RSTRIDE * 4;
+    static constexpr int RED = MMA ? 0 : NW * 32 * RSTRIDE * 4;
     static constexpr int BUDGET = 222 * 1024;
     static constexpr int ST_RAW = (BUDGET - RED - 4096) / STAGE;
     static constexpr int STAGES = ST_RAW > 8 ? 8 : ST_RAW;
@@ -151,21 +159,187 @@ WSVD_DEV Unit unit_geom(int u, int nch, int chunk, int len) {
 }
 
 // ----------------------------------------------------------------------------
-// Consumer state of one warp over one unit, tensor-core variant (bf16 cache).
-// Per 16-token group g16: D_s(16 x 8) = K(16 x R) . Q(R x 8), Q's columns
-// 0/1 = qt_hi/qt_lo, so a lane with t = lane%4 == 0 holds the scores of tokens
-// g and g+8 (g = lane/4) as d0+d1 and d2+d3.  P(16 tok x 8) has columns 0/1 =
-// p_hi/p_lo; acc(R x 8) += V^T(R x 16) . P accumulates in MMA D fragments.
-template <int R>
-struct MmaState {
-    static constexpr int KR = R / 16;
-    uint32_t qf[KR][2];  // B fragments of [qt_hi | qt_lo]
-    float acc[KR][4];    // D fragments of V^T . P
-};
+// Tensor-core consumer (bf16 cache) of one warp over one unit.  The warp owns
+// GPW 16-token groups of every 256-token stage.
+//
+// TS = 0: scores D(16 tok x 8) = K(16 tok x R) . [qt_hi | qt_lo](R x 8): the
+//   lane (g8, t4 = 0) holds the hi / lo partial scores of tokens g8, g8 + 8;
+//   four shuffles per group build the P fragment of the P.V MMA.
+// TS = 1: transposed tile S(16 x 8 tok) = Q(16 x R) . K^T with Q rows 0 and 1
+//   both the query (hi part in one MMA, lo part in a second accumulating one):
+//   lanes g8 in {0,1} hold the full scores of exactly the token pair their P
+//   fragment needs -- no shuffles, 4x the score MMAs.
+// Both: P.V as acc(R x 8) += V^T(R x 16 tok) . [p_hi | p_lo](16 tok x 8), the
+// x_hi = bf16(x), x_lo = bf16(x - x_hi) split keeping ~16 bits of the fp32
+// query and probabilities; the running max is a warp-uniform reference moved
+// lazily (only when a score exceeds it by 2^8, decided by one vote), so no
+// per-stage shuffle reduction sits on the critical path.
+template <class C, int R, int TS>
+WSVD_DEV void consume_mma(const AttnArgs& a, const Unit& g, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                          int& slot, uint32_t& phase, int warp, int lane) {
+    constexpr int KR = R / 16;
+    constexpr int GPW = C::GPW;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const bool qlane = g8 < 2;
+    float m_w = -INFINITY, l = 0.f;
+    const int ns = (g.ntok + kStageTok - 1) / kStageTok;
+    uint32_t qa[KR][2][2];  // TS=0: B fragments [kk][b0/b1][unused]; TS=1: A frags [kk][hi/lo][a0/a2]
+    float acc[KR][4];
+#pragma unroll
+    for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[kk][i] = 0.f;
+    for (int s = 0; s < ns; ++s) {
+        mbar_wait(&full[slot], phase);
+        const uint8_t* sp = smem + slot * C::STAGE;
+        const uint32_t sbase = smem_u32(sp);
+        if (s == 0) {
+            const float* q = reinterpret_cast<const float*>(sp + C::QT_OFF);
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const int k0 = kk * 16 + 2 * t4 + 8 * j;
+                    uint32_t h0, l0, h1, l1;
+                    split_bf16(q[k0], h0, l0);
+                    split_bf16(q[k0 + 1], h1, l1);
+                    if (TS == 0) {
+                        qa[kk][j][0] = (g8 == 0) ? (h0 | (h1 << 16)) : (g8 == 1 ? (l0 | (l1 << 16)) : 0u);
+                    } else {
+                        qa[kk][0][j] = qlane ? (h0 | (h1 << 16)) : 0u;
+                        qa[kk][1][j] = qlane ? (l0 | (l1 << 16)) : 0u;
+                    }
+                }
+        }
+        const int rows = min(kStageTok, g.ntok - s * kStageTok);
+        // ---- scores: sc[grp][i], i = the lane's 4 token slots of the group
+        float sc[GPW][4];
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) {
+            const int tb = (warp * GPW + grp) * 16;
+            if (TS == 0) {
+                float d[4] = {0.f, 0.f, 0.f, 0.f};
+                const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+                for (int kk = 0; kk < KR; ++kk) {
+                    uint32_t a0, a1, a2, a3;
+                    const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
+                    ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
+                    mma_bf16_16816(d, a0, a1, a2, a3, qa[kk][0][0], qa[kk][1][0]);
+                }
+                // slots 0/1: tokens g8, g8 + 8 (valid on t4 == 0)
+                sc[grp][0] = (t4 == 0 && tb + g8 < rows) ? d[0] + d[1] : -INFINITY;
+                sc[grp][1] = (t4 == 0 && tb + g8 + 8 < rows) ? d[2] + d[3] : -INFINITY;
+                sc[grp][2] = sc[grp][3] = -INFINITY;
+            } else {
+#pragma unroll
+                for (int tile = 0; tile < 2; ++tile) {
+                    float d[4] = {0.f, 0.f, 0.f, 0.f};
+                    const uint32_t rowoff = static_cast<uint32_t>((tb + tile * 8 + (lane & 7)) * C::ROWB);
+#pragma unroll
+                    for (int kk = 0; kk + 1 < KR; kk += 2) {
+                        uint32_t b0, b1, b2, b3;
+                        ldsm_x4(sbase + cache_swz(rowoff + (kk * 2 + (lane >> 3)) * 16), b0, b1, b2, b3);
+                        mma_bf16_16816(d, qa[kk][0][0], 0u, qa[kk][0][1], 0u, b0, b1);
+                        mma_bf16_16816(d, qa[kk][1][0], 0u, qa[kk][1][1], 0u, b0, b1);
+                        mma_bf16_16816(d, qa[kk + 1][0][0], 0u, qa[kk + 1][0][1], 0u, b2, b3);
+                        mma_bf16_16816(d, qa[kk + 1][1][0], 0u, qa[kk + 1][1][1], 0u, b2, b3);
+                    }
+                    if constexpr (KR & 1) {
+                        constexpr int kk = KR - 1;
+                        uint32_t b0, b1;
+                        ldsm_x2(sbase + cache_swz(rowoff + (kk * 2 + ((lane >> 3) & 1)) * 16), b0, b1);
+                        mma_bf16_16816(d, qa[kk][0][0], 0u, qa[kk][0][1], 0u, b0, b1);
+                        mma_bf16_16816(d, qa[kk][1][0], 0u, qa[kk][1][1], 0u, b0, b1);
+                    }
+                    const int tok = tb + tile * 8 + 2 * t4;
+                    sc[grp][2 * tile] = (qlane && tok < rows) ? d[0] : -INFINITY;
+                    sc[grp][2 * tile + 1] = (qlane && tok + 1 < rows) ? d[1] : -INFINITY;
+                }
+            }
+        }
+        // ---- lazily moved reference max
+        float lm = -INFINITY;
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) lm = fmaxf(lm, sc[grp][i]);
+        if (__any_sync(0xffffffffu, lm > m_w + 8.f)) {
+            const float wm = warp_max(lm);
+            const float f = ex2(m_w - wm);
+            l *= f;
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[kk][i] *= f;
+            m_w = wm;
+        }
+        // ---- probabilities and P.V
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) {
+            const int tb = (warp * GPW + grp) * 16;
+            float p[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) p[i] = (sc[grp][i] == -INFINITY) ? 0.f : ex2(sc[grp][i] - m_w);
+            uint32_t b[2];
+            if (TS == 0) {
+                l += p[0] + p[1];
+                uint32_t h0, l0, h1, l1;
+                split_bf16(p[0], h0, l0);
+                split_bf16(p[1], h1, l1);
+                const uint32_t hi2 = h0 | (h1 << 16), lo2 = l0 | (l1 << 16);
+                // lane (g8 in {0,1}, t4) needs p of tokens 2t4, 2t4+1 (+8): held by
+                // lanes 4*(2t4) and 4*(2t4+1) as (token, token + 8) pairs
+                const int s0 = 8 * t4, s1 = 8 * t4 + 4;
+                const uint32_t xh = __shfl_sync(0xffffffffu, hi2, s0), yh = __shfl_sync(0xffffffffu, hi2, s1);
+                const uint32_t xl = __shfl_sync(0xffffffffu, lo2, s0), yl = __shfl_sync(0xffffffffu, lo2, s1);
+                const uint32_t x = (g8 == 0) ? xh : xl, y = (g8 == 0) ? yh : yl;
+                b[0] = (g8 < 2) ? __byte_perm(x, y, 0x5410) : 0u;
+                b[1] = (g8 < 2) ? __byte_perm(x, y, 0x7632) : 0u;
+            } else {
+                if (g8 == 0) l += (p[0] + p[1]) + (p[2] + p[3]);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    uint32_t h0, l0, h1, l1;
+                    split_bf16(p[2 * j], h0, l0);
+                    split_bf16(p[2 * j + 1], h1, l1);
+                    b[j] = (g8 == 0) ? (h0 | (h1 << 16)) : (g8 == 1 ? (l0 | (l1 << 16)) : 0u);
+                }
+            }
+            const int stok = tb + (lane & 7) + ((lane >> 4) & 1) * 8;
+#pragma unroll
+            for (int mm = 0; mm < KR; ++mm) {
+                uint32_t a0, a1, a2, a3;
+                const uint32_t off = static_cast<uint32_t>(stok * C::ROWB + C::PART + (mm * 2 + ((lane >> 3) & 1)) * 16);
+                ldsm_x4_trans(sbase + cache_swz(off), a0, a1, a2, a3);
+                mma_bf16_16816(acc[mm], a0, a1, a2, a3, b[0], b[1]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == C::STAGES) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+    const float lsum = warp_sum(l);
+    float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kMaxWarps + warp) * (R + 2);
+    if (t4 == 0) {
+#pragma unroll
+        for (int mm = 0; mm < KR; ++mm) {
+            wsp[mm * 16 + g8] = acc[mm][0] + acc[mm][1];      // r = mm*16 + g8
+            wsp[mm * 16 + g8 + 8] = acc[mm][2] + acc[mm][3];  // r = mm*16 + g8 + 8
+        }
+    }
+    if (lane == 0) {
+        wsp[R] = m_w;
+        wsp[R + 1] = lsum;
+    }
+}
 
-template <int CD, int R>
-__global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs a) {
-    using C = Cfg<CD, R>;
+template <int CD, int R, int V>
+__global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(const AttnArgs a) {
+    using C = Cfg<CD, R, V>;
     constexpr int NC = C::NC, EPC = C::EPC;
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
@@ -178,13 +352,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
     // Zero the stage ring once: rows past a stage's valid end are read by the
     // MMAs (times p = 0) and must hold finite values.  This prologue overlaps
     // the previous kernel (programmatic dependent launch).
-    for (int i = tid; i < C::STAGES * C::STAGE / 16; i += kThreads)
+    for (int i = tid; i < C::STAGES * C::STAGE / 16; i += C::THREADS)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (tid == 0) {
         for (int i = 0; i < C::STAGES; ++i) {
             mbar_init(&full[i], 1);
-            mbar_init(&empty[i], kConsumerWarps);
+            mbar_init(&empty[i], C::NW);
         }
         fence_mbar_init();
     }
@@ -198,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
     const int n_units = a.B * a.nh * nch;
 
     // ======================================================== producer warp
-    if (warp == kConsumerWarps) {
+    if (warp == C::NW) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             int slot = 0;
@@ -241,89 +415,13 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
         const Unit g = unit_geom(u, nch, chunk, len);
         float m_w = -INFINITY, l = 0.f;
         const int ns = (g.ntok + kStageTok - 1) / kStageTok;
-        float wacc[2 * (R / 16 > 0 ? R / 16 : 1)];  // MMA path: this lane's acc rows (t4 == 0)
 
-        if constexpr (C::MMA) {
-            constexpr int KR = R / 16;
-            MmaState<R> st;
-#pragma unroll
-            for (int kk = 0; kk < KR; ++kk)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) st.acc[kk][i] = 0.f;
+        if constexpr (C::MMA && (V & 4)) {
+            // pipeline probe (WSVD_ATTN_VARIANT bit 2): drain the stages without
+            // computing -- the streaming ceiling of this producer structure
+            const int ns = (g.ntok + kStageTok - 1) / kStageTok;
             for (int s = 0; s < ns; ++s) {
                 mbar_wait(&full[slot], phase);
-                const uint8_t* sp = smem + slot * C::STAGE;
-                const uint32_t sbase = smem_u32(sp);
-                if (s == 0) {
-                    const float* q = reinterpret_cast<const float*>(sp + C::QT_OFF);
-#pragma unroll
-                    for (int kk = 0; kk < KR; ++kk)
-#pragma unroll
-                        for (int j = 0; j < 2; ++j) {
-                            const int k0 = kk * 16 + 2 * t4 + 8 * j;
-                            uint32_t h0, l0, h1, l1;
-                            split_bf16(q[k0], h0, l0);
-                            split_bf16(q[k0 + 1], h1, l1);
-                            st.qf[kk][j] = (g8 == 0) ? (h0 | (h1 << 16)) : (g8 == 1 ? (l0 | (l1 << 16)) : 0u);
-                        }
-                }
-                const int rows = min(kStageTok, g.ntok - s * kStageTok);
-                // ---- scores of the warp's 2 groups of 16 tokens
-                float sc[2][2];
-#pragma unroll
-                for (int grp = 0; grp < 2; ++grp) {
-                    const int tb = warp * 32 + grp * 16;
-                    float d[4] = {0.f, 0.f, 0.f, 0.f};
-                    const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
-#pragma unroll
-                    for (int kk = 0; kk < KR; ++kk) {
-                        uint32_t a0, a1, a2, a3;
-                        const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
-                        ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
-                        mma_bf16_16816(d, a0, a1, a2, a3, st.qf[kk][0], st.qf[kk][1]);
-                    }
-                    const bool v0 = (t4 == 0) && (tb + g8 < rows);
-                    const bool v1 = (t4 == 0) && (tb + g8 + 8 < rows);
-                    sc[grp][0] = v0 ? d[0] + d[1] : -INFINITY;
-                    sc[grp][1] = v1 ? d[2] + d[3] : -INFINITY;
-                }
-                // ---- online softmax, warp-uniform running max (exp2 domain)
-                const float wm = warp_max(fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])));
-                if (wm > m_w) {
-                    const float f = ex2(m_w - wm);
-                    l *= f;
-#pragma unroll
-                    for (int kk = 0; kk < KR; ++kk)
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) st.acc[kk][i] *= f;
-                    m_w = wm;
-                }
-#pragma unroll
-                for (int grp = 0; grp < 2; ++grp) {
-                    const int tb = warp * 32 + grp * 16;
-                    const float p0 = (sc[grp][0] == -INFINITY) ? 0.f : ex2(sc[grp][0] - m_w);
-                    const float p1 = (sc[grp][1] == -INFINITY) ? 0.f : ex2(sc[grp][1] - m_w);
-                    l += p0 + p1;
-                    uint32_t h0, l0, h1, l1;
-                    split_bf16(p0, h0, l0);
-                    split_bf16(p1, h1, l1);
-                    const uint32_t hi2 = h0 | (h1 << 16), lo2 = l0 | (l1 << 16);
-                    // P fragment: lane (g8 in {0,1}, t4) needs p of tokens 2t4, 2t4+1 (+8)
-                    const int s0 = 8 * t4, s1 = 8 * t4 + 4;
-                    const uint32_t xh = __shfl_sync(0xffffffffu, hi2, s0), yh = __shfl_sync(0xffffffffu, hi2, s1);
-                    const uint32_t xl = __shfl_sync(0xffffffffu, lo2, s0), yl = __shfl_sync(0xffffffffu, lo2, s1);
-                    const uint32_t x = (g8 == 0) ? xh : xl, y = (g8 == 0) ? yh : yl;
-                    const uint32_t b0 = (g8 < 2) ? __byte_perm(x, y, 0x5410) : 0u;
-                    const uint32_t b1 = (g8 < 2) ? __byte_perm(x, y, 0x7632) : 0u;
-                    const int stok = tb + (lane & 7) + ((lane >> 4) & 1) * 8;
-#pragma unroll
-                    for (int mm = 0; mm < KR; ++mm) {
-                        uint32_t a0, a1, a2, a3;
-                        const uint32_t off = static_cast<uint32_t>(stok * C::ROWB + C::PART + (mm * 2 + ((lane >> 3) & 1)) * 16);
-                        ldsm_x4_trans(sbase + cache_swz(off), a0, a1, a2, a3);
-                        mma_bf16_16816(st.acc[mm], a0, a1, a2, a3, b0, b1);
-                    }
-                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[slot]);
                 if (++slot == C::STAGES) {
@@ -331,24 +429,8 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
                     phase ^= 1u;
                 }
             }
-#pragma unroll
-            for (int mm = 0; mm < KR; ++mm) {
-                wacc[2 * mm] = st.acc[mm][0] + st.acc[mm][1];      // r = mm*16 + g8
-                wacc[2 * mm + 1] = st.acc[mm][2] + st.acc[mm][3];  // r = mm*16 + g8 + 8
-            }
-            const float lsum = warp_sum(l);
-            float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kConsumerWarps + warp) * (R + 2);
-            if (t4 == 0) {
-#pragma unroll
-                for (int mm = 0; mm < KR; ++mm) {
-                    wsp[mm * 16 + g8] = wacc[2 * mm];
-                    wsp[mm * 16 + g8 + 8] = wacc[2 * mm + 1];
-                }
-            }
-            if (lane == 0) {
-                wsp[R] = m_w;
-                wsp[R + 1] = lsum;
-            }
+        } else if constexpr (C::MMA) {
+            consume_mma<C, R, (V & 1)>(a, g, smem, full, empty, slot, phase, warp, lane);
         } else {
             // ------------------------------------------ CUDA-core path (f32, int8)
             float qr[NC][EPC];
@@ -424,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
                     *reinterpret_cast<float4*>(wr + lane * C::RSTRIDE + c * EPC + e) =
                         make_float4(acc[c][e], acc[c][e + 1], acc[c][e + 2], acc[c][e + 3]);
             const float lsum = warp_sum(l);
-            float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kConsumerWarps + warp) * (R + 2);
+            float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kMaxWarps + warp) * (R + 2);
             for (int j = lane; j < R; j += 32) {
                 float sum = 0.f;
 #pragma unroll 8
@@ -437,7 +519,6 @@ __global__ void __launch_bounds__(kThreads, 1) decode_attn_kernel(const AttnArgs
             }
             __syncwarp();  // scratch reuse by the next unit
         }
-        (void)wacc;
         // each warp published its own partial (m, l, acc[R]); no CTA-wide sync
     }
 }
@@ -458,8 +539,14 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a, int
     float* part = sm;
     float* vt = sm + a.max_chunks * parts_per_chunk * (R + 2);
     // stage every partial of this (sequence, head) with coalesced loads
-    const float* wsb = a.ws + static_cast<size_t>(bh) * a.max_chunks * parts_per_chunk * (R + 2);
-    for (int i = tid; i < np * (R + 2); i += blockDim.x) part[i] = __ldcg(wsb + i);
+    // (workspace layout [bh][max_chunks][kMaxWarps][R+2]; this variant used
+    // the first parts_per_chunk warp slots of each chunk)
+    const int pw = parts_per_chunk * (R + 2);
+    const float* wsb = a.ws + static_cast<size_t>(bh) * a.max_chunks * kMaxWarps * (R + 2);
+    for (int i = tid; i < np * (R + 2); i += blockDim.x) {
+        const int c = i / pw, r = i - c * pw;
+        part[i] = __ldcg(wsb + static_cast<size_t>(c) * kMaxWarps * (R + 2) + r);
+    }
     __syncthreads();
     float M = -INFINITY;
     for (int p = 0; p < np; ++p) M = fmaxf(M, part[p * (R + 2) + R]);
@@ -490,29 +577,58 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a, int
 
 int g_combine_smem_attr = 0;
 
-template <int CD, int R>
-cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
-    using C = Cfg<CD, R>;
+template <int CD, int R, int V>
+cudaError_t launch_v(const AttnArgs& a, cudaStream_t s) {
+    using C = Cfg<CD, R, V>;
     if constexpr (!C::OK) {
         return cudaErrorInvalidValue;
     } else {
-        auto k = decode_attn_kernel<CD, R>;
+        auto k = decode_attn_kernel<CD, R, V>;
         static bool attr_set = false;
         if (!attr_set) {
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
             if (e != cudaSuccess) return e;
             attr_set = true;
         }
-        cudaError_t e = launch_pdl(k, dim3(a.grid), dim3(kThreads), C::SMEM, s, a);
+        cudaError_t e = launch_pdl(k, dim3(a.grid), dim3(C::THREADS), C::SMEM, s, a);
         if (e != cudaSuccess) return e;
-        const int csmem = (a.max_chunks * kConsumerWarps * (R + 2) + R) * 4;
+        const int csmem = (a.max_chunks * C::NW * (R + 2) + R) * 4;
         if (csmem > g_combine_smem_attr) {  // one (non-template) kernel: track its attribute globally
             e = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
             if (e != cudaSuccess) return e;
             g_combine_smem_attr = csmem;
         }
         return launch_pdl(attn_combine_kernel, dim3(a.B * a.nh), dim3(128), csmem, s, a,
-                          static_cast<int>(kConsumerWarps));
+                          static_cast<int>(C::NW));
+    }
+}
+
+// tensor-core variant (bf16 cache); WSVD_ATTN_VARIANT overrides it for A/B runs
+int attn_variant() {
+    static const int v = [] {
+        const char* e = std::getenv("WSVD_ATTN_VARIANT");
+        return e ? (std::atoi(e) & 7) : kDefaultVariant;
+    }();
+    return v;
+}
+
+template <int CD, int R>
+cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
+    if constexpr (CD != BF16) {
+        return launch_v<CD, R, 0>(a, s);
+    } else {
+        if constexpr (R != 32) {
+            return launch_v<CD, R, kDefaultVariant>(a, s);
+        } else {
+            switch (attn_variant()) {
+                case 0: return launch_v<CD, R, 0>(a, s);
+                case 1: return launch_v<CD, R, 1>(a, s);
+                case 2: return launch_v<CD, R, 2>(a, s);
+                case 3: return launch_v<CD, R, 3>(a, s);
+                case 4: return launch_v<CD, R, 4>(a, s);
+                default: return launch_v<CD, R, 6>(a, s);
+            }
+        }
     }
 }
 
@@ -549,7 +665,7 @@ int attn_smem_bytes(int cdtype, int R) {
     return 0;
 }
 
-int attn_parts_per_chunk() { return kConsumerWarps; }
+int attn_parts_per_chunk() { return kMaxWarps; }
 
 int attn_occupancy(int cdtype, int R) {
     return attn_smem_bytes(cdtype, R) > 0 ? 1 : 0;  // persistent: one CTA per SM

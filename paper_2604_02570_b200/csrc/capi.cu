@@ -236,7 +236,9 @@ struct wsvd_cache_s {
     int P_M = 0, P_splits = 0;        // rows / K splits of the last projection
     DevBuf oP, y_tmp;                 // O-proj partials
     DevBuf x_dev, y_dev;              // staging for the host-buffer step
+    DevBuf trace;                     // fused-step phase timeline (WSVD_STEP_TRACE)
     int chunk = 512, max_chunks = 1, grid = 148;
+    int fmax_chunks = 1;              // split-KV chunks of the fused step kernel
     int sms = 148;
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;
@@ -433,9 +435,63 @@ int run_oproj(wsvd_cache_s* c, const float* vlat, float* y, int* commit_len, cud
     return WSVD_OK;
 }
 
+bool fused_step_ok(wsvd_cache_s* c) {
+    static const bool off = getenv("WSVD_STEP_MULTI") != nullptr;  // A/B switch: multi-kernel step
+    const wsvd_layer_s* L = c->L;
+    if (off || c->cdtype != BF16 || L->d.weight_dtype != BF16 || L->o_dtype != BF16 || !L->Wo.p) return false;
+    if (L->ks != step_item_k() || L->oks != step_item_k()) return false;
+    // the chunk count never exceeds max_chunks (adaptive) or the capacity split (fixed chunk)
+    const int mc = c->chunk > 0 ? c->max_chunks : c->fmax_chunks;
+    return step_supported(L->R, c->B, L->d.n_heads, c->B * L->d.n_heads * mc, L->Kp, L->oKp,
+                          round_up(L->e_out, 16) / 16, c->sms);
+}
+
+// the whole step as one persistent kernel (step.cu)
+int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s) {
+    wsvd_layer_s* L = c->L;
+    int rc = ensure_mqk(L);
+    if (rc) return rc;
+    const int splits = L->Kp / L->ks;
+    const size_t need = static_cast<size_t>(splits) * c->B * L->Nrows * 4;
+    if (c->P.n < need) CUDA_TRY(c->P.alloc(need));
+    StepArgs a{};
+    a.x = x;
+    a.y = y;
+    a.A = L->A.as<uint8_t>();
+    a.P = c->P.as<float>();
+    a.mqk = L->mqk.as<float>();
+    a.cache = c->data.as<uint8_t>();
+    a.ws = c->attn_ws.as<float>();
+    a.counters = c->attn_cnt.as<int>();
+    a.vlat = c->vlat.as<float>();
+    a.Wo = L->Wo.as<uint8_t>();
+    a.d_len = c->d_len();
+    a.bar = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 4);
+    a.B = c->B;
+    a.nh = L->d.n_heads;
+    a.E = L->d.embed_dim;
+    a.Kp = L->Kp;
+    a.Nrows = L->Nrows;
+    a.e_out = L->e_out;
+    a.oKp = L->oKp;
+    a.otiles = round_up(L->e_out, 16) / 16;
+    a.cap = c->cap_alloc;
+    a.chunk = c->chunk;
+    a.max_chunks = c->chunk > 0 ? c->max_chunks : c->fmax_chunks;
+    a.grid = c->sms;
+    static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
+    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 10 * 8));
+    a.trace = trace ? c->trace.as<uint64_t>() : nullptr;
+    CUDA_TRY(launch_layer_step(a, s));
+    c->P_M = c->B;
+    c->P_splits = splits;
+    return WSVD_OK;
+}
+
 // append (row written, length not yet committed) -> attention over len + 1
 // -> combine -> folded O-projection, whose first thread commits the length
 int layer_step_impl(wsvd_cache_s* c, const float* x, float* attn_out, float* y, cudaStream_t s) {
+    if (attn_out == nullptr && fused_step_ok(c)) return run_step_fused(c, x, y, s);
     int rc = run_append(c, x, 1, nullptr, c->qt.as<float>(), 0, s);
     if (rc) return rc;
     rc = run_attention(c, attn_out, c->vlat.as<float>(), 1, s);
@@ -664,7 +720,8 @@ int wsvd_layer_set_oproj(wsvd_layer_t L, const double* w, int32_t e_out, int32_t
     L->e_out = e_out;
     L->o_dtype = dtype;
     L->oKp = round_up(K, 256);
-    L->oks = L->oKp <= 1024 ? L->oKp : ((L->oKp % 512 == 0) ? 512 : 256);
+    // 512-wide K splits (16 KB W-tile items, the fused step's weight-ring slot)
+    L->oks = (L->oKp % 512 == 0) ? 512 : 256;
     if (dtype == WSVD_F32) L->oks = std::min(L->oKp, 1024);
     const int e_pad = round_up(e_out, 16);  // whole W-tiles
     const size_t el = dtype == WSVD_F32 ? 4 : 2;
@@ -727,12 +784,23 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
         c->chunk = std::max(32, round_up(atoi(env), 32));
         c->max_chunks = (c->cap_alloc + c->chunk - 1) / c->chunk;
     }
+    // the fused step streams up to step_max_units() units per CTA
+    {
+        const int mu = step_max_units();
+        int fu = mu;
+        if (const char* env = getenv("WSVD_STEP_UNITS")) fu = std::max(1, std::min(mu, atoi(env)));
+        const int pairs = batch * nh;
+        c->fmax_chunks = std::max(1, (fu * c->sms + pairs - 1) / pairs);
+        while (c->fmax_chunks > 1 && (pairs * c->fmax_chunks + c->sms - 1) / c->sms > mu) --c->fmax_chunks;
+    }
     const size_t rows = static_cast<size_t>(batch) * nh * c->cap_alloc;
     cudaError_t e = c->data.alloc(rows * c->row_bytes);
     if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4);
     if (e == cudaSuccess) e = c->ctrl.alloc(64);
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
-    if (e == cudaSuccess) e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh * c->max_chunks * attn_parts_per_chunk() * (L->R + 2) * 4);
+    if (e == cudaSuccess)
+        e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh *
+                             std::max(c->max_chunks * attn_parts_per_chunk(), c->fmax_chunks) * (L->R + 2) * 4);
     if (e == cudaSuccess) e = c->attn_cnt.alloc(static_cast<size_t>(batch) * nh * 4);
     if (e == cudaSuccess) e = c->vlat.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     (void)H;
@@ -784,6 +852,24 @@ int wsvd_cache_bind_layer(wsvd_cache_t c, wsvd_layer_t L) {
 int wsvd_cache_length(wsvd_cache_t c, int32_t* len) {
     if (!c || !len) return set_err(WSVD_ECONFIG, "null argument");
     *len = c->len;
+    return WSVD_OK;
+}
+
+int wsvd_cache_step_info(wsvd_cache_t c, int32_t* fused, int32_t* launches) {
+    if (!c || !fused || !launches) return set_err(WSVD_ECONFIG, "null argument");
+    const wsvd_layer_s* L = c->L;
+    if (fused_step_ok(c)) {
+        *fused = 1;
+        *launches = 1;
+        return WSVD_OK;
+    }
+    const int wd = L->d.weight_dtype;
+    int n = 4;                                               // projection, epilogue, attention, combine
+    if (wd == WSVD_I8 || wd == WSVD_I4) n += 1;              // activation quantiser
+    n += 1;                                                  // O-projection GEMM
+    if (L->oKp > 0 && L->oKp / L->oks > 1) n += 1;           // its split reduction
+    *fused = 0;
+    *launches = n;
     return WSVD_OK;
 }
 
@@ -962,6 +1048,14 @@ int wsvd_layer_step_graph(wsvd_cache_t c, const float* x, float* y, void* stream
     if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
     CUDA_TRY(cudaSetDevice(c->L->d.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (fused_step_ok(c)) {
+        // one persistent kernel per step: a plain (PDL) launch is already as
+        // cheap as a graph replay, and x / y may change from step to step
+        rc = run_step_fused(c, x, y, s);
+        if (rc) return rc;
+        c->len += 1;
+        return WSVD_OK;
+    }
     const bool same = c->gkey.x == x && c->gkey.y == y && c->gkey.s == s;
     if (c->gexec && same) {
         CUDA_TRY(cudaGraphLaunch(c->gexec, c->gstream ? c->gstream : s));
@@ -1063,6 +1157,13 @@ int wsvd_cache_debug_copy(wsvd_cache_t c, int32_t what, void* host, int64_t* byt
         if (*bytes < static_cast<int64_t>(n)) return set_err(WSVD_ESHAPE, "host buffer too small");
         CUDA_TRY(cudaMemcpy(host, c->qt.p, n, cudaMemcpyDeviceToHost));
         *bytes = static_cast<int64_t>(n);
+        return WSVD_OK;
+    }
+    if (what == 4) {
+        if (!c->trace.p) return set_err(WSVD_ECONFIG, "no step trace (set WSVD_STEP_TRACE)");
+        if (*bytes < static_cast<int64_t>(c->trace.n)) return set_err(WSVD_ESHAPE, "host buffer too small");
+        CUDA_TRY(cudaMemcpy(host, c->trace.p, c->trace.n, cudaMemcpyDeviceToHost));
+        *bytes = static_cast<int64_t>(c->trace.n);
         return WSVD_OK;
     }
     return set_err(WSVD_ECONFIG, "unknown debug buffer");

@@ -100,4 +100,29 @@ int attn_occupancy(int cdtype, int R);  // resident CTAs per SM (0 if unsupporte
 int attn_parts_per_chunk();             // warp partials published per unit
 cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s);
 
+// ------------------------------------------------- fused layer step (step.cu) --
+// projection -> append -> attention -> combine -> folded O-projection as one
+// persistent kernel (bf16 weights / cache, rank 32, batch <= 32).
+struct StepArgs {
+    const float* x;        // [B][E] fp32 tokens
+    float* y;              // [B][e_out] fp32 output
+    const uint8_t* A;      // projection W-tiles (bf16, K split 512)
+    float* P;              // [splits][B][Nrows] projection partials
+    const float* mqk;      // [nh][R][R]
+    uint8_t* cache;        // [B][nh][cap][4R] bf16, swizzled
+    float* ws;             // [B*nh][max_chunks][R+2] per-unit states
+    int* counters;         // [B*nh] self-resetting
+    float* vlat;           // [B][nh*R]
+    const uint8_t* Wo;     // folded O-projection W-tiles (bf16, K split 512)
+    int* d_len;            // committed length (the new row goes to *d_len)
+    unsigned* bar;         // [2] grid barrier (count, generation)
+    uint64_t* trace;       // [grid][8] %globaltimer at the phase marks, or null
+    int B, nh, E, Kp, Nrows, e_out, oKp, otiles, cap;
+    int chunk, max_chunks, grid;
+};
+bool step_supported(int R, int B, int nh, int max_units, int Kp, int oKp, int otiles, int grid);
+int step_item_k();
+int step_max_units();  // attention units one CTA of the fused step can hold
+cudaError_t launch_layer_step(const StepArgs& a, cudaStream_t s);
+
 }  // namespace wsvd_k

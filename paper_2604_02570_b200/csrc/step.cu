@@ -1,0 +1,654 @@
+// step.cu -- the whole decode-layer step as ONE persistent kernel (bf16 weights,
+// bf16 latent cache, rank 32).
+//
+// pipe::decode_factored's per-layer body (reference src/pipeline.cpp:320-329)
+// is append_token (decode.cpp:127-153) -> fused_decode_step (decode.cpp:155-206)
+// -> heads_row . W_o.  The multi-kernel path (capi.cu layer_step_impl) runs it
+// as projection GEMM -> append epilogue -> attention -> combine -> O-projection:
+// five launches, each with its own ramp-up and tail, and HBM idle across every
+// kernel boundary.  This kernel runs the same arithmetic with one CTA per SM
+// and two grid-wide barriers:
+//
+//   P1  latent projection  P[split][b][n] = x_b . A_all[:, n] over one K split
+//       (swap-AB mma.sync over W-tiles streamed by TMA, as gemm.cu);
+//   --  grid barrier 1 (all projection partials written)
+//   P2  attention units (sequence, head, chunk) exactly as attn.cu's
+//       tensor-core consumer; each unit derives its absorbed query from the
+//       partials itself (qt = (sum_split c_Q) . M_QK, the append epilogue's
+//       fold), the unit holding the new token writes the token's latent row
+//       into the cache and patches it into the shared-memory stage; each
+//       unit's 8 warp states are merged (fixed order) into a unit state;
+//   --  grid barrier 2 (unit states complete; the cache length is committed)
+//   P3  folded O-projection y = vlat . (B_V . W_o) over W-tiles that were
+//       prefetched into shared memory during P2; the CTA builds the vlat rows
+//       it needs by merging each (sequence, head)'s chunk states in chunk
+//       order (SoftmaxState::merge, decode.cpp:59-75) -- no atomics, and the
+//       result is run-to-run deterministic.
+//
+// One producer warp keeps HBM busy across the phase boundaries: it first
+// fills the weight ring and the attention ring (the cache rows are ready
+// before the step starts), then streams the rest of the projection weights,
+// the O-projection weights and the remaining cache stages.
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace wsvd_dev;
+
+namespace wsvd_k {
+
+namespace {
+
+constexpr int kNW = 8;               // consumer warps
+constexpr int kThr = 32 * kNW + 64;  // + one producer warp + one helper warp
+constexpr int kSync = 32 * kNW + 32; // threads in the grid barrier (consumers + helper)
+constexpr int kST = 256;             // tokens per attention stage
+constexpr int kKS = 512;             // K per weight work item
+constexpr int kItem = 16 * kKS * 2;  // one weight work item: 16 rows x 512 bf16 = 16 KB
+constexpr int kNA = 4;               // weight ring slots == projection consumer warps
+constexpr int kXS = kKS * 2 + 64;    // bytes per staged token row (stride == 64 mod 128)
+constexpr int kMaxU = 8;             // attention units per CTA (host-checked)
+constexpr int kMaxSplits = 16;       // projection K splits (host-checked)
+
+template <int R, int MT>
+struct SC {
+    static constexpr int ROWB = 4 * R;  // bf16 [C_K | C_V]
+    static constexpr int PART = 2 * R;
+    static constexpr int STAGE = kST * ROWB;
+    static constexpr int XB = MT * 16 * kXS;               // one staged X slice
+    // per-unit scratch: absorbed queries, the new token's row, the warp states
+    static constexpr int RED = kMaxU * (R * 4 + 4 * R + kNW * (R + 2) * 4);
+    static constexpr int FIXED = kNA * kItem + XB + RED + 768;
+    static constexpr int NB_RAW = (225 * 1024 - FIXED) / STAGE;
+    static constexpr int NB = NB_RAW > 6 ? 6 : NB_RAW;
+    static constexpr int B_OFF = kNA * kItem;
+    static constexpr int X_OFF = B_OFF + NB * STAGE;
+    static constexpr int RED_OFF = X_OFF + XB;
+    static constexpr int BAR_OFF = RED_OFF + RED;
+    static constexpr int SMEM = BAR_OFF + 512;
+    static constexpr bool OK = NB_RAW >= 2 && 2 * XB <= NB * STAGE;
+};
+
+WSVD_DEV float ex2(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+WSVD_DEV void split_bf16(float x, uint32_t& hi, uint32_t& lo) {
+    const __nv_bfloat16 h = __float2bfloat16_rn(x);
+    const __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
+    hi = *reinterpret_cast<const uint16_t*>(&h);
+    lo = *reinterpret_cast<const uint16_t*>(&l);
+}
+
+WSVD_DEV uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define STEP_MARK(k) \
+    do { if (a.trace && tid == 0) a.trace[cta * 10 + (k)] = gtimer(); } while (0)
+
+WSVD_DEV unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid-wide barrier among the consumer warps of every CTA (all CTAs are
+// resident: one per SM).  bar[0] counts arrivals, bar[1] is the generation;
+// the last arriver resets the count before releasing the others.
+WSVD_DEV void grid_sync(unsigned* bar) {
+    named_bar_sync(1, kSync);
+    if (threadIdx.x == 0) {
+        const unsigned g0 = ld_acquire(bar + 1);
+        unsigned old;
+        // release: the CTA's writes (ordered before by bar.sync) become visible
+        // to whoever acquires the generation bump
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+        if (old == gridDim.x - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+        } else {
+            while (ld_acquire(bar + 1) == g0) {
+            }
+        }
+    }
+    named_bar_sync(1, kSync);
+}
+
+// split-KV geometry, identical to attn.cu chunking()
+WSVD_DEV void step_chunking(const StepArgs& a, int len, int& nch, int& chunk) {
+    if (a.chunk > 0) {
+        chunk = a.chunk;
+    } else {
+        const int n = max(1, min(a.max_chunks, (len + 31) / 32));
+        chunk = (((len + n - 1) / n) + 31) & ~31;
+    }
+    nch = (len + chunk - 1) / chunk;
+}
+
+// fp32 X[rows][ldx] columns [k0, k0 + kKS) -> bf16 smem [MT*16][kXS], zero padded
+template <int MT>
+WSVD_DEV void stage_rows(const float* X, int rows, int ldx, int kvalid, int k0, uint8_t* xs, int ctid) {
+    constexpr int PER = kKS / 8;  // 8-element items per row
+    for (int i = ctid; i < MT * 16 * PER; i += 32 * kNW) {
+        const int m = i / PER, kk = (i - m * PER) * 8;
+        const int k = k0 + kk;
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = 0.f;
+        if (m < rows) {
+            const float* src = X + static_cast<size_t>(m) * ldx + k;
+            if (k + 8 <= kvalid && (ldx % 4) == 0) {
+                const float4 p0 = __ldcg(reinterpret_cast<const float4*>(src));
+                const float4 p1 = __ldcg(reinterpret_cast<const float4*>(src + 4));
+                v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w;
+                v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) v[j] = (k + j < kvalid) ? __ldcg(src + j) : 0.f;
+            }
+        }
+        uint4 o;
+        o.x = pack_bf16x2(v[0], v[1]); o.y = pack_bf16x2(v[2], v[3]);
+        o.z = pack_bf16x2(v[4], v[5]); o.w = pack_bf16x2(v[6], v[7]);
+        *reinterpret_cast<uint4*>(xs + m * kXS + kk * 2) = o;
+    }
+}
+
+// One weight work item (16 W-rows x kKS, W-tile layout of gemm.cu) against the
+// staged tokens: D fragments facc[mt][hh][i] = (row g | g+8, token 2t | 2t+1).
+template <int MT>
+WSVD_DEV void item_mma(uint32_t slot_addr, uint32_t xs_addr, int lane, float (&facc)[MT][2][4]) {
+    const int g = lane >> 2, t = lane & 3;
+    const uint32_t swz = static_cast<uint32_t>((g & 1) << 2);
+    const uint32_t row_lo = slot_addr + static_cast<uint32_t>(g * kKS * 2);
+    const uint32_t row_hi = row_lo + static_cast<uint32_t>(8 * kKS * 2);
+    const uint32_t xbase = xs_addr + static_cast<uint32_t>(g * kXS + t * 16);
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) facc[mt][hh][i] = 0.f;
+#pragma unroll 4
+    for (int b = 0; b < kKS / 32; ++b) {
+        const uint32_t uoff = ((static_cast<uint32_t>(4 * b + t)) ^ swz) * 16;
+        const uint4 wl = lds128(row_lo + uoff);
+        const uint4 wh = lds128(row_hi + uoff);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const uint4 xv = lds128(xbase + static_cast<uint32_t>((mt * 16 + hh * 8) * kXS + b * 64));
+                mma_bf16_16816(facc[mt][hh], wl.x, wh.x, wl.y, wh.y, xv.x, xv.y);
+                mma_bf16_16816(facc[mt][hh], wl.z, wh.z, wl.w, wh.w, xv.z, xv.w);
+            }
+    }
+}
+
+template <int R, int MT>
+__global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
+    static_assert(R == 32, "the fused step is specialised for rank 32 (one latent dim per lane)");
+    using C = SC<R, MT>;
+    constexpr int KR = R / 16;
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint8_t* ringA = smem;
+    uint8_t* ringB = smem + C::B_OFF;
+    uint8_t* xbuf = smem + C::X_OFF;
+    float* qts = reinterpret_cast<float*>(smem + C::RED_OFF);                // [kMaxU][R]
+    __nv_bfloat16* nrow = reinterpret_cast<__nv_bfloat16*>(qts + kMaxU * R);  // [kMaxU][2R]
+    float* wst = qts + 2 * kMaxU * R;                                         // [kMaxU][kNW][R+2]
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+    uint64_t* emptyA = fullA + kNA;
+    uint64_t* fullB = emptyA + kNA;
+    uint64_t* emptyB = fullB + C::NB;
+    uint64_t* uready = emptyB + C::NB;  // [kMaxU] unit j's query / new row prepared (helper)
+    uint64_t* sfull = uready + kMaxU;   // [kMaxU] unit j's warp states written (consumers)
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int G = gridDim.x, cta = blockIdx.x;
+
+    STEP_MARK(0);
+    // prologue (overlaps the predecessor under PDL): rows past a stage's valid
+    // end are read by the MMAs (times p = 0) and must be finite
+    for (int i = tid; i < C::NB * C::STAGE / 16; i += kThr)
+        reinterpret_cast<uint4*>(ringB)[i] = make_uint4(0, 0, 0, 0);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    if (tid == 0) {
+        for (int i = 0; i < kNA; ++i) {
+            mbar_init(&fullA[i], 1);
+            mbar_init(&emptyA[i], 1);
+        }
+        for (int i = 0; i < C::NB; ++i) {
+            mbar_init(&fullB[i], 1);
+            mbar_init(&emptyB[i], kNW);
+        }
+        for (int i = 0; i < kMaxU; ++i) {
+            mbar_init(&uready[i], 1);
+            mbar_init(&sfull[i], kNW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    griddep_wait();
+    griddep_launch_dependents();
+    STEP_MARK(1);
+
+    const int pos = *a.d_len;  // the new token's row; attention covers pos + 1 rows
+    const int len = pos + 1;
+    const int splits = a.Kp / kKS;
+    const int cps = G / splits;  // CTAs per projection split
+    const int ps = cta % splits, pj = cta / splits;
+    const int ptiles = a.Nrows / 16;
+    const int plo = pj < cps ? static_cast<int>(static_cast<long>(pj) * ptiles / cps) : 0;
+    const int phi = pj < cps ? static_cast<int>(static_cast<long>(pj + 1) * ptiles / cps) : 0;
+    const int np1 = phi - plo;
+    const int osplits = a.oKp / kKS;
+    const int n_oitems = a.otiles * osplits;
+    const int np3 = cta < n_oitems ? (n_oitems - 1 - cta) / G + 1 : 0;  // <= kNA (host-checked)
+    int nch, chunk;
+    step_chunking(a, len, nch, chunk);
+    const int n_units = a.B * a.nh * nch;
+    const int nu = cta < n_units ? (n_units - 1 - cta) / G + 1 : 0;  // this CTA's units u = cta + j*G
+    const size_t cap = static_cast<size_t>(a.cap);
+    const size_t pstride = static_cast<size_t>(a.B) * a.Nrows;
+
+    // ================================================================ producer
+    if (warp == kNW) {
+        if (lane == 0) {
+            const uint64_t pol = policy_evict_first();
+            int ia = 0;
+            const int na = np1 + np3;
+            auto issue_a = [&]() {
+                const int slot = ia % kNA;
+                const uint32_t ph = static_cast<uint32_t>(ia / kNA) & 1u;
+                mbar_wait(&emptyA[slot], ph ^ 1u);
+                mbar_arrive_expect_tx(&fullA[slot], kItem);
+                const uint8_t* src = ia < np1
+                    ? a.A + (static_cast<size_t>(plo + ia) * splits + ps) * kItem
+                    : a.Wo + static_cast<size_t>(cta + (ia - np1) * G) * kItem;
+                tma_bulk_g2s(ringA + slot * kItem, src, kItem, &fullA[slot]);
+                ++ia;
+            };
+            int u = cta, st = 0, ib = 0;
+            auto issue_b = [&]() -> bool {
+                if (u >= n_units) return false;
+                const int bh = u / nch, ck = u - bh * nch;
+                const int t0 = ck * chunk, ntok = min(chunk, len - t0);
+                const int rows = min(kST, ntok - st * kST);
+                const uint32_t rbytes = static_cast<uint32_t>(min(C::STAGE, ((rows * C::ROWB + 1023) / 1024) * 1024));
+                const int slot = ib % C::NB;
+                const uint32_t ph = static_cast<uint32_t>(ib / C::NB) & 1u;
+                mbar_wait(&emptyB[slot], ph ^ 1u);
+                mbar_arrive_expect_tx(&fullB[slot], rbytes);
+                const uint8_t* src = a.cache + (static_cast<size_t>(bh) * cap + t0) * C::ROWB + static_cast<size_t>(st) * C::STAGE;
+                tma_bulk_g2s_stream(ringB + slot * C::STAGE, src, rbytes, &fullB[slot], pol);
+                ++ib;
+                if (++st * kST >= ntok) {
+                    st = 0;
+                    u += G;
+                }
+                return true;
+            };
+            while (ia < na && ia < kNA) issue_a();            // fill the weight ring
+            for (int k = 0; k < C::NB && issue_b(); ++k) {}   // and the attention ring
+            while (ia < na) issue_a();                        // projection rest, O-proj weights
+            while (issue_b()) {}                              // cache stream
+        }
+        return;
+    }
+
+    const int g8 = lane >> 2, t4 = lane & 3;
+    // ---- P1 (consumer warps 0..kNA-1): latent projection of this CTA's K split
+    if (warp < kNW) {
+        if (np1 > 0) stage_rows<MT>(a.x, a.B, a.E, a.E, ps * kKS, xbuf, tid);
+        if (osplits > 1) {  // P3 accumulates its K splits into y (2 addends: order-free)
+            const int n = a.B * a.e_out;
+            for (int i = cta * 32 * kNW + tid; i < n; i += G * 32 * kNW) a.y[i] = 0.f;
+        }
+        named_bar_sync(2, 32 * kNW);
+        if (warp < kNA) {
+            // weight-ring slot s is always consumed by warp s (items k = s mod kNA)
+            for (int k = warp; k < np1; k += kNA) {
+                const int slot = k % kNA;
+                mbar_wait(&fullA[slot], static_cast<uint32_t>(k / kNA) & 1u);
+                float facc[MT][2][4];
+                item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(xbuf), lane, facc);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyA[slot]);
+                const int tile = plo + k;
+                float* P = a.P + static_cast<size_t>(ps) * a.B * a.Nrows;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int n = tile * 16 + g8 + ((i & 2) ? 8 : 0);
+                            const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
+                            if (m < a.B) P[static_cast<size_t>(m) * a.Nrows + n] = facc[mt][hh][i];
+                        }
+            }
+        }
+    }
+    STEP_MARK(2);
+    grid_sync(a.bar);  // consumers + helper
+    STEP_MARK(3);
+
+    if (warp == kNW + 1) {
+        // ============================================================ helper warp
+        // (a) per unit, ahead of the consumers: qt = (sum_split c_Q) . M_QK in
+        //     the append epilogue's order (fixed split order, sequential fma);
+        //     for the unit holding the new token, its latent row [c_K | c_V] ->
+        //     cache and shared memory (the stage is patched by its owner warp)
+        for (int j = 0; j < nu; ++j) {
+            const int u = cta + j * G;
+            const int bh = u / nch, ck = u - bh * nch;
+            const int b = bh / a.nh, h = bh - b * a.nh;
+            const bool has_new = (ck + 1) * chunk >= len;
+            const float* pb = a.P + static_cast<size_t>(b) * a.Nrows + static_cast<size_t>(h) * 3 * R + lane;
+            float pv[3][kMaxSplits];
+#pragma unroll
+            for (int s = 0; s < kMaxSplits; ++s) {
+                pv[0][s] = s < splits ? __ldcg(pb + s * pstride) : 0.f;
+                pv[1][s] = (has_new && s < splits) ? __ldcg(pb + s * pstride + R) : 0.f;
+                pv[2][s] = (has_new && s < splits) ? __ldcg(pb + s * pstride + 2 * R) : 0.f;
+            }
+            float mqv[R];
+            const float* mq = a.mqk + static_cast<size_t>(h) * R * R + lane;
+#pragma unroll
+            for (int jj = 0; jj < R; ++jj) mqv[jj] = __ldg(mq + jj * R);
+            float v[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+            for (int s = 0; s < kMaxSplits; ++s)
+#pragma unroll
+                for (int r = 0; r < 3; ++r) v[r] += pv[r][s];  // zeros past `splits` leave the sum exact
+            float qt = 0.f;
+#pragma unroll
+            for (int jj = 0; jj < R; ++jj) qt = fmaf(__shfl_sync(0xffffffffu, v[0], jj), mqv[jj], qt);
+            qts[j * R + lane] = qt;
+            if (has_new) {
+                uint8_t* region = a.cache + static_cast<size_t>(bh) * cap * C::ROWB;
+                const uint32_t grow = static_cast<uint32_t>(pos) * C::ROWB;
+#pragma unroll
+                for (int half = 0; half < 2; ++half) {
+                    const __nv_bfloat16 bv = __float2bfloat16_rn(v[1 + half]);
+                    nrow[j * 2 * R + half * R + lane] = bv;
+                    *reinterpret_cast<__nv_bfloat16*>(region + cache_swz(grow + half * C::PART + 2 * lane)) = bv;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&uready[j]);
+        }
+        // (b) per unit as the consumers finish it: merge the kNW warp states in
+        //     warp order; the last unit of a (sequence, head) to finish merges its
+        //     chunks in chunk order (SoftmaxState::merge, decode.cpp:59-75) into vlat
+        for (int j = 0; j < nu; ++j) {
+            mbar_wait(&sfull[j], 0u);
+            const int u = cta + j * G;
+            const int bh = u / nch, ck = u - bh * nch;
+            const int b = bh / a.nh, h = bh - b * a.nh;
+            const float* rb = wst + j * kNW * (R + 2);
+            float M = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < kNW; ++w) M = fmaxf(M, rb[w * (R + 2) + R]);
+            float L = 0.f, av = 0.f;
+#pragma unroll
+            for (int w = 0; w < kNW; ++w) {
+                const float mw = rb[w * (R + 2) + R];
+                if (mw == -INFINITY) continue;
+                const float f = ex2(mw - M);
+                L = fmaf(rb[w * (R + 2) + R + 1], f, L);
+                av = fmaf(rb[w * (R + 2) + lane], f, av);
+            }
+            float* vout = a.vlat + static_cast<size_t>(b) * a.nh * R + static_cast<size_t>(h) * R;
+            if (nch == 1) {
+                vout[lane] = av / L;
+                continue;
+            }
+            float* wsp = a.ws + (static_cast<size_t>(bh) * a.max_chunks + ck) * (R + 2);
+            wsp[lane] = av;
+            if (lane == 0) {
+                wsp[R] = M;
+                wsp[R + 1] = L;
+            }
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) {
+                int old;
+                asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.counters + bh) : "memory");
+                last = (old == nch - 1);
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (!last) continue;
+            const float* wb = a.ws + static_cast<size_t>(bh) * a.max_chunks * (R + 2);
+            float M2 = -INFINITY;
+            for (int c = 0; c < nch; ++c) M2 = fmaxf(M2, __ldcg(wb + c * (R + 2) + R));
+            float L2 = 0.f, a2 = 0.f;
+            for (int c = 0; c < nch; ++c) {
+                const float mc = __ldcg(wb + c * (R + 2) + R);
+                if (mc == -INFINITY) continue;
+                const float f = ex2(mc - M2);
+                L2 = fmaf(__ldcg(wb + c * (R + 2) + R + 1), f, L2);
+                a2 = fmaf(__ldcg(wb + c * (R + 2) + lane), f, a2);
+            }
+            vout[lane] = a2 / L2;
+            if (lane == 0) a.counters[bh] = 0;  // self-resetting for the next step
+        }
+    } else {
+        // ========================================================= consumer warps
+        // ---- P2: attention units
+        int slot = 0;
+        uint32_t phase = 0;
+        for (int j = 0; j < nu; ++j) {
+            const int u = cta + j * G;
+            const int bh = u / nch, ck = u - bh * nch;
+            const int t0 = ck * chunk, ntok = min(chunk, len - t0);
+            const int ns = (ntok + kST - 1) / kST;
+            const bool has_new = (t0 + ntok == len);
+            mbar_wait(&uready[j], 0u);
+            if (j == 0) STEP_MARK(4);
+            uint32_t qf[KR][2];
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                for (int jj = 0; jj < 2; ++jj) {
+                    const int k0 = kk * 16 + 2 * t4 + 8 * jj;
+                    uint32_t h0, l0, h1, l1;
+                    split_bf16(qts[j * R + k0], h0, l0);
+                    split_bf16(qts[j * R + k0 + 1], h1, l1);
+                    qf[kk][jj] = (g8 == 0) ? (h0 | (h1 << 16)) : (g8 == 1 ? (l0 | (l1 << 16)) : 0u);
+                }
+            float m_w = -INFINITY, l = 0.f;
+            float acc[KR][4];
+#pragma unroll
+            for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) acc[kk][i] = 0.f;
+
+            for (int s = 0; s < ns; ++s) {
+                mbar_wait(&fullB[slot], phase);
+                uint8_t* sp = ringB + slot * C::STAGE;
+                const uint32_t sbase = smem_u32(sp);
+                const int rows = min(kST, ntok - s * kST);
+                const bool patch = has_new && s == ns - 1 && (rows - 1) / 32 == warp;
+                if (patch) {
+                    // the stage was copied before the step's own row existed
+                    const uint32_t srow = static_cast<uint32_t>(rows - 1) * C::ROWB;
+#pragma unroll
+                    for (int half = 0; half < 2; ++half)
+                        *reinterpret_cast<__nv_bfloat16*>(sp + cache_swz(srow + half * C::PART + 2 * lane)) =
+                            nrow[j * 2 * R + half * R + lane];
+                    __syncwarp();
+                }
+                // scores D(16 tok x 8) = K(16 x R) . [qt_hi | qt_lo]: lane (g8, t4 = 0)
+                // holds the hi / lo partials of tokens g8 and g8 + 8
+                float sc[2][2];
+#pragma unroll
+                for (int grp = 0; grp < 2; ++grp) {
+                    const int tb = warp * 32 + grp * 16;
+                    float d[4] = {0.f, 0.f, 0.f, 0.f};
+                    const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+                    for (int kk = 0; kk < KR; ++kk) {
+                        uint32_t a0, a1, a2, a3;
+                        const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
+                        ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
+                        mma_bf16_16816(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+                    }
+                    sc[grp][0] = (t4 == 0 && tb + g8 < rows) ? d[0] + d[1] : -INFINITY;
+                    sc[grp][1] = (t4 == 0 && tb + g8 + 8 < rows) ? d[2] + d[3] : -INFINITY;
+                }
+                const float wm = warp_max(fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])));
+                if (wm > m_w) {
+                    const float f = ex2(m_w - wm);
+                    l *= f;
+#pragma unroll
+                    for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) acc[kk][i] *= f;
+                    m_w = wm;
+                }
+#pragma unroll
+                for (int grp = 0; grp < 2; ++grp) {
+                    const int tb = warp * 32 + grp * 16;
+                    const float p0 = (sc[grp][0] == -INFINITY) ? 0.f : ex2(sc[grp][0] - m_w);
+                    const float p1 = (sc[grp][1] == -INFINITY) ? 0.f : ex2(sc[grp][1] - m_w);
+                    l += p0 + p1;
+                    uint32_t h0, l0, h1, l1;
+                    split_bf16(p0, h0, l0);
+                    split_bf16(p1, h1, l1);
+                    const uint32_t hi2 = h0 | (h1 << 16), lo2 = l0 | (l1 << 16);
+                    const int s0 = 8 * t4, s1 = 8 * t4 + 4;
+                    const uint32_t xh = __shfl_sync(0xffffffffu, hi2, s0), yh = __shfl_sync(0xffffffffu, hi2, s1);
+                    const uint32_t xl = __shfl_sync(0xffffffffu, lo2, s0), yl = __shfl_sync(0xffffffffu, lo2, s1);
+                    const uint32_t xx = (g8 == 0) ? xh : xl, yy = (g8 == 0) ? yh : yl;
+                    const uint32_t b0 = (g8 < 2) ? __byte_perm(xx, yy, 0x5410) : 0u;
+                    const uint32_t b1 = (g8 < 2) ? __byte_perm(xx, yy, 0x7632) : 0u;
+                    const int stok = tb + (lane & 7) + ((lane >> 4) & 1) * 8;
+#pragma unroll
+                    for (int mm = 0; mm < KR; ++mm) {
+                        uint32_t a0, a1, a2, a3;
+                        const uint32_t off = static_cast<uint32_t>(stok * C::ROWB + C::PART + (mm * 2 + ((lane >> 3) & 1)) * 16);
+                        ldsm_x4_trans(sbase + cache_swz(off), a0, a1, a2, a3);
+                        mma_bf16_16816(acc[mm], a0, a1, a2, a3, b0, b1);
+                    }
+                }
+                if (patch)  // generic-proxy writes precede the slot's next TMA
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&emptyB[slot]);
+                if (++slot == C::NB) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+            }
+            // this warp's state of unit j -> the helper
+            float* wr = wst + (j * kNW + warp) * (R + 2);
+            const float lsum = warp_sum(l);
+            if (t4 == 0) {
+#pragma unroll
+                for (int mm = 0; mm < KR; ++mm) {
+                    wr[mm * 16 + g8] = acc[mm][0] + acc[mm][1];
+                    wr[mm * 16 + g8 + 8] = acc[mm][2] + acc[mm][3];
+                }
+            }
+            if (lane == 0) {
+                wr[R] = m_w;
+                wr[R + 1] = lsum;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sfull[j]);
+        }
+        STEP_MARK(5);
+    }
+    STEP_MARK(6);
+    grid_sync(a.bar);  // every vlat row is written; every CTA has read the length
+    STEP_MARK(7);
+    if (cta == 0 && tid == 0) *a.d_len = len;
+
+    // ---- P3: folded O-projection over the prefetched W'_o items
+    if (np3 == 0 || warp >= kNW) {
+        STEP_MARK(8);
+        STEP_MARK(9);
+        return;
+    }
+    // stage the K splits this CTA's items use (vlat rows -> bf16) in the drained attention ring
+    const int K = a.nh * R;
+    unsigned need = 0;
+    for (int j = 0; j < np3; ++j) need |= 1u << ((cta + j * G) % osplits);
+    for (int s = 0; s < osplits; ++s)
+        if (need & (1u << s)) stage_rows<MT>(a.vlat, a.B, K, K, s * kKS, ringB + s * C::XB, tid);
+    named_bar_sync(2, 32 * kNW);
+    STEP_MARK(8);
+    for (int j = 0; j < np3; ++j) {
+        const int k = np1 + j, slot = k % kNA;
+        if (slot != warp) continue;
+        mbar_wait(&fullA[slot], static_cast<uint32_t>(k / kNA) & 1u);
+        const int item = cta + j * G;
+        const int tile = item / osplits, s = item - tile * osplits;
+        float facc[MT][2][4];
+        item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(ringB + s * C::XB), lane, facc);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int n = tile * 16 + g8 + ((i & 2) ? 8 : 0);
+                    const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
+                    if (m < a.B && n < a.e_out) {
+                        float* dst = a.y + static_cast<size_t>(m) * a.e_out + n;
+                        if (osplits == 1) *dst = facc[mt][hh][i];
+                        else atomicAdd(dst, facc[mt][hh][i]);
+                    }
+                }
+    }
+    STEP_MARK(9);
+}
+
+template <int MT>
+cudaError_t launch_mt(const StepArgs& a, cudaStream_t s) {
+    using C = SC<32, MT>;
+    if constexpr (!C::OK) {
+        return cudaErrorInvalidValue;
+    } else {
+        auto k = layer_step_kernel<32, MT>;
+        static bool attr = false;
+        if (!attr) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        return launch_pdl(k, dim3(a.grid), dim3(kThr), C::SMEM, s, a);
+    }
+}
+
+}  // namespace
+
+bool step_supported(int R, int B, int nh, int max_units, int Kp, int oKp, int otiles, int grid) {
+    if (R != 32 || B < 1 || B > 32) return false;
+    if (Kp % kKS != 0 || oKp % kKS != 0) return false;
+    const int splits = Kp / kKS, osplits = oKp / kKS;
+    if (osplits > 2 || splits > grid || splits > kMaxSplits) return false;
+    if ((max_units + grid - 1) / grid > kMaxU) return false;
+    (void)nh;
+    const int n_oitems = otiles * osplits;
+    return (n_oitems + grid - 1) / grid <= kNA;
+}
+
+int step_item_k() { return kKS; }
+
+int step_max_units() { return kMaxU; }
+
+cudaError_t launch_layer_step(const StepArgs& a, cudaStream_t s) {
+    switch ((a.B + 15) / 16) {
+        case 1: return launch_mt<1>(a, s);
+        case 2: return launch_mt<2>(a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace wsvd_k

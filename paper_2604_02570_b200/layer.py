@@ -104,6 +104,20 @@ class DecodeLayer:
                    self._ptr(attn_out) if attn_out is not None else None, self._ptr(y),
                    self._stream(stream))
 
+    def _step_info(self):
+        fused, launches = C.c_int32(0), C.c_int32(0)
+        N.call("wsvd_cache_step_info", self.h, C.byref(fused), C.byref(launches))
+        return bool(fused.value), int(launches.value)
+
+    def launches_per_step(self) -> int:
+        """Kernels one layer step launches (wsvd_cache_step_info)."""
+        return self._step_info()[1]
+
+    def step_kind(self) -> str:
+        fused, n = self._step_info()
+        return ("one persistent fused-step kernel per step (PDL launch)" if fused
+                else f"{n} kernels per step, replayed as one CUDA graph")
+
     def step_host(self, x_host, y_host, stream=None):
         """Same through host buffers (pinned torch tensors or numpy arrays)."""
         def hp(t):
@@ -122,13 +136,15 @@ class DecodeLayer:
 
     def debug_copy(self, what: str) -> np.ndarray:
         """Internal buffers of the last append (see wsvd_cache_debug_copy)."""
-        code = {"xq": 0, "sx": 1, "acc": 2, "qt": 3}[what]
+        code = {"xq": 0, "sx": 1, "acc": 2, "qt": 3, "trace": 4}[what]
         nbytes = C.c_int64(1 << 30)
         buf = np.empty(1 << 28, dtype=np.uint8)
         N.call("wsvd_cache_debug_copy", self.h, code, C.c_void_p(buf.ctypes.data), C.byref(nbytes))
         raw = buf[: nbytes.value].copy()
         if what == "xq":
             return raw.view(np.int8)
+        if what == "trace":
+            return raw.view(np.uint64).reshape(-1, 10)
         if what == "acc":
             return raw.view(np.int32 if self.layer.weight_dtype in ("i8", "i4") else np.float32)
         return raw.view(np.float32)

@@ -30,7 +30,10 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1)
         if (lane == 0) {
             int slot = 0;
             uint32_t ph = 0;
-            for (size_t s = blockIdx.x; s < nstage; s += gridDim.x) {
+            const size_t per = (nstage + gridDim.x - 1) / gridDim.x;
+            const size_t s0 = (mode & 2) ? blockIdx.x * per : blockIdx.x, s1 = (mode & 2) ? min(nstage, s0 + per) : nstage;
+            const size_t ds = (mode & 2) ? 1 : gridDim.x;
+            for (size_t s = s0; s < s1; s += ds) {
                 mbar_wait(&empty[slot], ph ^ 1u);
                 mbar_arrive_expect_tx(&full[slot], stage_bytes);
                 tma_bulk_g2s(smem + slot * stage_bytes, src + s * stage_bytes, stage_bytes, &full[slot]);
@@ -43,9 +46,12 @@ __global__ void __launch_bounds__(32 * (NCW + 1), 1)
     uint32_t ph = 0;
     float acc = 0.f;
     const int rowb = stage_bytes / (32 * NCW);
-    for (size_t s = blockIdx.x; s < nstage; s += gridDim.x) {
+    const size_t per = (nstage + gridDim.x - 1) / gridDim.x;
+    const size_t s0 = (mode & 2) ? blockIdx.x * per : blockIdx.x, s1 = (mode & 2) ? min(nstage, s0 + per) : nstage;
+    const size_t ds = (mode & 2) ? 1 : gridDim.x;
+    for (size_t s = s0; s < s1; s += ds) {
         mbar_wait(&full[slot], ph);
-        if (mode >= 1) {
+        if (mode & 1) {
             const uint32_t row = smem_u32(smem + slot * stage_bytes) + tid * rowb;
             for (int c = 0; c < rowb; c += 16) {
                 uint4 v = lds128(row + ((c + lane * 16) % rowb));
@@ -70,7 +76,7 @@ __global__ void ldg_kernel(const uint4* __restrict__ src, size_t n, float* sink)
 }
 
 int main() {
-    const size_t total = 256ull << 20;
+    const size_t total = 1024ull << 20;
     uint8_t* buf;
     float* sink;
     cudaMalloc(&buf, total);
@@ -93,7 +99,7 @@ int main() {
         return total / (ms / 10 / 1e3) / 1e9;
     };
     printf("ldg 148x8x256: %.0f GB/s\n", timeit([&] { ldg_kernel<<<sms * 8, 256>>>((const uint4*)buf, total / 16, sink); }));
-    for (int mode = 0; mode < 2; ++mode)
+    for (int mode = 0; mode < 4; ++mode)
         for (int sb : {8192, 16384, 32768})
             for (int st : {4, 6, 8, 12}) {
                 const int smem = sb * st + 256;

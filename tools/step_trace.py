@@ -1,0 +1,54 @@
+"""Phase timeline of the fused layer-step kernel (step.cu STEP_MARK points),
+from %globaltimer stamps of every CTA: run with WSVD_STEP_TRACE=1.
+
+    WSVD_STEP_TRACE=1 python tools/step_trace.py [--config ...]
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("WSVD_STEP_TRACE", "1")
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2604_02570_b200.layer import DecodeLayer  # noqa: E402
+
+MARKS = ["entry", "griddep", "P1 done", "barrier1", "qt ready", "attn done", "merged", "barrier2",
+         "P3 staged", "end"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
+    ap.add_argument("--steps", type=int, default=5)
+    args = ap.parse_args()
+    cfg = bench.CONFIGS[args.config]
+    E, B, L = cfg["E"], cfg["B"], cfg["L"]
+    f, w_o = bench.synthetic_layer(cfg)
+    layer = DecodeLayer(f, w_o, batch=B, capacity=L + 64, cache_dtype=cfg["cache"], weight_dtype=cfg["weights"])
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    for t0 in range(0, L - 1 - args.steps, 256):
+        n = min(256, L - 1 - args.steps - t0)
+        layer.prefill(torch.randn((n, B, E), generator=g, device=dev))
+    x = torch.randn((B, E), generator=g, device=dev)
+    y = torch.empty((B, E), device=dev)
+    for _ in range(args.steps):
+        layer.step(x, y, graph=False)
+    torch.cuda.synchronize()
+    t = layer.debug_copy("trace").astype(np.int64)
+    t0 = t[:, 0].min()
+    rel = (t - t0) / 1e3
+    print(f"{'mark':10s} {'min':>8s} {'median':>8s} {'max':>8s}   (us from the first CTA's entry)")
+    for k, name in enumerate(MARKS):
+        col = rel[:, k]
+        print(f"{name:10s} {col.min():8.2f} {np.median(col):8.2f} {col.max():8.2f}")
+
+
+if __name__ == "__main__":
+    main()
