@@ -237,6 +237,7 @@ struct wsvd_cache_s {
     DevBuf oP, y_tmp;                 // O-proj partials
     DevBuf x_dev, y_dev;              // staging for the host-buffer step
     DevBuf trace;                     // fused-step phase timeline (WSVD_STEP_TRACE)
+    DevBuf xo;                        // fused step: bf16 X rows of the O-projection
     int chunk = 512, max_chunks = 1, grid = 148;
     int fmax_chunks = 1;              // split-KV chunks of the fused step kernel
     int sms = 148;
@@ -442,7 +443,7 @@ bool fused_step_ok(wsvd_cache_s* c) {
     if (L->ks != step_item_k() || L->oks != step_item_k()) return false;
     // the chunk count never exceeds max_chunks (adaptive) or the capacity split (fixed chunk)
     const int mc = c->chunk > 0 ? c->max_chunks : c->fmax_chunks;
-    return step_supported(L->R, c->B, L->d.n_heads, c->B * L->d.n_heads * mc, L->Kp, L->oKp,
+    return step_supported(L->R, c->B, L->d.n_heads, c->B * L->d.n_heads * mc, mc, L->Kp, L->oKp,
                           round_up(L->e_out, 16) / 16, c->sms);
 }
 
@@ -467,6 +468,9 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s) {
     a.Wo = L->Wo.as<uint8_t>();
     a.d_len = c->d_len();
     a.bar = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 4);
+    const size_t xob = step_xo_bytes(c->B, L->oKp);
+    if (c->xo.n < xob) CUDA_TRY(c->xo.alloc(xob));  // zeroed: rows past the batch stay 0
+    a.xo = c->xo.as<uint8_t>();
     a.B = c->B;
     a.nh = L->d.n_heads;
     a.E = L->d.embed_dim;
@@ -800,7 +804,7 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     if (e == cudaSuccess)
         e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh *
-                             std::max(c->max_chunks * attn_parts_per_chunk(), c->fmax_chunks) * (L->R + 2) * 4);
+                             std::max(c->max_chunks * attn_parts_per_chunk() * (L->R + 2), c->fmax_chunks * (L->R + 4)) * 4);
     if (e == cudaSuccess) e = c->attn_cnt.alloc(static_cast<size_t>(batch) * nh * 4);
     if (e == cudaSuccess) e = c->vlat.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     (void)H;

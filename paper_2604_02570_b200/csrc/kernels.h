@@ -116,12 +116,14 @@ struct StepArgs {
     const uint8_t* Wo;     // folded O-projection W-tiles (bf16, K split 512)
     int* d_len;            // committed length (the new row goes to *d_len)
     unsigned* bar;         // [2] grid barrier (count, generation)
+    uint8_t* xo;           // [osplits][MT*16][1088] bf16 X rows of the O-projection
     uint64_t* trace;       // [grid][8] %globaltimer at the phase marks, or null
     int B, nh, E, Kp, Nrows, e_out, oKp, otiles, cap;
     int chunk, max_chunks, grid;
 };
-bool step_supported(int R, int B, int nh, int max_units, int Kp, int oKp, int otiles, int grid);
+bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp, int oKp, int otiles, int grid);
 int step_item_k();
+size_t step_xo_bytes(int B, int oKp);  // bytes of StepArgs::xo
 int step_max_units();  // attention units one CTA of the fused step can hold
 cudaError_t launch_layer_step(const StepArgs& a, cudaStream_t s);
 

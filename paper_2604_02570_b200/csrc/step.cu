@@ -48,6 +48,7 @@ constexpr int kNA = 4;               // weight ring slots == projection consumer
 constexpr int kXS = kKS * 2 + 64;    // bytes per staged token row (stride == 64 mod 128)
 constexpr int kMaxU = 8;             // attention units per CTA (host-checked)
 constexpr int kMaxSplits = 16;       // projection K splits (host-checked)
+constexpr int kWS = 36;              // floats per unit state in ws: acc[32], m, l, pad (16 B rows)
 
 template <int R, int MT>
 struct SC {
@@ -65,7 +66,7 @@ struct SC {
     static constexpr int RED_OFF = X_OFF + XB;
     static constexpr int BAR_OFF = RED_OFF + RED;
     static constexpr int SMEM = BAR_OFF + 512;
-    static constexpr bool OK = NB_RAW >= 2 && 2 * XB <= NB * STAGE;
+    static constexpr bool OK = NB_RAW >= 2;
 };
 
 WSVD_DEV float ex2(float x) {
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     uint64_t* emptyB = fullB + C::NB;
     uint64_t* uready = emptyB + C::NB;  // [kMaxU] unit j's query / new row prepared (helper)
     uint64_t* sfull = uready + kMaxU;   // [kMaxU] unit j's warp states written (consumers)
+    uint64_t* p3bar = sfull + kMaxU;    // P3: chunk states landed (one phase per staged split)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
             mbar_init(&uready[i], 1);
             mbar_init(&sfull[i], kNW);
         }
+        mbar_init(p3bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -383,13 +386,17 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
             if (lane == 0) mbar_arrive(&uready[j]);
         }
         // (b) per unit as the consumers finish it: merge the kNW warp states in
-        //     warp order; the last unit of a (sequence, head) to finish merges its
-        //     chunks in chunk order (SoftmaxState::merge, decode.cpp:59-75) into vlat
+        //     warp order.  A unit that is not the last chunk of its (sequence,
+        //     head) publishes its state to ws and releases a count; the last
+        //     chunk's unit ("home") waits for the others and merges every chunk
+        //     in chunk order (SoftmaxState::merge, decode.cpp:59-75) into the
+        //     bf16 X rows of the O-projection (xo).  A home unit only waits for
+        //     units of an earlier or equal round on lower CTAs, so the waits
+        //     cannot form a cycle.
         for (int j = 0; j < nu; ++j) {
             mbar_wait(&sfull[j], 0u);
             const int u = cta + j * G;
             const int bh = u / nch, ck = u - bh * nch;
-            const int b = bh / a.nh, h = bh - b * a.nh;
             const float* rb = wst + j * kNW * (R + 2);
             float M = -INFINITY;
 #pragma unroll
@@ -403,39 +410,47 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 L = fmaf(rb[w * (R + 2) + R + 1], f, L);
                 av = fmaf(rb[w * (R + 2) + lane], f, av);
             }
-            float* vout = a.vlat + static_cast<size_t>(b) * a.nh * R + static_cast<size_t>(h) * R;
-            if (nch == 1) {
-                vout[lane] = av / L;
+            if (ck < nch - 1) {
+                float* wsp = a.ws + (static_cast<size_t>(bh) * a.max_chunks + ck) * kWS;
+                wsp[lane] = av;
+                if (lane == 0) {
+                    wsp[R] = M;
+                    wsp[R + 1] = L;
+                }
+                __syncwarp();
+                if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.counters + bh) : "memory");
                 continue;
             }
-            float* wsp = a.ws + (static_cast<size_t>(bh) * a.max_chunks + ck) * (R + 2);
-            wsp[lane] = av;
-            if (lane == 0) {
-                wsp[R] = M;
-                wsp[R + 1] = L;
+            if (nch > 1) {
+                if (lane == 0)
+                    while (ld_acquire(reinterpret_cast<const unsigned*>(a.counters + bh)) < static_cast<unsigned>(nch - 1)) {
+                    }
+                __syncwarp();
+                const float* wb = a.ws + static_cast<size_t>(bh) * a.max_chunks * kWS;
+                float M2 = M;
+                for (int c = 0; c < nch - 1; ++c) M2 = fmaxf(M2, __ldcg(wb + c * kWS + R));
+                float L2 = 0.f, a2 = 0.f;
+                for (int c = 0; c < nch - 1; ++c) {
+                    const float mc = __ldcg(wb + c * kWS + R);
+                    if (mc == -INFINITY) continue;
+                    const float f = ex2(mc - M2);
+                    L2 = fmaf(__ldcg(wb + c * kWS + R + 1), f, L2);
+                    a2 = fmaf(__ldcg(wb + c * kWS + lane), f, a2);
+                }
+                if (M != -INFINITY) {
+                    const float f = ex2(M - M2);
+                    L2 = fmaf(L, f, L2);
+                    a2 = fmaf(av, f, a2);
+                }
+                av = a2;
+                L = L2;
+                if (lane == 0) a.counters[bh] = 0;  // self-resetting for the next step
             }
-            __syncwarp();
-            int last = 0;
-            if (lane == 0) {
-                int old;
-                asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.counters + bh) : "memory");
-                last = (old == nch - 1);
-            }
-            last = __shfl_sync(0xffffffffu, last, 0);
-            if (!last) continue;
-            const float* wb = a.ws + static_cast<size_t>(bh) * a.max_chunks * (R + 2);
-            float M2 = -INFINITY;
-            for (int c = 0; c < nch; ++c) M2 = fmaxf(M2, __ldcg(wb + c * (R + 2) + R));
-            float L2 = 0.f, a2 = 0.f;
-            for (int c = 0; c < nch; ++c) {
-                const float mc = __ldcg(wb + c * (R + 2) + R);
-                if (mc == -INFINITY) continue;
-                const float f = ex2(mc - M2);
-                L2 = fmaf(__ldcg(wb + c * (R + 2) + R + 1), f, L2);
-                a2 = fmaf(__ldcg(wb + c * (R + 2) + lane), f, a2);
-            }
-            vout[lane] = a2 / L2;
-            if (lane == 0) a.counters[bh] = 0;  // self-resetting for the next step
+            // latent output -> X row of the O-projection (bf16, K index h*R + lane)
+            const int b = bh / a.nh, h = bh - b * a.nh;
+            const int k = h * R + lane, s = k / kKS;
+            __nv_bfloat16* xr = reinterpret_cast<__nv_bfloat16*>(a.xo + (static_cast<size_t>(s) * MT * 16 + b) * kXS);
+            xr[k - s * kKS] = __float2bfloat16_rn(av / L);
         }
     } else {
         // ========================================================= consumer warps
@@ -565,7 +580,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         STEP_MARK(5);
     }
     STEP_MARK(6);
-    grid_sync(a.bar);  // every vlat row is written; every CTA has read the length
+    grid_sync(a.bar);  // every unit state is written; every CTA has read the length
     STEP_MARK(7);
     if (cta == 0 && tid == 0) *a.d_len = len;
 
@@ -575,12 +590,23 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         STEP_MARK(9);
         return;
     }
-    // stage the K splits this CTA's items use (vlat rows -> bf16) in the drained attention ring
-    const int K = a.nh * R;
+    // The X slices this CTA's items use (bf16 rows built by the home units)
+    // arrive with one TMA bulk copy each
     unsigned need = 0;
     for (int j = 0; j < np3; ++j) need |= 1u << ((cta + j * G) % osplits);
-    for (int s = 0; s < osplits; ++s)
-        if (need & (1u << s)) stage_rows<MT>(a.vlat, a.B, K, K, s * kKS, ringB + s * C::XB, tid);
+    if (tid == 0) {
+        // xo was written by other CTAs' generic stores (ordered by barrier 2);
+        // order them before this thread's async-proxy reads
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        uint32_t bytes = 0;
+        for (int s = 0; s < osplits; ++s)
+            if (need & (1u << s)) bytes += C::XB;
+        mbar_arrive_expect_tx(p3bar, bytes);
+        for (int s = 0; s < osplits; ++s)
+            if (need & (1u << s))
+                tma_bulk_g2s(ringB + s * C::XB, a.xo + static_cast<size_t>(s) * C::XB, C::XB, p3bar);
+    }
+    mbar_wait(p3bar, 0u);
     named_bar_sync(2, 32 * kNW);
     STEP_MARK(8);
     for (int j = 0; j < np3; ++j) {
@@ -628,7 +654,7 @@ cudaError_t launch_mt(const StepArgs& a, cudaStream_t s) {
 
 }  // namespace
 
-bool step_supported(int R, int B, int nh, int max_units, int Kp, int oKp, int otiles, int grid) {
+bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp, int oKp, int otiles, int grid) {
     if (R != 32 || B < 1 || B > 32) return false;
     if (Kp % kKS != 0 || oKp % kKS != 0) return false;
     const int splits = Kp / kKS, osplits = oKp / kKS;
@@ -636,10 +662,17 @@ bool step_supported(int R, int B, int nh, int max_units, int Kp, int oKp, int ot
     if ((max_units + grid - 1) / grid > kMaxU) return false;
     (void)nh;
     const int n_oitems = otiles * osplits;
-    return (n_oitems + grid - 1) / grid <= kNA;
+    if ((n_oitems + grid - 1) / grid > kNA) return false;
+    // P3 stages its X slices in the attention ring
+    const int mt = (B + 15) / 16;
+    const int ring = (mt == 1 ? SC<32, 1>::NB * SC<32, 1>::STAGE : SC<32, 2>::NB * SC<32, 2>::STAGE);
+    (void)max_chunks;
+    return osplits * mt * 16 * kXS <= ring;
 }
 
 int step_item_k() { return kKS; }
+
+size_t step_xo_bytes(int B, int oKp) { return static_cast<size_t>(oKp / kKS) * ((B + 15) / 16) * 16 * kXS; }
 
 int step_max_units() { return kMaxU; }
 
