@@ -8,13 +8,15 @@ nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem,power.limit --for
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 python tools/timing.py > gpurun_out/timing.txt 2>&1
-# prefill = 1024 kernel launches matching the filter; then the timed decode steps
-FILTER='regex:skinny_stream|append_epilogue|decode_attn|attn_combine|reduce_partials|act_quant'
+# the decode steps (one fused layer_step_kernel each; the prefill uses other
+# kernels), then the attention kernel the bench times alone
+FILTER='regex:layer_step|decode_attn|attn_combine'
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k "$FILTER" -s 1024 -c 40 --csv --log-file gpurun_out/launches.csv \
+    -k "$FILTER" -c 12 --csv --log-file gpurun_out/launches.csv \
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:layer_step -s 3 -c 1 \
+    -o gpurun_out/step_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:decode_attn -s 3 -c 1 \
     -o gpurun_out/attn_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:skinny_stream -s 512 -c 1 \
-    -o gpurun_out/gemm_full python bench.py --steps 3 --warmup 3 --no-cpu-baseline --soak-ms 0 > /dev/null 2>&1
+python tools/step_trace.py > gpurun_out/step_trace.txt 2>&1
 ls -la gpurun_out

@@ -86,12 +86,15 @@ def summarize_launches(tag):
                      f"{m.get('dram__bytes_read.sum', 0) / 1e6:.2f},{m.get('dram__bytes_write.sum', 0) / 1e6:.2f}")
     with open(os.path.join(OUT, f"{tag}_launches.csv"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    attn = [m for (i, k), m in per.items() if "decode_attn" in k]
-    if attn:
-        traffic = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for m in attn) / len(attn)
-        with open(os.path.join(OUT, "attn_traffic.json"), "w") as fh:
+    for key, fname, unit in (("decode_attn", "attn_traffic.json", "decode_attn_kernel"),
+                             ("layer_step", "step_traffic.json", "layer_step_kernel")):
+        ms = [m for (i, k), m in per.items() if key in k]
+        if not ms:
+            continue
+        traffic = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for m in ms) / len(ms)
+        with open(os.path.join(OUT, fname), "w") as fh:
             json.dump({"7b-r32-b16-ctx4k-bf16": round(traffic), "source": f"profiles/{tag}_launches.csv",
-                       "unit": "bytes per decode_attn_kernel launch (dram read + write, ncu)"}, fh, indent=1)
+                       "unit": f"bytes per {unit} launch (dram read + write, ncu)"}, fh, indent=1)
     return per
 
 
@@ -99,9 +102,9 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(OUT, exist_ok=True)
     summarize_launches(tag)
-    for name in ("attn_full", "gemm_full"):
+    for name in ("step_full", "attn_full", "gemm_full"):
         summarize_full(name, tag)
-    for f in ("bench.json", "bench_ref.json", "timing.txt", "gpu.txt"):
+    for f in ("bench.json", "bench_ref.json", "timing.txt", "gpu.txt", "step_trace.txt"):
         src = os.path.join(RAW, f)
         if os.path.exists(src):
             with open(src) as a, open(os.path.join(OUT, f"{tag}_{f}"), "w") as b:
