@@ -145,6 +145,19 @@ int wsvd_cache_read_host(wsvd_cache_t cache, int32_t b, int32_t head, double* ck
 /* raw device rows of sequence b, head h: rows [len][row_bytes] and (I8 only)
  * fp16 scale pairs [len][2]; for bit-exact checks. */
 int wsvd_cache_row_bytes(wsvd_cache_t cache, int32_t* row_bytes);
+/* Attention algorithm of a cache (both give the reference's results up to fp32
+ * reassociation; SURVEY.md 7 "hard parts"):
+ *   WSVD_ATTN_ABSORBED     scores against the absorbed query qt = q . B_K^T
+ *                          (r MACs per cached token; default, all dtypes);
+ *   WSVD_ATTN_EXPLICIT_TC  the reference's explicit key rebuild
+ *                          key_j = C_K[j] . B_K (decode.cpp:188) on tcgen05
+ *                          tensor cores into TMEM (bf16 cache and factors,
+ *                          rank 32, head dim 128; ECONFIG otherwise). */
+#define WSVD_ATTN_ABSORBED 0
+#define WSVD_ATTN_EXPLICIT_TC 1
+int wsvd_cache_set_attention_mode(wsvd_cache_t cache, int32_t mode);
+int wsvd_cache_attention_mode(wsvd_cache_t cache, int32_t* mode);
+
 /* How wsvd_layer_step(_graph/_host) runs for this cache: *fused = 1 when the
  * whole step is the single persistent kernel of step.cu (bf16, rank 32,
  * batch <= 32), 0 for the multi-kernel path; *launches = kernels per step. */

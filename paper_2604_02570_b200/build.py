@@ -29,7 +29,7 @@ CUDA_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompil
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall", "-Wextra", f"-I{os.path.join(ROOT, 'include')}",
              "-I/usr/local/cuda/include"]
 
-CU_SOURCES = ["attn.cu", "gemm.cu", "append.cu", "step.cu", "capi.cu"]
+CU_SOURCES = ["attn.cu", "attn_tc.cu", "gemm.cu", "append.cu", "step.cu", "capi.cu"]
 CXX_SOURCES = ["host_decode.cpp"]
 
 

@@ -671,6 +671,16 @@ int attn_occupancy(int cdtype, int R) {
     return attn_smem_bytes(cdtype, R) > 0 ? 1 : 0;  // persistent: one CTA per SM
 }
 
+cudaError_t launch_attn_combine(const AttnArgs& a, int parts_per_chunk, cudaStream_t s) {
+    const int csmem = (a.max_chunks * parts_per_chunk * (a.R + 2) + a.R) * 4;
+    if (csmem > g_combine_smem_attr) {
+        cudaError_t e = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
+        if (e != cudaSuccess) return e;
+        g_combine_smem_attr = csmem;
+    }
+    return launch_pdl(attn_combine_kernel, dim3(a.B * a.nh), dim3(128), csmem, s, a, parts_per_chunk);
+}
+
 cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s) {
     switch (a.cdtype) {
         case F32: return launch_cd<F32>(a, s);

@@ -218,6 +218,8 @@ struct wsvd_layer_s {
     std::vector<double> b_host[3];    // [nh][R][H] device B values per role (for host folds)
     DevBuf mqk;                       // [nh][R][R] qt_scale * B_Q . B_K^T (fp32)
     bool mqk_ready = false;
+    DevBuf bkt;                       // [nh] B_K^T tiles for the tcgen05 attention (attn_tc.cu)
+    bool bkt_ready = false;
 };
 
 struct GraphKey {
@@ -238,6 +240,8 @@ struct wsvd_cache_s {
     DevBuf x_dev, y_dev;              // staging for the host-buffer step
     DevBuf trace;                     // fused-step phase timeline (WSVD_STEP_TRACE)
     DevBuf xo;                        // fused step: bf16 X rows of the O-projection
+    int attn_mode = 0;                // WSVD_ATTN_ABSORBED or WSVD_ATTN_EXPLICIT_TC
+    DevBuf qfull;                     // [B][nh][H] query of the last append (explicit mode)
     int chunk = 512, max_chunks = 1, grid = 148;
     int fmax_chunks = 1;              // split-KV chunks of the fused step kernel
     int sms = 148;
@@ -329,6 +333,25 @@ int ensure_mqk(wsvd_layer_s* L) {
     return WSVD_OK;
 }
 
+// B_K^T of every head in the tcgen05 B-operand layout (attn_tc.cu), from the
+// device's bf16 B_K values
+int ensure_bkt(wsvd_layer_s* L) {
+    if (L->bkt_ready) return WSVD_OK;
+    const int nh = L->d.n_heads, R = L->R, H = L->d.head_dim;
+    const size_t per = static_cast<size_t>(attn_tc_btile_bytes());
+    std::vector<uint8_t> t(per * nh, 0);
+    for (int h = 0; h < nh; ++h)
+        for (int r = 0; r < R; ++r)
+            for (int d = 0; d < H; ++d) {
+                const uint16_t v = f32_to_bf16_bits(static_cast<float>(L->b_host[1][(static_cast<size_t>(h) * R + r) * H + d]));
+                std::memcpy(t.data() + h * per + attn_tc_btile_offset(d, r), &v, 2);
+            }
+    if (!L->bkt.p) CUDA_TRY(L->bkt.alloc(t.size()));
+    CUDA_TRY(cudaMemcpy(L->bkt.p, t.data(), t.size(), cudaMemcpyHostToDevice));
+    L->bkt_ready = true;
+    return WSVD_OK;
+}
+
 int run_append(wsvd_cache_s* c, const float* x, int T, float* q_out, float* qt, int commit, cudaStream_t s) {
     wsvd_layer_s* L = c->L;
     const int M = T * c->B;
@@ -375,7 +398,8 @@ int run_append(wsvd_cache_s* c, const float* x, int T, float* q_out, float* qt, 
 
 // out: per-head outputs (B_V applied) or null; vlat: latent outputs or null;
 // len_add: rows appended by this step but not yet committed to *d_len
-int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStream_t s) {
+int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStream_t s,
+                  const float* q = nullptr) {
     wsvd_layer_s* L = c->L;
     AttnArgs a{};
     a.cache = c->data.as<uint8_t>();
@@ -400,6 +424,17 @@ int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStr
     a.cdtype = c->cdtype;
     a.row_bytes = c->row_bytes;
     a.grid = c->grid;
+    if (c->attn_mode == WSVD_ATTN_EXPLICIT_TC) {
+        // explicit key reconstruction on tcgen05 (attn_tc.cu), then the combine
+        int rc = ensure_bkt(L);
+        if (rc) return rc;
+        a.bkt = L->bkt.as<uint8_t>();
+        a.q = q ? q : c->qfull.as<float>();
+        a.grid = c->sms;
+        CUDA_TRY(launch_decode_attn_tc(a, s));
+        CUDA_TRY(launch_attn_combine(a, 8, s));
+        return WSVD_OK;
+    }
     CUDA_TRY(launch_decode_attn(a, s));
     return WSVD_OK;
 }
@@ -439,7 +474,8 @@ int run_oproj(wsvd_cache_s* c, const float* vlat, float* y, int* commit_len, cud
 bool fused_step_ok(wsvd_cache_s* c) {
     static const bool off = getenv("WSVD_STEP_MULTI") != nullptr;  // A/B switch: multi-kernel step
     const wsvd_layer_s* L = c->L;
-    if (off || c->cdtype != BF16 || L->d.weight_dtype != BF16 || L->o_dtype != BF16 || !L->Wo.p) return false;
+    if (off || c->attn_mode != WSVD_ATTN_ABSORBED) return false;
+    if (c->cdtype != BF16 || L->d.weight_dtype != BF16 || L->o_dtype != BF16 || !L->Wo.p) return false;
     if (L->ks != step_item_k() || L->oks != step_item_k()) return false;
     // the chunk count never exceeds max_chunks (adaptive) or the capacity split (fixed chunk)
     const int mc = c->chunk > 0 ? c->max_chunks : c->fmax_chunks;
@@ -496,7 +532,9 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s) {
 // -> combine -> folded O-projection, whose first thread commits the length
 int layer_step_impl(wsvd_cache_s* c, const float* x, float* attn_out, float* y, cudaStream_t s) {
     if (attn_out == nullptr && fused_step_ok(c)) return run_step_fused(c, x, y, s);
-    int rc = run_append(c, x, 1, nullptr, c->qt.as<float>(), 0, s);
+    const bool tc = c->attn_mode == WSVD_ATTN_EXPLICIT_TC;
+    int rc = tc ? run_append(c, x, 1, c->qfull.as<float>(), nullptr, 0, s)
+                : run_append(c, x, 1, nullptr, c->qt.as<float>(), 0, s);
     if (rc) return rc;
     rc = run_attention(c, attn_out, c->vlat.as<float>(), 1, s);
     if (rc) return rc;
@@ -807,6 +845,10 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
                              std::max(c->max_chunks * attn_parts_per_chunk() * (L->R + 2), c->fmax_chunks * (L->R + 4)) * 4);
     if (e == cudaSuccess) e = c->attn_cnt.alloc(static_cast<size_t>(batch) * nh * 4);
     if (e == cudaSuccess) e = c->vlat.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
+    if (e == cudaSuccess) e = c->qfull.alloc(static_cast<size_t>(batch) * nh * L->d.head_dim * 4);
+    if (const char* env = getenv("WSVD_ATTN_MODE"))  // default for new caches (A/B runs)
+        if (std::string(env) == "tc" && attn_tc_supported(cache_dtype, L->R, L->d.head_dim, L->bdtype))
+            c->attn_mode = WSVD_ATTN_EXPLICIT_TC;
     (void)H;
     if (e != cudaSuccess) {
         delete c;
@@ -856,6 +898,26 @@ int wsvd_cache_bind_layer(wsvd_cache_t c, wsvd_layer_t L) {
 int wsvd_cache_length(wsvd_cache_t c, int32_t* len) {
     if (!c || !len) return set_err(WSVD_ECONFIG, "null argument");
     *len = c->len;
+    return WSVD_OK;
+}
+
+int wsvd_cache_set_attention_mode(wsvd_cache_t c, int32_t mode) {
+    if (!c) return set_err(WSVD_ECONFIG, "null cache");
+    if (mode == WSVD_ATTN_ABSORBED) {
+        c->attn_mode = mode;
+        return WSVD_OK;
+    }
+    if (mode != WSVD_ATTN_EXPLICIT_TC) return set_err(WSVD_ECONFIG, "unknown attention mode");
+    const wsvd_layer_s* L = c->L;
+    if (!attn_tc_supported(c->cdtype, L->R, L->d.head_dim, L->bdtype))
+        return set_err(WSVD_ECONFIG, "explicit tcgen05 attention needs a bf16 cache, bf16 factors, rank 32 and head dim 128");
+    c->attn_mode = mode;
+    return WSVD_OK;
+}
+
+int wsvd_cache_attention_mode(wsvd_cache_t c, int32_t* mode) {
+    if (!c || !mode) return set_err(WSVD_ECONFIG, "null argument");
+    *mode = c->attn_mode;
     return WSVD_OK;
 }
 
@@ -987,8 +1049,18 @@ int wsvd_append_token(wsvd_cache_t c, const float* x, float* q_out, void* stream
     if (rc) return rc;
     if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
     CUDA_TRY(cudaSetDevice(c->L->d.device));
-    rc = run_append(c, x, 1, q_out, c->qt.as<float>(), 1, static_cast<cudaStream_t>(stream));
-    if (rc) return rc;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (c->attn_mode == WSVD_ATTN_EXPLICIT_TC) {
+        // the explicit kernel attends with q itself (kept for wsvd_decode_attention)
+        rc = run_append(c, x, 1, c->qfull.as<float>(), nullptr, 1, s);
+        if (rc) return rc;
+        if (q_out)
+            CUDA_TRY(cudaMemcpyAsync(q_out, c->qfull.p, static_cast<size_t>(c->B) * c->L->d.n_heads * c->L->d.head_dim * 4,
+                                     cudaMemcpyDeviceToDevice, s));
+    } else {
+        rc = run_append(c, x, 1, q_out, c->qt.as<float>(), 1, s);
+        if (rc) return rc;
+    }
     c->len += 1;
     return WSVD_OK;
 }
@@ -1020,6 +1092,7 @@ int wsvd_fused_decode_step(wsvd_cache_t c, const float* q, int32_t tile_len, flo
     wsvd_layer_s* L = c->L;
     CUDA_TRY(cudaSetDevice(L->d.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (c->attn_mode == WSVD_ATTN_EXPLICIT_TC) return run_attention(c, out, nullptr, 0, s, q);
     CUDA_TRY(launch_absorb_query(q, c->B, L->d.n_heads, L->R, L->d.head_dim, L->B[1].p, L->b_scale[1].as<float>(),
                                  L->bdtype, 1.4426950408889634f / std::sqrt(static_cast<float>(L->d.head_dim)),
                                  c->qt.as<float>(), s));

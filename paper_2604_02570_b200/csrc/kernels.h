@@ -94,11 +94,22 @@ struct AttnArgs {
     int len_add;            // 1 when the step's own row is appended but not yet committed
     int B, nh, H, R, cap, chunk, max_chunks, cdtype, row_bytes;
     int grid;               // persistent CTAs
+    // explicit key reconstruction (attn_tc.cu): per-head B_K^T tiles and the query
+    const uint8_t* bkt;     // [nh][attn_tc_btile_bytes()] bf16, MMA B-operand layout
+    const float* q;         // [B][nh][H] query rows
 };
 int attn_smem_bytes(int cdtype, int R);
 int attn_occupancy(int cdtype, int R);  // resident CTAs per SM (0 if unsupported)
 int attn_parts_per_chunk();             // warp partials published per unit
 cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s);
+// split-KV combine alone (attn.cu): merges parts_per_chunk warp partials per chunk
+cudaError_t launch_attn_combine(const AttnArgs& a, int parts_per_chunk, cudaStream_t s);
+
+// tcgen05 explicit-reconstruction attention (attn_tc.cu): bf16 cache, R = 32, H = 128
+bool attn_tc_supported(int cdtype, int R, int H, int bdtype);
+int attn_tc_btile_bytes();
+size_t attn_tc_btile_offset(int d, int r);
+cudaError_t launch_decode_attn_tc(const AttnArgs& a, cudaStream_t s);  // + launch_attn_combine(a, 8)
 
 // ------------------------------------------------- fused layer step (step.cu) --
 // projection -> append -> attention -> combine -> folded O-projection as one

@@ -28,7 +28,7 @@ class DecodeLayer:
     def __init__(self, f: LayerFactors, w_o_rows: np.ndarray | None, batch: int, capacity: int,
                  cache_dtype: str = "bf16", weight_dtype: str = "bf16", oproj_dtype: str = "bf16",
                  device: int = 0, head_offset: int = 0, act_rotation: bool | None = None,
-                 quantized=None):
+                 quantized=None, attention: str | None = None):
         if cache_dtype not in ("f32", "bf16", "i8"):
             raise ConfigError(f"unknown cache dtype '{cache_dtype}'")
         self.device = device
@@ -50,6 +50,23 @@ class DecodeLayer:
         rb = C.c_int32()
         N.call("wsvd_cache_row_bytes", self.h, C.byref(rb))
         self.row_bytes = rb.value
+        if attention is not None:
+            self.set_attention(attention)
+
+    ATTENTION = {"absorbed": 0, "explicit_tc": 1}
+
+    def set_attention(self, mode: str):
+        """'absorbed' (scores against qt = q . B_K^T) or 'explicit_tc' (the
+        reference's key_j = C_K[j] . B_K rebuilt on tcgen05 tensor cores)."""
+        if mode not in self.ATTENTION:
+            raise ConfigError(f"unknown attention mode '{mode}'")
+        N.call("wsvd_cache_set_attention_mode", self.h, self.ATTENTION[mode])
+
+    @property
+    def attention(self) -> str:
+        m = C.c_int32()
+        N.call("wsvd_cache_attention_mode", self.h, C.byref(m))
+        return {v: k for k, v in self.ATTENTION.items()}[m.value]
 
     def __del__(self):
         if getattr(self, "h", None) and N._lib is not None:

@@ -22,7 +22,9 @@ KEYS = [
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "launch__grid_size", "launch__block_size",
     "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum", "lts__t_sector_hit_rate.pct",
-    "sm__cycles_elapsed.avg",
+    "sm__cycles_elapsed.avg", "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_tensor_subpipe_hmma.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -102,7 +104,7 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(OUT, exist_ok=True)
     summarize_launches(tag)
-    for name in ("step_full", "attn_full", "gemm_full"):
+    for name in ("step_full", "attn_full", "tc_full", "gemm_full"):
         summarize_full(name, tag)
     for f in ("bench.json", "bench_ref.json", "timing.txt", "gpu.txt", "step_trace.txt"):
         src = os.path.join(RAW, f)
