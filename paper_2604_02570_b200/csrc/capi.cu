@@ -250,6 +250,11 @@ struct wsvd_cache_s {
     cudaStream_t gstream = nullptr;
     bool gpending = false;
     GraphKey gkey;
+    // host-buffer step (wsvd_layer_step_host): mapped-pointer cache of the last buffers
+    GraphKey hkey;
+    bool hzc = false;
+    const float* hx = nullptr;
+    float* hy = nullptr;
     ~wsvd_cache_s() {
         if (gexec) cudaGraphExecDestroy(gexec);
         if (graph) cudaGraphDestroy(graph);
@@ -484,7 +489,7 @@ bool fused_step_ok(wsvd_cache_s* c) {
 }
 
 // the whole step as one persistent kernel (step.cu)
-int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s) {
+int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bool x_host = false) {
     wsvd_layer_s* L = c->L;
     int rc = ensure_mqk(L);
     if (rc) return rc;
@@ -494,6 +499,12 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s) {
     StepArgs a{};
     a.x = x;
     a.y = y;
+    a.x_host = x_host ? 1 : 0;
+    if (x_host) {
+        const size_t xb = static_cast<size_t>(c->B) * L->d.embed_dim * 4;
+        if (c->x_dev.n < xb) CUDA_TRY(c->x_dev.alloc(xb));
+        a.xd = c->x_dev.as<float>();
+    }
     a.A = L->A.as<uint8_t>();
     a.P = c->P.as<float>();
     a.mqk = L->mqk.as<float>();
@@ -504,6 +515,8 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s) {
     a.Wo = L->Wo.as<uint8_t>();
     a.d_len = c->d_len();
     a.bar = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 4);
+    a.epoch = c->ctrl.as<int>() + 2;
+    a.xcnt = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 16);
     const size_t xob = step_xo_bytes(c->B, L->oKp);
     if (c->xo.n < xob) CUDA_TRY(c->xo.alloc(xob));  // zeroed: rows past the batch stay 0
     a.xo = c->xo.as<uint8_t>();
@@ -838,7 +851,7 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     const size_t rows = static_cast<size_t>(batch) * nh * c->cap_alloc;
     cudaError_t e = c->data.alloc(rows * c->row_bytes);
     if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4);
-    if (e == cudaSuccess) e = c->ctrl.alloc(64);
+    if (e == cudaSuccess) e = c->ctrl.alloc(256);  // [0] len [1] done [2] step epoch [4,5] barrier [16..32) x-fetch counters
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     if (e == cudaSuccess)
         e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh *
@@ -891,6 +904,7 @@ int wsvd_cache_bind_layer(wsvd_cache_t c, wsvd_layer_t L) {
     }
     c->gpending = false;
     c->gkey = GraphKey{};
+    c->hkey = GraphKey{};
     c->L = L;
     return WSVD_OK;
 }
@@ -1180,17 +1194,50 @@ int wsvd_layer_step_host(wsvd_cache_t c, const float* x_host, float* y_host, voi
     if (!c || !x_host || !y_host) return set_err(WSVD_ECONFIG, "null argument");
     wsvd_layer_s* L = c->L;
     if (!L->Wo.p) return set_err(WSVD_ECONFIG, "layer has no O-projection (wsvd_layer_set_oproj)");
+    int rc = check_layer(L);
+    if (rc) return rc;
+    if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
     CUDA_TRY(cudaSetDevice(L->d.device));
     const size_t xb = static_cast<size_t>(c->B) * L->d.embed_dim * 4;
     const size_t yb = static_cast<size_t>(c->B) * L->e_out * 4;
     if (c->x_dev.n < xb) CUDA_TRY(c->x_dev.alloc(xb));
     if (c->y_dev.n < yb) CUDA_TRY(c->y_dev.alloc(yb));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    CUDA_TRY(cudaMemcpyAsync(c->x_dev.p, x_host, xb, cudaMemcpyHostToDevice, s));
-    int rc = wsvd_layer_step_graph(c, c->x_dev.as<float>(), c->y_dev.as<float>(), stream);
+    // A/B switch: WSVD_HOST_ZEROCOPY=0 moves x / y with the copy engine
+    static const bool no_zc = getenv("WSVD_HOST_ZEROCOPY") && std::string(getenv("WSVD_HOST_ZEROCOPY")) == "0";
+    if (!fused_step_ok(c) || no_zc) {
+        CUDA_TRY(cudaMemcpyAsync(c->x_dev.p, x_host, xb, cudaMemcpyHostToDevice, s));
+        rc = wsvd_layer_step_graph(c, c->x_dev.as<float>(), c->y_dev.as<float>(), stream);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(y_host, c->y_dev.p, yb, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return WSVD_OK;
+    }
+    // fused step with pinned (mapped) host buffers: the kernel itself moves the
+    // bytes -- x is fetched once over the bus by the projection CTAs, y is
+    // written with plain stores from the O-projection epilogue -- so the step
+    // is one launch and one synchronise, with no copy engine round trips
+    if (!(c->hkey.x == x_host && c->hkey.y == y_host)) {
+        cudaPointerAttributes ax{}, ay{};
+        const bool okx = cudaPointerGetAttributes(&ax, x_host) == cudaSuccess;
+        const bool oky = cudaPointerGetAttributes(&ay, y_host) == cudaSuccess;
+        cudaGetLastError();
+        c->hzc = okx && oky && ax.type == cudaMemoryTypeHost && ay.type == cudaMemoryTypeHost && ax.devicePointer &&
+                 ay.devicePointer;
+        c->hx = c->hzc ? static_cast<const float*>(ax.devicePointer) : nullptr;
+        c->hy = c->hzc ? static_cast<float*>(ay.devicePointer) : nullptr;
+        c->hkey = {x_host, y_host, s};
+    }
+    if (c->hzc) {
+        rc = run_step_fused(c, c->hx, c->hy, s, true);
+    } else {  // pageable host memory: copy engine
+        CUDA_TRY(cudaMemcpyAsync(c->x_dev.p, x_host, xb, cudaMemcpyHostToDevice, s));
+        rc = run_step_fused(c, c->x_dev.as<float>(), c->y_dev.as<float>(), s);
+        if (rc == WSVD_OK) CUDA_TRY(cudaMemcpyAsync(y_host, c->y_dev.p, yb, cudaMemcpyDeviceToHost, s));
+    }
     if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(y_host, c->y_dev.p, yb, cudaMemcpyDeviceToHost, s));
     CUDA_TRY(cudaStreamSynchronize(s));
+    c->len += 1;
     return WSVD_OK;
 }
 

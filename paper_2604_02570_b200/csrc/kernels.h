@@ -115,8 +115,12 @@ cudaError_t launch_decode_attn_tc(const AttnArgs& a, cudaStream_t s);  // + laun
 // projection -> append -> attention -> combine -> folded O-projection as one
 // persistent kernel (bf16 weights / cache, rank 32, batch <= 32).
 struct StepArgs {
-    const float* x;        // [B][E] fp32 tokens
-    float* y;              // [B][e_out] fp32 output
+    const float* x;        // [B][E] fp32 tokens (device, or mapped host memory when x_host)
+    int x_host;            // x is pinned host memory: fetched once over the bus into xd
+    float* xd;             // [B][E] device copy of a host x
+    unsigned* xcnt;        // [kMaxSplits] per-K-split fetch counters (monotone)
+    int* epoch;            // fused steps run so far (their generation)
+    float* y;              // [B][e_out] fp32 output (plain stores: device or mapped host memory)
     const uint8_t* A;      // projection W-tiles (bf16, K split 512)
     float* P;              // [splits][B][Nrows] projection partials
     const float* mqk;      // [nh][R][R]

@@ -249,8 +249,11 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     const int phi = pj < cps ? static_cast<int>(static_cast<long>(pj + 1) * ptiles / cps) : 0;
     const int np1 = phi - plo;
     const int osplits = a.oKp / kKS;
-    const int n_oitems = a.otiles * osplits;
-    const int np3 = cta < n_oitems ? (n_oitems - 1 - cta) / G + 1 : 0;  // <= kNA (host-checked)
+    // P3: this CTA owns output tiles cta + i*G with all their K splits (items
+    // (tile, split) in that order), so it sums the splits itself: y is written
+    // with plain stores, once (it may live in mapped host memory)
+    const int nt3 = cta < a.otiles ? (a.otiles - 1 - cta) / G + 1 : 0;
+    const int np3 = nt3 * osplits;  // <= kNA (host-checked)
     int nch, chunk;
     step_chunking(a, len, nch, chunk);
     const int n_units = a.B * a.nh * nch;
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 mbar_arrive_expect_tx(&fullA[slot], kItem);
                 const uint8_t* src = ia < np1
                     ? a.A + (static_cast<size_t>(plo + ia) * splits + ps) * kItem
-                    : a.Wo + static_cast<size_t>(cta + (ia - np1) * G) * kItem;
+                    : a.Wo + (static_cast<size_t>(cta + ((ia - np1) / osplits) * G) * osplits + (ia - np1) % osplits) * kItem;
                 tma_bulk_g2s(ringA + slot * kItem, src, kItem, &fullA[slot]);
                 ++ia;
             };
@@ -306,11 +309,35 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     const int g8 = lane >> 2, t4 = lane & 3;
     // ---- P1 (consumer warps 0..kNA-1): latent projection of this CTA's K split
     if (warp < kNW) {
-        if (np1 > 0) stage_rows<MT>(a.x, a.B, a.E, a.E, ps * kKS, xbuf, tid);
-        if (osplits > 1) {  // P3 accumulates its K splits into y (2 addends: order-free)
-            const int n = a.B * a.e_out;
-            for (int i = cta * 32 * kNW + tid; i < n; i += G * 32 * kNW) a.y[i] = 0.f;
+        const float* xsrc = a.x;
+        if (a.x_host && pj < cps) {
+            // x lives in mapped (pinned) host memory: the cps CTAs of this K
+            // split (with or without projection tiles) each fetch 1/cps of its
+            // [B][kKS] slice over the bus into the device copy xd and publish a
+            // count; all stage from xd once the count is complete (the host
+            // bytes cross the bus once; the weight stream runs meanwhile)
+            const int per = (a.B * kKS / 4 + cps - 1) / cps;  // float4 items per CTA
+            for (int i = pj * per + tid; i < min((pj + 1) * per, a.B * kKS / 4); i += 32 * kNW) {
+                const int m = i / (kKS / 4), k4 = i - m * (kKS / 4);
+                const size_t off = static_cast<size_t>(m) * a.E + ps * kKS + 4 * k4;
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (ps * kKS + 4 * k4 + 4 <= a.E) v = __ldcv(reinterpret_cast<const float4*>(a.x + off));
+                *reinterpret_cast<float4*>(a.xd + off) = v;
+            }
+            named_bar_sync(2, 32 * kNW);
+            if (tid == 0) {
+                const unsigned target = static_cast<unsigned>(cps) * (static_cast<unsigned>(*a.epoch) + 1u);
+                asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.xcnt + ps) : "memory");
+                while (ld_acquire(a.xcnt + ps) < target) {
+                }
+            }
+            named_bar_sync(2, 32 * kNW);
+            xsrc = a.xd;
+        } else if (pj < cps && tid == 0) {
+            // keep the counters' invariant (cps arrivals per fused step) in device mode
+            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.xcnt + ps) : "memory");
         }
+        if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid);
         named_bar_sync(2, 32 * kNW);
         if (warp < kNA) {
             // weight-ring slot s is always consumed by warp s (items k = s mod kNA)
@@ -582,7 +609,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     STEP_MARK(6);
     grid_sync(a.bar);  // every unit state is written; every CTA has read the length
     STEP_MARK(7);
-    if (cta == 0 && tid == 0) *a.d_len = len;
+    if (cta == 0 && tid == 0) {
+        *a.d_len = len;
+        *a.epoch += 1;  // fused steps run (the x-fetch counters' generation)
+    }
 
     // ---- P3: folded O-projection over the prefetched W'_o items
     if (np3 == 0 || warp >= kNW) {
@@ -592,45 +622,48 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     }
     // The X slices this CTA's items use (bf16 rows built by the home units)
     // arrive with one TMA bulk copy each
-    unsigned need = 0;
-    for (int j = 0; j < np3; ++j) need |= 1u << ((cta + j * G) % osplits);
     if (tid == 0) {
         // xo was written by other CTAs' generic stores (ordered by barrier 2);
         // order them before this thread's async-proxy reads
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        uint32_t bytes = 0;
+        mbar_arrive_expect_tx(p3bar, static_cast<uint32_t>(osplits * C::XB));
         for (int s = 0; s < osplits; ++s)
-            if (need & (1u << s)) bytes += C::XB;
-        mbar_arrive_expect_tx(p3bar, bytes);
-        for (int s = 0; s < osplits; ++s)
-            if (need & (1u << s))
-                tma_bulk_g2s(ringB + s * C::XB, a.xo + static_cast<size_t>(s) * C::XB, C::XB, p3bar);
+            tma_bulk_g2s(ringB + s * C::XB, a.xo + static_cast<size_t>(s) * C::XB, C::XB, p3bar);
     }
     mbar_wait(p3bar, 0u);
     named_bar_sync(2, 32 * kNW);
     STEP_MARK(8);
+    // item j = (tile i = j / osplits, split s = j % osplits) -> partial tile in
+    // shared memory, then the splits are summed in split order
+    float* part = reinterpret_cast<float*>(ringB + osplits * C::XB);  // [np3][16 rows][MT*16 tokens]
     for (int j = 0; j < np3; ++j) {
         const int k = np1 + j, slot = k % kNA;
         if (slot != warp) continue;
         mbar_wait(&fullA[slot], static_cast<uint32_t>(k / kNA) & 1u);
-        const int item = cta + j * G;
-        const int tile = item / osplits, s = item - tile * osplits;
+        const int s = j % osplits;
         float facc[MT][2][4];
         item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(ringB + s * C::XB), lane, facc);
+        float* pj = part + j * 16 * MT * 16;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
-                    const int n = tile * 16 + g8 + ((i & 2) ? 8 : 0);
+                    const int n = g8 + ((i & 2) ? 8 : 0);
                     const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
-                    if (m < a.B && n < a.e_out) {
-                        float* dst = a.y + static_cast<size_t>(m) * a.e_out + n;
-                        if (osplits == 1) *dst = facc[mt][hh][i];
-                        else atomicAdd(dst, facc[mt][hh][i]);
-                    }
+                    pj[n * MT * 16 + m] = facc[mt][hh][i];
                 }
+    }
+    named_bar_sync(2, 32 * kNW);
+    for (int i = tid; i < nt3 * 16 * a.B; i += 32 * kNW) {
+        const int ti = i / (16 * a.B), r = i - ti * 16 * a.B;
+        const int m = r / 16, n = r - m * 16;  // n fastest: 64-byte row segments of y
+        const int col = (cta + ti * G) * 16 + n;
+        if (col >= a.e_out) continue;
+        float v = 0.f;
+        for (int s = 0; s < osplits; ++s) v += part[((ti * osplits + s) * 16 + n) * MT * 16 + m];
+        a.y[static_cast<size_t>(m) * a.e_out + col] = v;
     }
     STEP_MARK(9);
 }
@@ -661,13 +694,12 @@ bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp,
     if (osplits > 2 || splits > grid || splits > kMaxSplits) return false;
     if ((max_units + grid - 1) / grid > kMaxU) return false;
     (void)nh;
-    const int n_oitems = otiles * osplits;
-    if ((n_oitems + grid - 1) / grid > kNA) return false;
+    if (((otiles + grid - 1) / grid) * osplits > kNA) return false;
     // P3 stages its X slices in the attention ring
     const int mt = (B + 15) / 16;
     const int ring = (mt == 1 ? SC<32, 1>::NB * SC<32, 1>::STAGE : SC<32, 2>::NB * SC<32, 2>::STAGE);
     (void)max_chunks;
-    return osplits * mt * 16 * kXS <= ring;
+    return osplits * mt * 16 * kXS + kNA * 16 * mt * 16 * 4 <= ring;
 }
 
 int step_item_k() { return kKS; }
