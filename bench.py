@@ -312,6 +312,16 @@ def run_ours(args, cfg_name, cfg):
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
         e2e_ms = float(et.item())
 
+    # ---- the paper's comparison point: dense layer over the full KV cache with
+    # Flash Decoding = torch SDPA, same shape and batch
+    base = None
+    if world == 1 and not args.no_baselines:
+        try:
+            base = flash_decoding_baseline(cfg, B, nh_g, L, dev)
+            base["speedup_of_ours"] = round(base["us_per_layer"] / (ms_step * 1e3), 3)
+        except Exception as e:  # reported, never the target
+            base = {"unavailable": str(e)[:200]}
+
     res = None
     if rank == 0:
         res = {
@@ -358,6 +368,7 @@ def run_ours(args, cfg_name, cfg):
                           "step_algorithmic_bytes": int(step_bytes),
                           "step_frac": round(step_bytes / (ms_step / 1e3) / 1e9 / peak, 4)}),
             "clocks": clocks,
+            "baselines": {"flash_decoding_sdpa": base} if base is not None else {},
             "gpu_launches": K * layer.launches_per_step(),
             "e2e": {"value": round(B / (e2e_ms / 1e3), 1) if e2e_ms else None, "unit": "tokens/s",
                     "ms_per_step": round(e2e_ms, 4) if e2e_ms else None,
@@ -371,6 +382,44 @@ def run_ours(args, cfg_name, cfg):
         dist.barrier()
         dist.destroy_process_group()
     return res
+
+
+def flash_decoding_baseline(cfg, B, nh_g, L, dev, steps=20):
+    """Dense full-rank layer step with SDPA over the full KV cache (library
+    kernels; paper_2604_02570_b200/baselines.py), CUDA-graph replayed, timed
+    with CUDA events at the bench's context length."""
+    import torch
+
+    from paper_2604_02570_b200.baselines import DenseFlashDecodeLayer
+    E, H = cfg["E"], cfg["H"]
+    base = DenseFlashDecodeLayer(E, nh_g, H, B, L + steps + 8, device=dev.index)
+    base.fill(L - 1)
+    x = torch.randn((B, E), device=dev, dtype=torch.bfloat16)
+    y = torch.empty((B, E), device=dev, dtype=torch.bfloat16)
+    fns = [base.step_fn(x, y, L - 1 + i) for i in range(steps)]
+    for fn in fns[:3]:
+        fn()
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        for fn in fns:
+            fn()
+    graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    graph.replay()
+    e1.record()
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / steps
+    out = {"us_per_layer": round(us, 2), "tokens_per_s": round(B / (us / 1e6), 1),
+           "kv_cache_bytes": base.kv_bytes(L), "dtype": "bf16",
+           "kernels": "cuBLAS QKV / O GEMMs + torch.nn.functional.scaled_dot_product_attention over the full KV cache",
+           "source": "PAPER.md:685-690 (Flash Decoding = SDPA, full KV cache)"}
+    del base, graph
+    torch.cuda.empty_cache()
+    return out
 
 
 # ------------------------------------------------------- CPU baselines ----
@@ -453,6 +502,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seqs", type=int, default=2)
+    ap.add_argument("--no-baselines", action="store_true", help="skip the Flash Decoding (SDPA) comparison")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         raise SystemExit("--warmup must be >= 3")
