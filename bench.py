@@ -46,6 +46,12 @@ CONFIGS = {
     "13b-r48-b64-ctx8k-w4a8-i8cache": dict(E=5120, nh=40, H=128, r=48, B=64, L=8192, cache="i8",
                                            weights="i4"),
 }
+# config 5: the 32-layer stack; every GPU holds one 8-way head shard (4 heads),
+# N GPUs run N of the 8 shards with the O-projection all-reduce among them
+STACK_CONFIGS = {
+    "7b-stack32-r32-b128-ctx32k-bf16": dict(E=4096, nh=32, H=128, r=32, B=128, L=32768, cache="bf16",
+                                            weights="bf16", layers=32, shard_of=8),
+}
 DEFAULT_CONFIG = "7b-r32-b16-ctx4k-bf16"
 METRIC = "WSVD decode attn µs/layer & tokens/s (LLaVA-7B shape, ctx 4K); % HBM roofline"
 
@@ -422,6 +428,114 @@ def flash_decoding_baseline(cfg, B, nh_g, L, dev, steps=20):
     return out
 
 
+# ------------------------------------------------------- config 5 stack ---
+def run_stack(args, cfg_name, cfg):
+    """pipe::decode_factored (pipeline.cpp:304-339) over `layers` WSVD layers +
+    the toy FFN, one token for every sequence per step, the whole stack step
+    replayed as one CUDA graph.  Caches are filled with synthetic latents
+    (wsvd_cache_fill_synthetic; a 32K-token prompt through the projection
+    is not part of the decode step being measured)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_02570_b200 import _native as N
+    from paper_2604_02570_b200.layer import DecodeLayer
+    from paper_2604_02570_b200.sharding import NcclComm
+    from paper_2604_02570_b200.stack import DecodeStack
+
+    world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    N.lib()
+    E, H, B, L, nl = cfg["E"], cfg["H"], cfg["B"], cfg["L"], cfg["layers"]
+    shard_of = cfg["shard_of"]
+    nh_g = cfg["nh"] // shard_of
+    sub = dict(cfg, nh=nh_g)
+    W, K = args.warmup, args.steps
+    cap = L + W + K + 8
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    layers = []
+    for li in range(nl):
+        f, w_o = synthetic_layer(sub, seed=args.seed * 1000 + rank * 100 + li)
+        lay = DecodeLayer(f, w_o, batch=B, capacity=cap, cache_dtype=cfg["cache"], weight_dtype=cfg["weights"],
+                          oproj_dtype="bf16", device=local, head_offset=rank * nh_g)
+        lay.fill_synthetic(L - 1 - W, seed=li + 1)
+        layers.append(lay)
+    comm = NcclComm(world, rank, local) if world > 1 else None
+    stack = DecodeStack(layers, comm=comm, seed=args.seed)
+    log(f"[rank {rank}] stack setup {time.time() - t0:.1f}s")
+    x = torch.randn((B, E), device=dev)
+    y = torch.empty((B, E), device=dev)
+    for _ in range(W):  # warm-up (sizes every workspace) -- outside any graph
+        stack.step(x, y)
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=side):
+        stack.step(x, y)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+    ev0.record(stream)
+    for _ in range(K):
+        graph.replay()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = sampler.stop()
+    ms_t = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_step = float(ms_t.item()) / K
+    for lay in layers:
+        lay.sync_length()
+    L_end = layers[0].length()
+    _, lbytes = algorithmic_bytes(sub, B, nh_g, L_end - K // 2)
+    step_bytes = nl * lbytes + stack.ffn_bytes()
+    peak, peak_kind = measured_peak()
+    achieved = step_bytes / (ms_step / 1e3) / 1e9
+    res = None
+    if rank == 0:
+        res = {
+            "metric": METRIC, "value": round(B / (ms_step / 1e3), 1), "unit": "tokens/s", "n_gpus": world,
+            "steps": K, "warmup": W, "ms_per_step": round(ms_step, 4),
+            "us_per_layer": round(ms_step * 1e3 / nl, 2), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16 storage / fp32 accumulate",
+            "data": "synthetic (random-init factors and FFN; synthetic N(0,1) latent caches)",
+            "config": {"workload": cfg_name, "layers": nl, "embed_dim": E, "heads": cfg["nh"],
+                       "heads_per_gpu": nh_g, "head_dim": H, "rank": cfg["r"], "global_batch": B,
+                       "ctx": L_end - K // 2, "ffn": f"toy tanh FFN 2E, bf16 cuBLAS, replicated",
+                       "parallelism": f"heads/{shard_of} (each GPU one {shard_of}-way head shard; {world} of "
+                                      f"the {shard_of} shards run)",
+                       "l2": f"inputs larger than L2: {nl * lbytes / 1e9:.1f} GB of latent caches per GPU",
+                       "launch": "whole 32-layer step captured as one CUDA graph"},
+            "roofline": {"bound": "hbm", "kernel": "whole stack step (all kernels)", "achieved": round(achieved, 1),
+                         "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": None, "algorithmic_bytes": int(step_bytes)},
+            "clocks": clocks,
+            "gpu_launches": K * nl * layers[0].launches_per_step(),
+            "e2e": {"value": None, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "note": "config-5 line: device-resident stack step only"},
+        }
+    del graph, stack, layers
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return res
+
+
 # ------------------------------------------------------- CPU baselines ----
 def cpu_threads():
     try:
@@ -496,7 +610,7 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS) + sorted(STACK_CONFIGS))
     ap.add_argument("--soak-ms", type=float, default=1500.0,
                     help="untimed attention load before the timed region while clocks are sampled")
     ap.add_argument("--seed", type=int, default=0)
@@ -506,6 +620,15 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         raise SystemExit("--warmup must be >= 3")
+    if args.config in STACK_CONFIGS:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config-5 stack line: the reference arm is "
+                              "measured on the single-layer headline workload"}), flush=True)
+            return
+        res = run_stack(args, args.config, STACK_CONFIGS[args.config])
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
     cfg = CONFIGS[args.config]
 
     if args.impl == "reference":

@@ -135,6 +135,14 @@ int wsvd_cache_reset(wsvd_cache_t cache);
  * head count, padded rank, E or H differ (decode.cpp:159-162). */
 int wsvd_cache_bind_layer(wsvd_cache_t cache, wsvd_layer_t layer);
 int wsvd_cache_length(wsvd_cache_t cache, int32_t* len);
+/* Re-reads the committed length from the device into the host mirror (after
+ * steps replayed inside a caller's CUDA graph, which the host does not see). */
+int wsvd_cache_sync_length(wsvd_cache_t cache, int32_t* len);
+/* Benchmark utility: rows 0..length-1 of every (sequence, head) become
+ * synthetic N(0, scale^2) latents in the cache format (no projection), and the
+ * cache length becomes `length` -- the reference's decode-bench prefill of
+ * random latents (wsvd_main.cpp:393-396) without the per-token projection. */
+int wsvd_cache_fill_synthetic(wsvd_cache_t cache, int32_t length, uint64_t seed, float scale);
 /* LatentCache::push + bump_length for every sequence and head at once:
  * ck / cv host fp64 [batch][n_heads][rpad] (entries beyond a head's rank are
  * ignored and stored as 0). */

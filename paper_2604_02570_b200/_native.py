@@ -49,6 +49,8 @@ SIGNATURES = {
     "wsvd_cache_read_host": (C.c_int, [_vp, _i32, _i32, _dp, _dp]),
     "wsvd_cache_row_bytes": (C.c_int, [_vp, _i32p]),
     "wsvd_cache_step_info": (C.c_int, [_vp, _i32p, _i32p]),
+    "wsvd_cache_sync_length": (C.c_int, [_vp, _i32p]),
+    "wsvd_cache_fill_synthetic": (C.c_int, [_vp, _i32, C.c_uint64, C.c_float]),
     "wsvd_cache_set_attention_mode": (C.c_int, [_vp, _i32]),
     "wsvd_cache_attention_mode": (C.c_int, [_vp, _i32p]),
     "wsvd_cache_read_raw": (C.c_int, [_vp, _i32, _i32, _vp, _vp]),

@@ -238,7 +238,70 @@ __global__ void __launch_bounds__(kEpThreads) absorb_query_kernel(const float* _
     absorb(qs, R, H, bk, bk_scale, bdtype, h, scale, qt + o * R);
 }
 
+// Synthetic latent rows for benchmarks (no prompt to prefill through the
+// projection): row t of region r gets N(0, scale^2)-distributed values from a
+// counter-based hash (Box-Muller), written in the cache format and swizzle.
+WSVD_DEV uint32_t mix32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x;
+}
+
+__global__ void fill_synthetic_kernel(uint8_t* cache, __half2* cscale, int regions, int cap, int length, int R,
+                                      int cdtype, int row_bytes, uint32_t seed, float scale) {
+    const size_t n = static_cast<size_t>(regions) * length;
+    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int reg = static_cast<int>(i / length), t = static_cast<int>(i - static_cast<size_t>(reg) * length);
+        uint8_t* region = cache + static_cast<size_t>(reg) * cap * row_bytes;
+        const uint32_t row0 = static_cast<uint32_t>(t) * row_bytes;
+        const uint32_t base = mix32(seed ^ mix32(static_cast<uint32_t>(i) * 0x9e3779b9u));
+        float v[128];
+        for (int e = 0; e < 2 * R; e += 2) {
+            const uint32_t h1 = mix32(base + 2u * e + 1u), h2 = mix32(base + 2u * e + 2u);
+            const float u1 = (static_cast<float>(h1 >> 8) + 0.5f) * (1.0f / 16777216.0f);
+            const float u2 = static_cast<float>(h2 >> 8) * (1.0f / 16777216.0f);
+            const float rad = sqrtf(-2.f * logf(u1)) * scale;
+            float sn, cs;
+            sincospif(2.f * u2, &sn, &cs);
+            v[e] = rad * cs;
+            v[e + 1] = rad * sn;
+        }
+        if (cdtype == BF16) {
+            for (int e = 0; e < 2 * R; ++e)
+                *reinterpret_cast<__nv_bfloat16*>(region + cache_swz(row0 + 2 * e)) = __float2bfloat16_rn(v[e]);
+        } else if (cdtype == F32) {
+            for (int e = 0; e < 2 * R; ++e) *reinterpret_cast<float*>(region + cache_swz(row0 + 4 * e)) = v[e];
+        } else {
+            for (int half = 0; half < 2; ++half) {
+                float mx = 0.f;
+                for (int e = 0; e < R; ++e) mx = fmaxf(mx, fabsf(v[half * R + e]));
+                __half hs = __float2half_rn(__fdiv_rn(mx, 127.f));
+                float sc = __half2float(hs);
+                if (sc == 0.f) {
+                    hs = __float2half_rn(1.f);
+                    sc = 1.f;
+                }
+                for (int e = 0; e < R; ++e)
+                    reinterpret_cast<int8_t*>(region)[cache_swz(row0 + half * R + e)] =
+                        static_cast<int8_t>(fminf(fmaxf(roundf(__fdiv_rn(v[half * R + e], sc)), -127.f), 127.f));
+                reinterpret_cast<__half*>(cscale + static_cast<size_t>(reg) * cap + t)[half] = hs;
+            }
+        }
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_fill_synthetic(uint8_t* cache, __half2* cscale, int regions, int cap, int length, int R,
+                                  int cdtype, int row_bytes, uint32_t seed, float scale, cudaStream_t s) {
+    if (2 * R > 128) return cudaErrorInvalidValue;
+    fill_synthetic_kernel<<<1184, 256, 0, s>>>(cache, cscale, regions, cap, length, R, cdtype, row_bytes, seed, scale);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_act_quant(const float* x, int M, int E, int Kp, int rot, int rot_blk,
                              float rot_scale, int8_t* xq, float* sx, cudaStream_t s) {

@@ -915,6 +915,33 @@ int wsvd_cache_length(wsvd_cache_t c, int32_t* len) {
     return WSVD_OK;
 }
 
+int wsvd_cache_sync_length(wsvd_cache_t c, int32_t* len) {
+    if (!c) return set_err(WSVD_ECONFIG, "null cache");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    int32_t d = 0;
+    CUDA_TRY(cudaMemcpy(&d, c->d_len(), 4, cudaMemcpyDeviceToHost));
+    if (d < 0 || d > c->cap) return set_err(WSVD_ESHAPE, "device length out of range");
+    c->len = d;
+    if (len) *len = d;
+    return WSVD_OK;
+}
+
+int wsvd_cache_fill_synthetic(wsvd_cache_t c, int32_t length, uint64_t seed, float scale) {
+    if (!c) return set_err(WSVD_ECONFIG, "null cache");
+    if (length < 0 || length > c->cap) return set_err(WSVD_ESHAPE, "synthetic length exceeds the capacity");
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    const int regions = c->B * c->L->d.n_heads;
+    if (length > 0)
+        CUDA_TRY(launch_fill_synthetic(c->data.as<uint8_t>(), c->scales.as<__half2>(), regions, c->cap_alloc, length,
+                                       c->L->R, c->cdtype, c->row_bytes, static_cast<uint32_t>(seed ^ (seed >> 32)),
+                                       scale, nullptr));
+    CUDA_TRY(cudaMemcpy(c->d_len(), &length, 4, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaDeviceSynchronize());
+    c->len = length;
+    return WSVD_OK;
+}
+
 int wsvd_cache_set_attention_mode(wsvd_cache_t c, int32_t mode) {
     if (!c) return set_err(WSVD_ECONFIG, "null cache");
     if (mode == WSVD_ATTN_ABSORBED) {

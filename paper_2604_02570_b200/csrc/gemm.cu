@@ -168,6 +168,12 @@ __global__ void __launch_bounds__(kStreamThreads, 1) skinny_stream_kernel(const 
     const int splits = a.Kp / KS;
     const int cps = gridDim.x / splits;  // CTAs per split
     const int s = blockIdx.x % splits, j = blockIdx.x / splits;
+    // the layer step's length commit, before any early exit (CTA 0 may own no
+    // tile when N/16 < the grid); after the predecessor, which read the length
+    if (a.commit_len && blockIdx.x == 0 && threadIdx.x == 0) {
+        griddep_wait();
+        atomicAdd(a.commit_len, 1);
+    }
     if (j >= cps) return;
     const int tiles = (a.N + 15) / 16;
     const int lo = static_cast<int>(static_cast<long>(j) * tiles / cps);
@@ -205,7 +211,6 @@ __global__ void __launch_bounds__(kStreamThreads, 1) skinny_stream_kernel(const 
     // token slice, the partial outputs and the length commit do
     griddep_wait();
     griddep_launch_dependents();
-    if (a.commit_len && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.commit_len, 1);
     stage_x<WT>(a, xbuf, s * KS, S::XROWS);
     named_bar_sync(1, 32 * kStreamConsumers);
 

@@ -69,6 +69,10 @@ struct AppendArgs {
 };
 cudaError_t launch_append_epilogue(const AppendArgs& a, cudaStream_t s);
 
+// synthetic N(0, scale^2) latent rows 0..length-1 of every region (benchmarks)
+cudaError_t launch_fill_synthetic(uint8_t* cache, __half2* cscale, int regions, int cap, int length, int R,
+                                  int cdtype, int row_bytes, uint32_t seed, float scale, cudaStream_t s);
+
 // host-provided rows [n][row_bytes] -> row `pos` of cache regions 0..n-1 (swizzled)
 cudaError_t launch_push_rows(const uint8_t* rows, int n, uint8_t* cache, int cap, int row_bytes,
                              int pos, cudaStream_t s);

@@ -121,6 +121,16 @@ class DecodeLayer:
                    self._ptr(attn_out) if attn_out is not None else None, self._ptr(y),
                    self._stream(stream))
 
+    def fill_synthetic(self, length: int, seed: int = 0, scale: float = 1.0):
+        """Benchmark prefill: synthetic N(0, scale^2) latent rows, length rows."""
+        N.call("wsvd_cache_fill_synthetic", self.h, int(length), int(seed), float(scale))
+
+    def sync_length(self) -> int:
+        """Host mirror of the length after steps replayed in a caller's graph."""
+        n = C.c_int32()
+        N.call("wsvd_cache_sync_length", self.h, C.byref(n))
+        return n.value
+
     def _step_info(self):
         fused, launches = C.c_int32(0), C.c_int32(0)
         N.call("wsvd_cache_step_info", self.h, C.byref(fused), C.byref(launches))
