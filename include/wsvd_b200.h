@@ -166,6 +166,29 @@ int wsvd_cache_row_bytes(wsvd_cache_t cache, int32_t* row_bytes);
 int wsvd_cache_set_attention_mode(wsvd_cache_t cache, int32_t mode);
 int wsvd_cache_attention_mode(wsvd_cache_t cache, int32_t* mode);
 
+/* ---- checkpoints of the reference (wsvd::ckpt, src/checkpoint.cpp:168-333):
+ * manifest.json + WSVDMAT1 fp64 / WSVDI8T1 int8 tensor files.  Host-only
+ * readers (no device needed) and a device-layer loader.  IO and format
+ * errors return WSVD_EIO (the reference's IoError). */
+/* info = {embed_dim, head_dim, n_heads, n_layers, weight_bits, activation_bits,
+ *         has_factors, has_quantized} */
+int wsvd_ckpt_info(const char* dir, int64_t info[8]);
+/* fp64 factors of (layer, head, role): a [E][rank], b [rank][H]; null buffers
+ * only return the rank */
+int wsvd_ckpt_head(const char* dir, int32_t layer, int32_t head, int32_t role, int32_t* rank, double* a, double* b);
+/* quantised factors Q(S1 A S2^T) [E][rank], Q(S2 B) [rank][H] and their
+ * per-column scales (quant.cpp:344-358) */
+int wsvd_ckpt_head_quantized(const char* dir, int32_t layer, int32_t head, int32_t role, int32_t* rank,
+                             int8_t* a_q, double* a_scales, int8_t* b_q, double* b_scales);
+/* a dense weight by manifest name (e.g. "layer0.w_o"); *rows x *cols must hold
+ * it when out is non-null */
+int wsvd_ckpt_weight(const char* dir, const char* name, int64_t* rows, int64_t* cols, double* out);
+/* device layer of heads [head_begin, head_end) of `layer`: quantised factors
+ * for WSVD_I8 / WSVD_I4 (act_rotation on), fp64 factors otherwise; with
+ * oproj_dtype >= 0 also the W_o rows of those heads (wsvd_layer_set_oproj) */
+int wsvd_layer_load_checkpoint(const char* dir, int32_t layer, int32_t head_begin, int32_t head_end,
+                               int32_t weight_dtype, int32_t oproj_dtype, int32_t device, wsvd_layer_t* out);
+
 /* How wsvd_layer_step(_graph/_host) runs for this cache: *fused = 1 when the
  * whole step is the single persistent kernel of step.cu (bf16, rank 32,
  * batch <= 32), 0 for the multi-kernel path; *launches = kernels per step. */

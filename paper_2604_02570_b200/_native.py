@@ -50,6 +50,11 @@ SIGNATURES = {
     "wsvd_cache_row_bytes": (C.c_int, [_vp, _i32p]),
     "wsvd_cache_step_info": (C.c_int, [_vp, _i32p, _i32p]),
     "wsvd_cache_sync_length": (C.c_int, [_vp, _i32p]),
+    "wsvd_ckpt_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_int64)]),
+    "wsvd_ckpt_head": (C.c_int, [C.c_char_p, _i32, _i32, _i32, _i32p, _dp, _dp]),
+    "wsvd_ckpt_head_quantized": (C.c_int, [C.c_char_p, _i32, _i32, _i32, _i32p, _i8p, _dp, _i8p, _dp]),
+    "wsvd_ckpt_weight": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64), _dp]),
+    "wsvd_layer_load_checkpoint": (C.c_int, [C.c_char_p, _i32, _i32, _i32, _i32, _i32, _i32, C.POINTER(_vp)]),
     "wsvd_cache_fill_synthetic": (C.c_int, [_vp, _i32, C.c_uint64, C.c_float]),
     "wsvd_cache_set_attention_mode": (C.c_int, [_vp, _i32]),
     "wsvd_cache_attention_mode": (C.c_int, [_vp, _i32p]),

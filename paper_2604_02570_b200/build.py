@@ -30,7 +30,7 @@ CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall", "-Wextra", f"-I{os.path.join
              "-I/usr/local/cuda/include"]
 
 CU_SOURCES = ["attn.cu", "attn_tc.cu", "gemm.cu", "append.cu", "step.cu", "capi.cu"]
-CXX_SOURCES = ["host_decode.cpp"]
+CXX_SOURCES = ["host_decode.cpp", "checkpoint.cpp"]
 
 
 def _stale(src: str, obj: str, deps: list[str]) -> bool:

@@ -562,6 +562,9 @@ extern "C" {
 const char* wsvd_last_error(void) { return g_err.c_str(); }
 int wsvd_abi_version(void) { return WSVD_ABI_VERSION; }
 
+// error slot shared with the checkpoint reader (checkpoint.cpp); not in the header
+void wsvd_internal_set_error(const char* msg) { g_err = msg ? msg : ""; }
+
 int wsvd_device_count(int32_t* n) {
     if (!n) return set_err(WSVD_ECONFIG, "null output");
     *n = sm100_devices();

@@ -192,6 +192,26 @@ class DeviceLayer:
         N.call("wsvd_layer_rank_pad", self.h, C.byref(rp))
         self.rpad = rp.value
 
+    @classmethod
+    def adopt(cls, handle, f: "LayerFactors", weight_dtype: str, device: int, e_out: int | None = None):
+        """Wrap a wsvd_layer_t built by the library itself (e.g.
+        wsvd_layer_load_checkpoint); f supplies the geometry."""
+        self = cls.__new__(cls)
+        self.f = f
+        self.weight_dtype = weight_dtype
+        self.device = device
+        self.n_heads = len(f.heads)
+        self.embed_dim = f.embed_dim
+        self.head_dim = f.head_dim
+        self.ranks = f.ranks()
+        self.h = handle
+        rp = C.c_int32()
+        N.call("wsvd_layer_rank_pad", self.h, C.byref(rp))
+        self.rpad = rp.value
+        if e_out is not None:
+            self.e_out = e_out
+        return self
+
     def set_oproj(self, w_o_rows: np.ndarray, dtype: str = "bf16"):
         """pipeline.cpp:329: rows of W_o multiplying this layer's heads."""
         w = np.ascontiguousarray(w_o_rows, dtype=np.float64)

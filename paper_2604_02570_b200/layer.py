@@ -28,14 +28,17 @@ class DecodeLayer:
     def __init__(self, f: LayerFactors, w_o_rows: np.ndarray | None, batch: int, capacity: int,
                  cache_dtype: str = "bf16", weight_dtype: str = "bf16", oproj_dtype: str = "bf16",
                  device: int = 0, head_offset: int = 0, act_rotation: bool | None = None,
-                 quantized=None, attention: str | None = None):
+                 quantized=None, attention: str | None = None, device_layer=None):
         if cache_dtype not in ("f32", "bf16", "i8"):
             raise ConfigError(f"unknown cache dtype '{cache_dtype}'")
         self.device = device
         self.batch = batch
-        self.layer = DeviceLayer(f, weight_dtype, device, act_rotation=act_rotation,
-                                 head_offset=head_offset, quantized=quantized)
-        self.e_out = None
+        if device_layer is not None:  # built by the library (e.g. from a checkpoint)
+            self.layer = device_layer
+        else:
+            self.layer = DeviceLayer(f, weight_dtype, device, act_rotation=act_rotation,
+                                     head_offset=head_offset, quantized=quantized)
+        self.e_out = getattr(self.layer, "e_out", None)
         if w_o_rows is not None:
             self.layer.set_oproj(w_o_rows, oproj_dtype)
             self.e_out = self.layer.e_out
