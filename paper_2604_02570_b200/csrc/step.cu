@@ -96,23 +96,19 @@ WSVD_DEV unsigned ld_acquire(const unsigned* p) {
     return v;
 }
 
-// Grid-wide barrier among the consumer warps of every CTA (all CTAs are
-// resident: one per SM).  bar[0] counts arrivals, bar[1] is the generation;
-// the last arriver resets the count before releasing the others.
-WSVD_DEV void grid_sync(unsigned* bar) {
+// Grid-wide barrier among the consumer and helper warps of every CTA (all
+// CTAs are resident: one per SM).  bar[0] is a monotone arrival count: the
+// k-th barrier of the n-th fused step completes when it reaches
+// (2n + k) * gridDim.x.  Arrival is a fire-and-forget release reduction and
+// everyone polls with acquire loads -- one round trip, 1.2 us on B200
+// against 2.0 us for a count-and-release barrier (tools/micro_barrier.cu).
+WSVD_DEV void grid_sync(unsigned* bar, unsigned target) {
     named_bar_sync(1, kSync);
     if (threadIdx.x == 0) {
-        const unsigned g0 = ld_acquire(bar + 1);
-        unsigned old;
         // release: the CTA's writes (ordered before by bar.sync) become visible
-        // to whoever acquires the generation bump
-        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
-        if (old == gridDim.x - 1) {
-            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
-            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
-        } else {
-            while (ld_acquire(bar + 1) == g0) {
-            }
+        // to every CTA that acquires the count
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        while (ld_acquire(bar) < target) {
         }
     }
     named_bar_sync(1, kSync);
@@ -240,6 +236,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     STEP_MARK(1);
 
     const int pos = *a.d_len;  // the new token's row; attention covers pos + 1 rows
+    const unsigned epoch = static_cast<unsigned>(*a.epoch);  // fused steps so far (barrier generations)
     const int len = pos + 1;
     const int splits = a.Kp / kKS;
     const int cps = G / splits;  // CTAs per projection split
@@ -326,7 +323,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
             }
             named_bar_sync(2, 32 * kNW);
             if (tid == 0) {
-                const unsigned target = static_cast<unsigned>(cps) * (static_cast<unsigned>(*a.epoch) + 1u);
+                const unsigned target = static_cast<unsigned>(cps) * (epoch + 1u);
                 asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.xcnt + ps) : "memory");
                 while (ld_acquire(a.xcnt + ps) < target) {
                 }
@@ -363,8 +360,17 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
             }
         }
     }
+    // helper: the first unit's M_QK column does not depend on the projection;
+    // load it while the barrier drains (one L2 round trip off the critical path)
+    float mq0[R];
+    if (warp == kNW + 1 && nu > 0) {
+        const int h0 = ((cta / nch) % a.nh);
+        const float* mq = a.mqk + static_cast<size_t>(h0) * R * R + lane;
+#pragma unroll
+        for (int jj = 0; jj < R; ++jj) mq0[jj] = __ldg(mq + jj * R);
+    }
     STEP_MARK(2);
-    grid_sync(a.bar);  // consumers + helper
+    grid_sync(a.bar, (2u * epoch + 1u) * G);  // consumers + helper
     STEP_MARK(3);
 
     if (warp == kNW + 1) {
@@ -373,7 +379,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         //     the append epilogue's order (fixed split order, sequential fma);
         //     for the unit holding the new token, its latent row [c_K | c_V] ->
         //     cache and shared memory (the stage is patched by its owner warp)
-        for (int j = 0; j < nu; ++j) {
+        auto prep = [&](int j, const float (&mqv)[R]) {
             const int u = cta + j * G;
             const int bh = u / nch, ck = u - bh * nch;
             const int b = bh / a.nh, h = bh - b * a.nh;
@@ -386,10 +392,6 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 pv[1][s] = (has_new && s < splits) ? __ldcg(pb + s * pstride + R) : 0.f;
                 pv[2][s] = (has_new && s < splits) ? __ldcg(pb + s * pstride + 2 * R) : 0.f;
             }
-            float mqv[R];
-            const float* mq = a.mqk + static_cast<size_t>(h) * R * R + lane;
-#pragma unroll
-            for (int jj = 0; jj < R; ++jj) mqv[jj] = __ldg(mq + jj * R);
             float v[3] = {0.f, 0.f, 0.f};
 #pragma unroll
             for (int s = 0; s < kMaxSplits; ++s)
@@ -411,6 +413,15 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&uready[j]);
+        };
+        if (nu > 0) prep(0, mq0);
+        for (int j = 1; j < nu; ++j) {
+            const int h = ((cta + j * G) / nch) % a.nh;
+            float mqv[R];
+            const float* mq = a.mqk + static_cast<size_t>(h) * R * R + lane;
+#pragma unroll
+            for (int jj = 0; jj < R; ++jj) mqv[jj] = __ldg(mq + jj * R);
+            prep(j, mqv);
         }
         // (b) per unit as the consumers finish it: merge the kNW warp states in
         //     warp order.  A unit that is not the last chunk of its (sequence,
@@ -607,7 +618,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         STEP_MARK(5);
     }
     STEP_MARK(6);
-    grid_sync(a.bar);  // every unit state is written; every CTA has read the length
+    grid_sync(a.bar, (2u * epoch + 2u) * G);  // every unit state is written; every CTA has read the length
     STEP_MARK(7);
     if (cta == 0 && tid == 0) {
         *a.d_len = len;
