@@ -14,6 +14,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 using namespace wsvd_dev;
 
 namespace wsvd_k {
@@ -67,6 +69,95 @@ __global__ void __launch_bounds__(kAqThreads) act_quant_kernel(const float* __re
         q[i] = static_cast<int8_t>(r);
     }
     if (threadIdx.x == 0) sx[m] = s;
+}
+
+// Fast variant (E % 512 == 0): thread t owns elements [16t, 16t + 16).  The
+// FWHT stages with len < 16 run in registers, len 16..256 through warp
+// shuffles (partner lane t ^ len/16), longer ones through shared memory; every
+// butterfly is the same fp32 (a + b, a - b) as the oracle's
+// (orc_fwht_f32), so the rotated token -- and everything after it -- is
+// bit-identical to the one-pass kernel above.
+__global__ void __launch_bounds__(512) act_quant_fast_kernel(const float* __restrict__ x, int E, int Kp, int rot,
+                                                             int rot_blk, float rot_scale, int8_t* __restrict__ xq,
+                                                             float* __restrict__ sx) {
+    extern __shared__ float sv[];  // [E] for the cross-warp stages
+    __shared__ float wmax[16];
+    const int m = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int nw = blockDim.x >> 5;
+    griddep_wait();
+    griddep_launch_dependents();
+    const float4* xm = reinterpret_cast<const float4*>(x + static_cast<size_t>(m) * E) + 4 * t;
+    float v[16];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float4 q = __ldg(xm + i);
+        v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+    }
+    if (rot) {
+#pragma unroll
+        for (int len = 1; len < 16; len <<= 1) {
+            if (len >= rot_blk) break;
+#pragma unroll
+            for (int i = 0; i < 16; i += 2 * len)
+#pragma unroll
+                for (int j = i; j < i + len; ++j) {
+                    const float a = v[j], b = v[j + len];
+                    v[j] = __fadd_rn(a, b);
+                    v[j + len] = __fsub_rn(a, b);
+                }
+        }
+        for (int len = 16; len < rot_blk && len < 512; len <<= 1) {
+            const int mk = len >> 4;  // partner thread t ^ mk holds elements +- len
+            const bool upper = (t & mk) != 0;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float o = __shfl_xor_sync(0xffffffffu, v[j], mk);
+                v[j] = upper ? __fsub_rn(o, v[j]) : __fadd_rn(v[j], o);
+            }
+        }
+        if (rot_blk > 512) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sv[16 * t + j] = v[j];
+            for (int len = 512; len < rot_blk; len <<= 1) {
+                __syncthreads();
+                for (int p = t; p < E / 2; p += blockDim.x) {
+                    const int lo = ((p & ~(len - 1)) << 1) | (p & (len - 1));
+                    const float a = sv[lo], b = sv[lo + len];
+                    sv[lo] = __fadd_rn(a, b);
+                    sv[lo + len] = __fsub_rn(a, b);
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = sv[16 * t + j];
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __fmul_rn(v[j], rot_scale);
+    }
+    float mx = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) mx = fmaxf(mx, fabsf(v[j]));
+    mx = warp_max(mx);
+    if (lane == 0) wmax[warp] = mx;
+    __syncthreads();
+    mx = 0.f;
+    for (int w = 0; w < nw; ++w) mx = fmaxf(mx, wmax[w]);
+    const float s = (mx == 0.f) ? 1.f : __fdiv_rn(mx, 127.f);
+    uint32_t packed[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const float r = fminf(fmaxf(roundf(__fdiv_rn(v[4 * i + k], s)), -127.f), 127.f);
+            w |= (static_cast<uint32_t>(static_cast<int32_t>(r)) & 0xffu) << (8 * k);
+        }
+        packed[i] = w;
+    }
+    int8_t* q = xq + static_cast<size_t>(m) * Kp;
+    *reinterpret_cast<uint4*>(q + 16 * t) = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+    for (int i = E + t; i < Kp; i += blockDim.x) q[i] = 0;
+    if (t == 0) sx[m] = s;
 }
 
 // ------------------------------------------------------ factor access --
@@ -305,6 +396,18 @@ cudaError_t launch_fill_synthetic(uint8_t* cache, __half2* cscale, int regions, 
 
 cudaError_t launch_act_quant(const float* x, int M, int E, int Kp, int rot, int rot_blk,
                              float rot_scale, int8_t* xq, float* sx, cudaStream_t s) {
+    static const bool slow = std::getenv("WSVD_ACT_QUANT_SLOW") != nullptr;  // A/B and parity switch
+    if (!slow && E % 512 == 0 && E / 16 <= 512 && (Kp % 16) == 0) {
+        const int smem = (rot && rot_blk > 512) ? E * 4 : 0;
+        static int attr = 0;
+        if (smem > attr) {
+            cudaError_t e = cudaFuncSetAttribute(act_quant_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (e != cudaSuccess) return e;
+            attr = smem;
+        }
+        return launch_pdl(act_quant_fast_kernel, dim3(M), dim3(E / 16), smem, s, x, E, Kp, rot, rot_blk, rot_scale,
+                          xq, sx);
+    }
     const int smem = E * 4;
     static int attr_smem = 0;
     if (smem > attr_smem) {

@@ -533,7 +533,7 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bo
     a.max_chunks = c->chunk > 0 ? c->max_chunks : c->fmax_chunks;
     a.grid = c->sms;
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
-    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 10 * 8));
+    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 12 * 8));
     a.trace = trace ? c->trace.as<uint64_t>() : nullptr;
     CUDA_TRY(launch_layer_step(a, s));
     c->P_M = c->B;

@@ -88,7 +88,7 @@ WSVD_DEV uint64_t gtimer() {
     return t;
 }
 #define STEP_MARK(k) \
-    do { if (a.trace && tid == 0) a.trace[cta * 10 + (k)] = gtimer(); } while (0)
+    do { if (a.trace && tid == 0) a.trace[cta * 12 + (k)] = gtimer(); } while (0)
 
 WSVD_DEV unsigned ld_acquire(const unsigned* p) {
     unsigned v;
@@ -209,6 +209,11 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     const int G = gridDim.x, cta = blockIdx.x;
 
     STEP_MARK(0);
+    if (a.trace && tid == 0) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        a.trace[cta * 12 + 10] = smid;
+    }
     // prologue (overlaps the predecessor under PDL): rows past a stage's valid
     // end are read by the MMAs (times p = 0) and must be finite
     for (int i = tid; i < C::NB * C::STAGE / 16; i += kThr)
@@ -255,6 +260,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     step_chunking(a, len, nch, chunk);
     const int n_units = a.B * a.nh * nch;
     const int nu = cta < n_units ? (n_units - 1 - cta) / G + 1 : 0;  // this CTA's units u = cta + j*G
+    if (a.trace && tid == 0) a.trace[cta * 12 + 11] = static_cast<uint64_t>(nu);
     const size_t cap = static_cast<size_t>(a.cap);
     const size_t pstride = static_cast<size_t>(a.B) * a.Nrows;
 

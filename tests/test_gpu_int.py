@@ -49,6 +49,7 @@ def quant_layer(lay, bits):
     (512, 4, 32, 128, 3, 70, 8),     # W8A8, power-of-two S1
     (640, 2, 48, 128, 2, 40, 4),     # W4A8, block-Hadamard S1 (5 x H_128), rank 48
     (4096, 32, 32, 128, 4, 24, 8),   # config-3 shape (fewer sequences / tokens)
+    (5120, 2, 48, 128, 2, 12, 4),    # config-4 width: block H_128 rotation in the fast quantiser
 ])
 def test_int_path_bit_exact_and_attention_parity(E, nh, r, H, B, L, bits):
     from paper_2604_02570_b200.layer import DecodeLayer

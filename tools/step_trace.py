@@ -25,6 +25,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--per-sm", action="store_true")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     E, B, L = cfg["E"], cfg["B"], cfg["L"]
@@ -41,13 +42,21 @@ def main():
     for _ in range(args.steps):
         layer.step(x, y, graph=False)
     torch.cuda.synchronize()
-    t = layer.debug_copy("trace").astype(np.int64)
+    raw = layer.debug_copy("trace").astype(np.int64)
+    t, smid, nu = raw[:, :10], raw[:, 10], raw[:, 11]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
     print(f"{'mark':10s} {'min':>8s} {'median':>8s} {'max':>8s}   (us from the first CTA's entry)")
     for k, name in enumerate(MARKS):
         col = rel[:, k]
         print(f"{name:10s} {col.min():8.2f} {np.median(col):8.2f} {col.max():8.2f}")
+    if args.per_sm:
+        # per-SM attention-phase duration (qt ready -> attn done) and units, by SM id
+        dur = rel[:, 5] - rel[:, 4]
+        order = np.argsort(smid)
+        print("smid units attn_us")
+        for i in order:
+            print(f"{smid[i]:4d} {nu[i]:5d} {dur[i]:7.2f}")
 
 
 if __name__ == "__main__":
