@@ -62,17 +62,23 @@ struct Cfg {
     static constexpr int NC = PART / 16;       // chunks per half
     static constexpr int ROWB = 2 * PART;
     static constexpr bool MMA = (CD == BF16);
+    // int8 cache on the tensor cores (consume_mma_i8): V bit 3 selects the
+    // CUDA-core consumer instead (A/B)
+    static constexpr bool IMMA = (CD == I8) && !(V & 8) && (R % 32 == 0);
     // tensor-core consumers: 16 warps x one 16-token group per stage (latency
     // hiding: 4 warps per SM sub-partition); CUDA-core consumers: one token per thread
-    static constexpr int NW = (MMA && (V & 2)) ? 16 : 8;
+    static constexpr int NW = ((MMA || IMMA) && (V & 2)) ? 16 : 8;
     static constexpr int THREADS = 32 * NW + 32;  // + one producer warp
-    static constexpr int GPW = kStageTok / (16 * NW);  // 16-token groups per warp per stage
-    static constexpr int ROWS = kStageTok * ROWB;
-    static constexpr int SC = (CD == I8) ? 4 * kStageTok : 0;
+    // tokens per stage: int8 rows are half as wide, so the tensor-core int8
+    // consumer takes 512-token stages (the same 32 KB per stage as bf16)
+    static constexpr int ST = IMMA ? 2 * kStageTok : kStageTok;
+    static constexpr int GPW = ST / (16 * NW);  // 16-token groups per warp per stage
+    static constexpr int ROWS = ST * ROWB;
+    static constexpr int SC = (CD == I8) ? 4 * ST : 0;
     static constexpr int QT_OFF = ROWS + SC;   // absorbed query of the unit (first stage)
     static constexpr int STAGE = QT_OFF + 256;
     static constexpr int RSTRIDE = R + 4;      // floats per lane row of the reduction scratch
-    static constexpr int RED = MMA ? 0 : NW * 32 * RSTRIDE * 4;
+    static constexpr int RED = (MMA || IMMA) ? 0 : NW * 32 * RSTRIDE * 4;
     static constexpr int BUDGET = 222 * 1024;
     static constexpr int ST_RAW = (BUDGET - RED - 4096) / STAGE;
     static constexpr int STAGES = ST_RAW > 8 ? 8 : ST_RAW;
@@ -182,7 +188,7 @@ WSVD_DEV void consume_mma(const AttnArgs& a, const Unit& g, uint8_t* smem, uint6
     const int g8 = lane >> 2, t4 = lane & 3;
     const bool qlane = g8 < 2;
     float m_w = -INFINITY, l = 0.f;
-    const int ns = (g.ntok + kStageTok - 1) / kStageTok;
+    const int ns = (g.ntok + C::ST - 1) / C::ST;
     uint32_t qa[KR][2][2];  // TS=0: B fragments [kk][b0/b1][unused]; TS=1: A frags [kk][hi/lo][a0/a2]
     float acc[KR][4];
 #pragma unroll
@@ -211,7 +217,7 @@ WSVD_DEV void consume_mma(const AttnArgs& a, const Unit& g, uint8_t* smem, uint6
                     }
                 }
         }
-        const int rows = min(kStageTok, g.ntok - s * kStageTok);
+        const int rows = min(C::ST, g.ntok - s * C::ST);
         // ---- scores: sc[grp][i], i = the lane's 4 token slots of the group
         float sc[GPW][4];
 #pragma unroll
@@ -337,6 +343,164 @@ WSVD_DEV void consume_mma(const AttnArgs& a, const Unit& g, uint8_t* smem, uint6
     }
 }
 
+// ----------------------------------------------------------------------------
+// Tensor-core consumer for INT8 caches (per-token scales s_K, s_V).
+// Scores on the integer tensor cores: the absorbed query is split into two
+// int8 rows, qt ~ s1.q1 + s2.q2 (s1 = max|qt|/127, s2 = s1/254, ~15 bits), and
+// D(16 tok x 8) = K_int8(16 x 32) . [q1 | q2](32 x 8) (mma.m16n8k32.s8, exact
+// int32), score = (d1.s1 + d2.s2).s_K.  P.V on the f16 tensor cores:
+// acc(16 x 8 r) += [p'_hi ; p'_lo](16 x 16 tok) . V(16 tok x 8 r) with
+// p' = p.s_V split into f16 hi / lo (~22 bits) and V converted exactly from
+// int8 (ldmatrix.trans pairs of bytes -> f16x2: r = 2n and 2n+1 of each
+// 16-byte unit feed two MMAs).  Results equal the CUDA-core consumer up to fp32
+// reassociation and the ~1e-5 relative query split.
+template <class C, int R>
+WSVD_DEV void consume_mma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                             int& slot, uint32_t& phase, int warp, int lane) {
+    constexpr int K32 = R / 32;     // s8 MMA k-steps for the scores
+    constexpr int UV = R / 16;      // 16-byte units of the V half
+    const int g8 = lane >> 2, t4 = lane & 3;
+    float m_w = -INFINITY, l = 0.f;
+    const int ns = (g.ntok + C::ST - 1) / C::ST;
+    uint32_t qf[K32][2];            // B fragments (int8 x4): b0 / b1 of each k-step
+    float s1 = 1.f, s2 = 1.f;
+    float acc[UV][2][4];            // [unit][even|odd r][D fragment]
+#pragma unroll
+    for (int u = 0; u < UV; ++u)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[u][e][i] = 0.f;
+    for (int s = 0; s < ns; ++s) {
+        mbar_wait(&full[slot], phase);
+        const uint8_t* sp = smem + slot * C::STAGE;
+        const uint32_t sbase = smem_u32(sp);
+        if (s == 0) {
+            const float* q = reinterpret_cast<const float*>(sp + C::QT_OFF);
+            float mx = 0.f;
+#pragma unroll
+            for (int k = 0; k < R; ++k) mx = fmaxf(mx, fabsf(q[k]));
+            s1 = (mx == 0.f) ? 1.f : mx / 127.f;
+            s2 = s1 / 254.f;
+#pragma unroll
+            for (int kk = 0; kk < K32; ++kk)
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    uint32_t w1 = 0, w2 = 0;
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float v = q[kk * 32 + 16 * j + 4 * t4 + e];
+                        const float h = rintf(v / s1);
+                        const float lo = rintf((v - h * s1) / s2);
+                        w1 |= (static_cast<uint32_t>(static_cast<int32_t>(h)) & 0xffu) << (8 * e);
+                        w2 |= (static_cast<uint32_t>(static_cast<int32_t>(fminf(fmaxf(lo, -127.f), 127.f))) & 0xffu) << (8 * e);
+                    }
+                    qf[kk][j] = (g8 == 0) ? w1 : (g8 == 1 ? w2 : 0u);
+                }
+        }
+        const int rows = min(C::ST, g.ntok - s * C::ST);
+        const __half2* sc2 = reinterpret_cast<const __half2*>(sp + C::ROWS);
+        constexpr int GPW = C::GPW;
+        float sc[GPW][2];
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) {
+            const int tb = (warp * GPW + grp) * 16;
+            int d[4] = {0, 0, 0, 0};
+            const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+            for (int kk = 0; kk < K32; ++kk) {
+                uint32_t a0, a1, a2, a3;
+                const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
+                ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
+                mma_s8_16832(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+            }
+            const int t0 = tb + g8, t1 = tb + g8 + 8;
+            const float k0 = __low2float(sc2[t0]), k1 = __low2float(sc2[t1]);
+            sc[grp][0] = (t4 == 0 && t0 < rows)
+                ? fmaf(static_cast<float>(d[0]), s1, static_cast<float>(d[1]) * s2) * k0 : -INFINITY;
+            sc[grp][1] = (t4 == 0 && t1 < rows)
+                ? fmaf(static_cast<float>(d[2]), s1, static_cast<float>(d[3]) * s2) * k1 : -INFINITY;
+        }
+        float lm = -INFINITY;
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) lm = fmaxf(lm, fmaxf(sc[grp][0], sc[grp][1]));
+        // lazily moved reference max: rescale only when a score exceeds it by
+        // more than 2^8 (p <= 256 in between), one vote instead of a reduction
+        if (__any_sync(0xffffffffu, lm > m_w + 8.f)) {
+            const float wm = warp_max(lm);
+            const float f = ex2(m_w - wm);
+            l *= f;
+#pragma unroll
+            for (int u = 0; u < UV; ++u)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[u][e][i] *= f;
+            m_w = wm;
+        }
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) {
+            const int tb = (warp * GPW + grp) * 16;
+            const int t0 = tb + g8, t1 = tb + g8 + 8;
+            const float p0 = (sc[grp][0] == -INFINITY) ? 0.f : ex2(sc[grp][0] - m_w);
+            const float p1 = (sc[grp][1] == -INFINITY) ? 0.f : ex2(sc[grp][1] - m_w);
+            l += p0 + p1;
+            // p' = p . s_V, split into f16 hi / lo
+            const float q0 = p0 * __high2float(sc2[t0]), q1 = p1 * __high2float(sc2[t1]);
+            const __half h0 = __float2half_rn(q0), h1 = __float2half_rn(q1);
+            const __half e0 = __float2half_rn(q0 - __half2float(h0)), e1 = __float2half_rn(q1 - __half2float(h1));
+            const uint32_t hi2 = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+            const uint32_t lo2 = static_cast<uint32_t>(__half_as_ushort(e0)) | (static_cast<uint32_t>(__half_as_ushort(e1)) << 16);
+            // A fragment of P (rows 0 = hi, 1 = lo; k = tokens): lane (g8 in {0,1}, t4)
+            // needs tokens 2t4, 2t4+1 (a0) and 2t4+8, 2t4+9 (a2), held by lanes
+            // 4*(2t4), 4*(2t4+1) as (token, token + 8) pairs
+            const int s0 = 8 * t4, s1l = 8 * t4 + 4;
+            const uint32_t xh = __shfl_sync(0xffffffffu, hi2, s0), yh = __shfl_sync(0xffffffffu, hi2, s1l);
+            const uint32_t xl = __shfl_sync(0xffffffffu, lo2, s0), yl = __shfl_sync(0xffffffffu, lo2, s1l);
+            const uint32_t xx = (g8 == 0) ? xh : xl, yy = (g8 == 0) ? yh : yl;
+            const uint32_t pa0 = (g8 < 2) ? __byte_perm(xx, yy, 0x5410) : 0u;  // tokens 2t4, 2t4+1
+            const uint32_t pa2 = (g8 < 2) ? __byte_perm(xx, yy, 0x7632) : 0u;  // tokens 2t4+8, 2t4+9
+            // V: for each 16-byte unit, matrices (tokens 0-7) and (tokens 8-15)
+            const int vtok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+            for (int u = 0; u < UV; ++u) {
+                uint32_t v0, v1;
+                const uint32_t off = static_cast<uint32_t>(vtok * C::ROWB + C::PART + u * 16);
+                ldsm_x2_trans(sbase + cache_swz(off), v0, v1);
+                // v0 = (tok 2t4: r 2g8, 2g8+1 | tok 2t4+1: r 2g8, 2g8+1) of this unit; v1 = +8 tokens
+                const uint32_t x0 = v0 ^ 0x80808080u, x1 = v1 ^ 0x80808080u;
+                const uint32_t be0 = s8pair_to_f16x2(x0, 0x4240), bo0 = s8pair_to_f16x2(x0, 0x4341);
+                const uint32_t be1 = s8pair_to_f16x2(x1, 0x4240), bo1 = s8pair_to_f16x2(x1, 0x4341);
+                mma_f16_16816(acc[u][0], pa0, 0u, pa2, 0u, be0, be1);
+                mma_f16_16816(acc[u][1], pa0, 0u, pa2, 0u, bo0, bo1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == C::STAGES) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+    // D fragment: lane (g8 in {0,1} = hi / lo row, t4) holds columns 2t4, 2t4+1 of
+    // each MMA; column c of the even (odd) MMA of unit u is r = 16u + 2c (+1)
+    const float lsum = warp_sum(l);
+    float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kMaxWarps + warp) * (R + 2);
+#pragma unroll
+    for (int u = 0; u < UV; ++u)
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const float v = acc[u][e][i] + __shfl_xor_sync(0xffffffffu, acc[u][e][i], 4);  // hi + lo rows
+                if (g8 == 0) wsp[16 * u + 2 * (2 * t4 + i) + e] = v;
+            }
+    if (lane == 0) {
+        wsp[R] = m_w;
+        wsp[R + 1] = lsum;
+    }
+}
+
 template <int CD, int R, int V>
 __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(const AttnArgs a) {
     using C = Cfg<CD, R, V>;
@@ -381,20 +545,20 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
                 const Unit g = unit_geom(u, nch, chunk, len);
                 const uint8_t* src = a.cache + (static_cast<size_t>(g.bh) * cap + g.t0) * C::ROWB;
                 const __half2* ssrc = a.cscale + static_cast<size_t>(g.bh) * cap + g.t0;
-                for (int s = 0; s * kStageTok < g.ntok; ++s) {
-                    const int rows = min(kStageTok, g.ntok - s * kStageTok);
+                for (int s = 0; s * C::ST < g.ntok; ++s) {
+                    const int rows = min(C::ST, g.ntok - s * C::ST);
                     // whole 16-byte units; the swizzle only permutes within 1 KB blocks,
                     // so copy the covering blocks (rows past the end are masked)
-                    const uint32_t rbytes = static_cast<uint32_t>(min(kStageTok * C::ROWB, ((rows * C::ROWB + 1023) / 1024) * 1024));
+                    const uint32_t rbytes = static_cast<uint32_t>(min(C::ST * C::ROWB, ((rows * C::ROWB + 1023) / 1024) * 1024));
                     const uint32_t sbytes = (CD == I8) ? static_cast<uint32_t>((rows * 4 + 15) & ~15) : 0u;
                     const uint32_t qbytes = (s == 0) ? static_cast<uint32_t>(R * 4) : 0u;
                     mbar_wait(&empty[slot], phase ^ 1u);
                     uint8_t* dst = smem + slot * C::STAGE;
                     mbar_arrive_expect_tx(&full[slot], rbytes + sbytes + qbytes);
-                    tma_bulk_g2s_stream(dst, src + static_cast<size_t>(s) * kStageTok * C::ROWB, rbytes,
+                    tma_bulk_g2s_stream(dst, src + static_cast<size_t>(s) * C::ST * C::ROWB, rbytes,
                                         &full[slot], pol);
                     if (CD == I8)
-                        tma_bulk_g2s_stream(dst + C::ROWS, ssrc + s * kStageTok, sbytes, &full[slot], pol);
+                        tma_bulk_g2s_stream(dst + C::ROWS, ssrc + s * C::ST, sbytes, &full[slot], pol);
                     if (s == 0)
                         tma_bulk_g2s(dst + C::QT_OFF, a.qt + static_cast<size_t>(g.bh) * R, qbytes, &full[slot]);
                     if (++slot == C::STAGES) {
@@ -414,12 +578,12 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const Unit g = unit_geom(u, nch, chunk, len);
         float m_w = -INFINITY, l = 0.f;
-        const int ns = (g.ntok + kStageTok - 1) / kStageTok;
+        const int ns = (g.ntok + C::ST - 1) / C::ST;
 
-        if constexpr (C::MMA && (V & 4)) {
+        if constexpr ((C::MMA || C::IMMA) && (V & 4)) {
             // pipeline probe (WSVD_ATTN_VARIANT bit 2): drain the stages without
             // computing -- the streaming ceiling of this producer structure
-            const int ns = (g.ntok + kStageTok - 1) / kStageTok;
+            const int ns = (g.ntok + C::ST - 1) / C::ST;
             for (int s = 0; s < ns; ++s) {
                 mbar_wait(&full[slot], phase);
                 __syncwarp();
@@ -431,6 +595,8 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
             }
         } else if constexpr (C::MMA) {
             consume_mma<C, R, (V & 1)>(a, g, smem, full, empty, slot, phase, warp, lane);
+        } else if constexpr (C::IMMA) {
+            consume_mma_i8<C, R>(a, g, smem, full, empty, slot, phase, warp, lane);
         } else {
             // ------------------------------------------ CUDA-core path (f32, int8)
             float qr[NC][EPC];
@@ -449,7 +615,7 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
 #pragma unroll
                         for (int e = 0; e < EPC; ++e) qr[c][e] = q[c * EPC + e];
                 }
-                const int rows = min(kStageTok, g.ntok - s * kStageTok);
+                const int rows = min(C::ST, g.ntok - s * C::ST);
                 const bool valid = tid < rows;
                 const uint32_t sbase = smem_u32(sp);
                 const uint32_t rlog = static_cast<uint32_t>(tid * C::ROWB);
@@ -607,20 +773,25 @@ cudaError_t launch_v(const AttnArgs& a, cudaStream_t s) {
 int attn_variant() {
     static const int v = [] {
         const char* e = std::getenv("WSVD_ATTN_VARIANT");
-        return e ? (std::atoi(e) & 7) : kDefaultVariant;
+        return e ? (std::atoi(e) & 15) : kDefaultVariant;
     }();
     return v;
 }
 
 template <int CD, int R>
 cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
-    if constexpr (CD != BF16) {
+    if constexpr (CD == I8) {
+        // WSVD_ATTN_VARIANT bit 3: the CUDA-core int8 consumer; bit 1: 16 consumer warps (A/B)
+        if (attn_variant() & 8) return launch_v<CD, R, 8>(a, s);
+        if (attn_variant() & 4) return launch_v<CD, R, 4>(a, s);  // streaming probe (no compute)
+        return (attn_variant() & 2) ? launch_v<CD, R, 2>(a, s) : launch_v<CD, R, 0>(a, s);
+    } else if constexpr (CD != BF16) {
         return launch_v<CD, R, 0>(a, s);
     } else {
         if constexpr (R != 32) {
             return launch_v<CD, R, kDefaultVariant>(a, s);
         } else {
-            switch (attn_variant()) {
+            switch (attn_variant() & 7) {
                 case 0: return launch_v<CD, R, 0>(a, s);
                 case 1: return launch_v<CD, R, 1>(a, s);
                 case 2: return launch_v<CD, R, 2>(a, s);

@@ -198,6 +198,31 @@ WSVD_DEV void ldsm_x4_trans(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t&
                  : "r"(addr));
 }
 
+// D(16x8 f32) += A(16x16 f16, row) * B(16x8 f16, col)
+WSVD_DEV void mma_f16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                            uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+        "{%8,%9}, {%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+WSVD_DEV void ldsm_x2_trans(uint32_t addr, uint32_t& r0, uint32_t& r1) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];"
+                 : "=r"(r0), "=r"(r1)
+                 : "r"(addr));
+}
+
+// Two signed bytes of w (selected by sel: 0x..B.A picks bytes A, B) -> exact
+// f16x2: (byte ^ 0x80) is v + 128 in [1, 255]; 0x6400 | u is the f16 1024 + u,
+// so subtracting 1152 leaves v exactly.
+WSVD_DEV uint32_t s8pair_to_f16x2(uint32_t w_xor80, uint32_t sel) {
+    const uint32_t h = __byte_perm(w_xor80, 0x64646464u, sel);
+    const __half2 v = __hsub2(*reinterpret_cast<const __half2*>(&h), __floats2half2_rn(1152.f, 1152.f));
+    return *reinterpret_cast<const uint32_t*>(&v);
+}
+
 // D(16x8 s32) += A(16x32 s8, row) * B(32x8 s8, col)
 WSVD_DEV void mma_s8_16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                            uint32_t b0, uint32_t b1) {
