@@ -128,6 +128,19 @@ WSVD_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// non-blocking test of an mbarrier phase
+WSVD_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 // 1-D bulk copy global -> shared, completion signalled on an mbarrier (TMA)
 WSVD_DEV void tma_bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
