@@ -236,13 +236,6 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         fence_mbar_init();
     }
     __syncthreads();
-    griddep_wait();
-    griddep_launch_dependents();
-    STEP_MARK(1);
-
-    const int pos = *a.d_len;  // the new token's row; attention covers pos + 1 rows
-    const unsigned epoch = static_cast<unsigned>(*a.epoch);  // fused steps so far (barrier generations)
-    const int len = pos + 1;
     const int splits = a.Kp / kKS;
     const int cps = G / splits;  // CTAs per projection split
     const int ps = cta % splits, pj = cta / splits;
@@ -256,6 +249,27 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     // with plain stores, once (it may live in mapped host memory)
     const int nt3 = cta < a.otiles ? (a.otiles - 1 - cta) / G + 1 : 0;
     const int np3 = nt3 * osplits;  // <= kNA (host-checked)
+    // The weights (projection W-tiles, then the folded O-projection) are
+    // constant across steps: the producer starts streaming them before the
+    // predecessor has drained (programmatic dependent launch), only the token,
+    // the length and the cache rows wait for it
+    int ia_pre = 0;
+    if (warp == kNW && lane == 0) {
+        for (; ia_pre < kNA && ia_pre < np1 + np3; ++ia_pre) {
+            mbar_arrive_expect_tx(&fullA[ia_pre], kItem);
+            const uint8_t* src = ia_pre < np1
+                ? a.A + (static_cast<size_t>(plo + ia_pre) * splits + ps) * kItem
+                : a.Wo + (static_cast<size_t>(cta + ((ia_pre - np1) / osplits) * G) * osplits + (ia_pre - np1) % osplits) * kItem;
+            tma_bulk_g2s(ringA + ia_pre * kItem, src, kItem, &fullA[ia_pre]);
+        }
+    }
+    griddep_wait();
+    griddep_launch_dependents();
+    STEP_MARK(1);
+
+    const int pos = *a.d_len;  // the new token's row; attention covers pos + 1 rows
+    const unsigned epoch = static_cast<unsigned>(*a.epoch);  // fused steps so far (barrier generations)
+    const int len = pos + 1;
     int nch, chunk;
     step_chunking(a, len, nch, chunk);
     const int n_units = a.B * a.nh * nch;
@@ -268,7 +282,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     if (warp == kNW) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            int ia = 0;
+            int ia = ia_pre;  // the first weight items went out before griddep_wait
             const int na = np1 + np3;
             auto issue_a = [&]() {
                 const int slot = ia % kNA;
