@@ -101,6 +101,16 @@ WSVD_DEV void mma_commit(uint64_t* bar) {
 WSVD_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 WSVD_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
+// 32 lanes x 16 consecutive fp32 columns, no wait (pair with tmem_wait)
+WSVD_DEV void tmem_ld16_nowait(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+}
+WSVD_DEV void tmem_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
 // 32 lanes x 16 consecutive fp32 columns: thread i gets lane (taddr.lane + i)
 WSVD_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     uint32_t r[16];
@@ -112,6 +122,16 @@ WSVD_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// packed fp32x2 FMA (FFMA2, sm_100): d.{x,y} = a.{x,y} * b.{x,y} + d.{x,y}
+WSVD_DEV void ffma2(float2& d, float ax, float ay, float bx, float by) {
+    uint64_t dd, aa, bb;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(dd) : "f"(d.x), "f"(d.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(aa) : "f"(ax), "f"(ay));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(bb) : "f"(bx), "f"(by));
+    asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(dd) : "l"(aa), "l"(bb));
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(dd));
 }
 
 struct TUnit {
@@ -279,19 +299,31 @@ __global__ void __launch_bounds__(kThr, 1) decode_attn_tc_kernel(const AttnArgs 
                 float sc = 0.f;
                 if (wg * 128 < rows) {
                     const uint32_t taddr = tmem + (static_cast<uint32_t>(wq * 32) << 16) + static_cast<uint32_t>(tb * 256 + wg * 128);
+                    // the 128-term dot as packed fp32x2 FMAs: half the instructions
+                    // and two independent chains
+                    float2 s2 = make_float2(0.f, 0.f);
+                    // two 16-column loads in flight per wait (the TMEM load latency,
+                    // not the math, bounds this loop)
 #pragma unroll
-                    for (int c = 0; c < H / 16; ++c) {
-                        float kv[16];
-                        tmem_ld16(taddr + c * 16, kv);
+                    for (int c = 0; c < H / 32; ++c) {
+                        uint32_t ka[16], kb[16];
+                        tmem_ld16_nowait(taddr + c * 32, ka);
+                        tmem_ld16_nowait(taddr + c * 32 + 16, kb);
+                        tmem_wait();
 #pragma unroll
                         for (int i = 0; i < 16; i += 4) {
-                            const float4 q4 = *reinterpret_cast<const float4*>(qs + c * 16 + i);
-                            sc = fmaf(kv[i], q4.x, sc);
-                            sc = fmaf(kv[i + 1], q4.y, sc);
-                            sc = fmaf(kv[i + 2], q4.z, sc);
-                            sc = fmaf(kv[i + 3], q4.w, sc);
+                            const float4 q4 = *reinterpret_cast<const float4*>(qs + c * 32 + i);
+                            ffma2(s2, __uint_as_float(ka[i]), __uint_as_float(ka[i + 1]), q4.x, q4.y);
+                            ffma2(s2, __uint_as_float(ka[i + 2]), __uint_as_float(ka[i + 3]), q4.z, q4.w);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 16; i += 4) {
+                            const float4 q4 = *reinterpret_cast<const float4*>(qs + c * 32 + 16 + i);
+                            ffma2(s2, __uint_as_float(kb[i]), __uint_as_float(kb[i + 1]), q4.x, q4.y);
+                            ffma2(s2, __uint_as_float(kb[i + 2]), __uint_as_float(kb[i + 3]), q4.z, q4.w);
                         }
                     }
+                    sc = s2.x + s2.y;
                 }
                 tc_fence_before();
                 __syncwarp();
@@ -316,14 +348,14 @@ __global__ void __launch_bounds__(kThr, 1) decode_attn_tc_kernel(const AttnArgs 
 #pragma unroll
                     for (int c = 0; c < PART / 16; ++c) {
                         const uint4 v = lds128(vrow + cache_swz(static_cast<uint32_t>(tok * ROWB + PART + c * 16)));
-                        acc[c * 8 + 0] = fmaf(p, bf16lo(v.x), acc[c * 8 + 0]);
-                        acc[c * 8 + 1] = fmaf(p, bf16hi(v.x), acc[c * 8 + 1]);
-                        acc[c * 8 + 2] = fmaf(p, bf16lo(v.y), acc[c * 8 + 2]);
-                        acc[c * 8 + 3] = fmaf(p, bf16hi(v.y), acc[c * 8 + 3]);
-                        acc[c * 8 + 4] = fmaf(p, bf16lo(v.z), acc[c * 8 + 4]);
-                        acc[c * 8 + 5] = fmaf(p, bf16hi(v.z), acc[c * 8 + 5]);
-                        acc[c * 8 + 6] = fmaf(p, bf16lo(v.w), acc[c * 8 + 6]);
-                        acc[c * 8 + 7] = fmaf(p, bf16hi(v.w), acc[c * 8 + 7]);
+                        const uint32_t vw[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            float2 a2 = make_float2(acc[c * 8 + 2 * k], acc[c * 8 + 2 * k + 1]);
+                            ffma2(a2, p, p, bf16lo(vw[k]), bf16hi(vw[k]));
+                            acc[c * 8 + 2 * k] = a2.x;
+                            acc[c * 8 + 2 * k + 1] = a2.y;
+                        }
                     }
                 }
                 __syncwarp();
