@@ -65,3 +65,60 @@ class DenseFlashDecodeLayer:
             out = F.scaled_dot_product_attention(q.view(B, nh, 1, H), K, V)  # flash decoding
             torch.matmul(out.reshape(B, nh * H), self.w_o, out=y)
         return run
+
+
+class SharedLatentLayer:
+    """The paper's "W/o per-head" comparison (reference
+    decode::shared_decode_step with materialize, src/decode.cpp:330-390): one
+    shared latent of width R_s = n_heads * r per layer (the same cache bytes as
+    the per-head latents), which every head reads in full; the naive schedule
+    rebuilds every head's full keys and values (K = C_K . B_K, V = C_V . B_V,
+    written back to memory) and then attends over them with SDPA.  Library
+    kernels (cuBLAS, SDPA) on purpose: it is a baseline."""
+
+    def __init__(self, embed_dim: int, n_heads: int, head_dim: int, shared_rank: int, batch: int,
+                 capacity: int, device=0, dtype=None, seed: int = 0):
+        import torch
+        self.torch = torch
+        dt = dtype or torch.bfloat16
+        self.E, self.nh, self.H, self.R, self.B = embed_dim, n_heads, head_dim, shared_rank, batch
+        self.dev = torch.device("cuda", device)
+        g = torch.Generator(device=self.dev)
+        g.manual_seed(seed)
+        d = n_heads * head_dim
+        self.a_q = (torch.randn((embed_dim, d), generator=g, device=self.dev) / math.sqrt(embed_dim)).to(dt)
+        self.a_kv = (torch.randn((embed_dim, 2 * shared_rank), generator=g, device=self.dev)
+                     / math.sqrt(embed_dim)).to(dt)
+        self.b_k = (torch.randn((shared_rank, d), generator=g, device=self.dev) / math.sqrt(shared_rank)).to(dt)
+        self.b_v = (torch.randn((shared_rank, d), generator=g, device=self.dev) / math.sqrt(shared_rank)).to(dt)
+        self.w_o = (torch.randn((d, embed_dim), generator=g, device=self.dev) / math.sqrt(d)).to(dt)
+        self.ck = torch.zeros((batch, capacity, shared_rank), device=self.dev, dtype=dt)
+        self.cv = torch.zeros_like(self.ck)
+        self.cap = capacity
+
+    def fill(self, length: int, seed: int = 1):
+        g = self.torch.Generator(device=self.dev)
+        g.manual_seed(seed)
+        self.ck[:, :length].normal_(generator=g)
+        self.cv[:, :length].normal_(generator=g)
+
+    def latent_bytes(self, length: int) -> int:
+        return self.B * length * 2 * self.R * self.ck.element_size()
+
+    def step_fn(self, x, y, pos: int):
+        torch = self.torch
+        F = torch.nn.functional
+        B, nh, H, R = self.B, self.nh, self.H, self.R
+        CK, CV = self.ck[:, :pos + 1], self.cv[:, :pos + 1]
+
+        def run():
+            q = (x @ self.a_q).view(B, nh, 1, H)
+            ckv = x @ self.a_kv
+            self.ck[:, pos].copy_(ckv[:, :R])
+            self.cv[:, pos].copy_(ckv[:, R:])
+            # materialised keys and values of every head, [B][nh][L][H]
+            K = (CK @ self.b_k).view(B, pos + 1, nh, H).transpose(1, 2).contiguous()
+            V = (CV @ self.b_v).view(B, pos + 1, nh, H).transpose(1, 2).contiguous()
+            out = F.scaled_dot_product_attention(q, K, V)
+            torch.matmul(out.reshape(B, nh * H), self.w_o, out=y)
+        return run
