@@ -113,3 +113,42 @@ def test_step_kind_reports_the_path():
     assert layer32.launches_per_step() == 1
     layer32.set_attention("explicit_tc")
     assert layer32.launches_per_step() > 1  # the explicit mode runs the multi-kernel step
+
+
+@pytest.mark.parametrize("B,L", [(1, 1), (3, 2), (16, 33), (7, 257)])
+def test_fused_step_short_caches_and_ragged_ranks(B, L):
+    """the first tokens of a sequence (the step's own row is the only or almost
+    the only one; decode.cpp:312-328 L = 1 case), odd batches, and ragged
+    per-head ranks zero-padded to 32 (test_decode.cpp:190-194)"""
+    from paper_2604_02570_b200.layer import DecodeLayer
+    E, nh, H = 512, 16, 128
+    rng = O.Rng(8400 + B * 1000 + L)
+    ranks = [[32 - (h % 5), 32 - (h % 3), 17 + h] for h in range(nh)]
+    lay = O.random_layer(rng, E, H, ranks)
+    wo = O.bf16_round(rng.normal_matrix(nh * H, E, 1.0 / np.sqrt(E)))
+    layer = DecodeLayer(to_factors(lay), wo, batch=B, capacity=L + 4, cache_dtype="bf16", weight_dtype="bf16")
+    assert layer.launches_per_step() == 1
+    dev = torch.device("cuda", 0)
+    toks = O.bf16_round(rng.normal_matrix(L * B, E)).reshape(L, B, E)
+    if L > 1:
+        layer.prefill(torch.from_numpy(toks[:-1].astype(np.float32)).to(dev))
+    y = torch.empty((B, E), device=dev)
+    layer.step(torch.from_numpy(toks[-1].astype(np.float32)).to(dev), y)
+    torch.cuda.synchronize()
+    assert layer.length() == L and layer.sync_length() == L
+    y = y.cpu().numpy().astype(np.float64)
+    lb = lay.map(O.bf16_round)
+    R = layer.rpad
+    for b in range(B):
+        ck = np.zeros((nh, L, lay.rmax))
+        cv = np.zeros((nh, L, lay.rmax))
+        q = None
+        for t in range(L):
+            q = O.append_token(lb, ck, cv, t, toks[t, b])
+        dev_k = np.stack([layer.read_latents(b, h)[0][:, :lay.rmax] for h in range(nh)])
+        dev_v = np.stack([layer.read_latents(b, h)[1][:, :lay.rmax] for h in range(nh)])
+        for h in range(nh):  # zero-padded latent columns stay zero
+            assert not layer.read_latents(b, h)[0][:, lay.ranks[h, 1]:R].any()
+        ref = O.fused_decode_step(lb, dev_k, dev_v, L, q, 32)
+        y_ref = ref.reshape(-1) @ wo
+        assert rel_err_rows(y[b:b + 1], y_ref[None]) <= 1e-2, f"b={b}"
