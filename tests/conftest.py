@@ -19,4 +19,9 @@ def _oracle_built():
     from oracle import oracle as O
     if not os.path.exists(O.ORACLE_SO):
         O.build()
+    # the native library (nvcc cross-compiles sm_100a without a GPU): a fresh
+    # checkout gets it built once, incrementally afterwards
+    from paper_2604_02570_b200 import build as B
+    if not os.path.exists(B.LIB):
+        B.build()
     yield
