@@ -26,6 +26,8 @@ def main():
     ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--per-sm", action="store_true")
+    ap.add_argument("--attn-only", action="store_true")
+    ap.add_argument("--proj-only", action="store_true")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     E, B, L = cfg["E"], cfg["B"], cfg["L"]
@@ -46,6 +48,10 @@ def main():
     t, smid, nu = raw[:, :10], raw[:, 10], raw[:, 11]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
+    if args.attn_only:  # attention CTAs only (nu > 0): the projection CTAs skip marks 3-5
+        rel = rel[nu > 0]
+    if args.proj_only:
+        rel = rel[nu == 0]
     print(f"{'mark':10s} {'min':>8s} {'median':>8s} {'max':>8s}   (us from the first CTA's entry)")
     for k, name in enumerate(MARKS):
         col = rel[:, k]
