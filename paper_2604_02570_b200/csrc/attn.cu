@@ -64,7 +64,7 @@ struct Cfg {
     static constexpr bool MMA = (CD == BF16);
     // int8 cache on the tensor cores (consume_mma_i8): V bit 3 selects the
     // CUDA-core consumer instead (A/B)
-    static constexpr bool IMMA = (CD == I8) && !(V & 8) && (R % 32 == 0);
+    static constexpr bool IMMA = (CD == I8) && !(V & 8) && (R % 16 == 0);
     // tensor-core consumers: 16 warps x one 16-token group per stage (latency
     // hiding: 4 warps per SM sub-partition); CUDA-core consumers: one token per thread
     static constexpr int NW = ((MMA || IMMA) && (V & 2)) ? 16 : 8;
@@ -357,7 +357,7 @@ WSVD_DEV void consume_mma(const AttnArgs& a, const Unit& g, uint8_t* smem, uint6
 template <class C, int R>
 WSVD_DEV void consume_mma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, uint64_t* full, uint64_t* empty,
                              int& slot, uint32_t& phase, int warp, int lane) {
-    constexpr int K32 = R / 32;     // s8 MMA k-steps for the scores
+    constexpr int K32 = (R + 31) / 32;  // s8 MMA k-steps for the scores (the last may be half: R % 32 == 16)
     constexpr int UV = R / 16;      // 16-byte units of the V half
     const int g8 = lane >> 2, t4 = lane & 3;
     float m_w = -INFINITY, l = 0.f;
@@ -389,6 +389,7 @@ WSVD_DEV void consume_mma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, ui
                     uint32_t w1 = 0, w2 = 0;
 #pragma unroll
                     for (int e = 0; e < 4; ++e) {
+                        if (kk * 32 + 16 * j >= R) break;  // the padded half of a last k-step
                         const float v = q[kk * 32 + 16 * j + 4 * t4 + e];
                         const float h = rintf(v / s1);
                         const float lo = rintf((v - h * s1) / s2);
@@ -409,9 +410,14 @@ WSVD_DEV void consume_mma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, ui
             const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
 #pragma unroll
             for (int kk = 0; kk < K32; ++kk) {
-                uint32_t a0, a1, a2, a3;
-                const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
-                ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
+                uint32_t a0, a1, a2 = 0u, a3 = 0u;
+                if (kk * 32 + 16 < R) {
+                    const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
+                    ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
+                } else {  // r in [32kk, 32kk + 16): the upper half of the k-step is zero
+                    const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2) * 16);
+                    ldsm_x2(sbase + cache_swz(off), a0, a1);
+                }
                 mma_s8_16832(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
             }
             const int t0 = tb + g8, t1 = tb + g8 + 8;
