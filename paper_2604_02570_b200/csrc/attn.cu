@@ -698,6 +698,10 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
 // Split-KV combine (SoftmaxState::merge, decode.cpp:59-75, over the chunk x
 // warp partials in a fixed order) and the single B_V up-projection per head
 // (decode.cpp:198-203).  One CTA per (sequence, head).
+inline int combine_smem(int max_chunks, int ppc, int R) {
+    return (max_chunks * ppc * (R + 3) + R + (R > 128 ? R : 128) + 8) * 4;
+}
+
 __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a, int parts_per_chunk) {
     extern __shared__ float sm[];  // parts [np][R+2], then vt [R]
     const int bh = blockIdx.x, tid = threadIdx.x, R = a.R;
@@ -715,24 +719,59 @@ __global__ void __launch_bounds__(128) attn_combine_kernel(const AttnArgs a, int
     // the first parts_per_chunk warp slots of each chunk)
     const int pw = parts_per_chunk * (R + 2);
     const float* wsb = a.ws + static_cast<size_t>(bh) * a.max_chunks * kMaxWarps * (R + 2);
-    for (int i = tid; i < np * (R + 2); i += blockDim.x) {
-        const int c = i / pw, r = i - c * pw;
-        part[i] = __ldcg(wsb + static_cast<size_t>(c) * kMaxWarps * (R + 2) + r);
+    const int n = np * (R + 2);
+    // 8 independent L2 loads in flight per thread (the partials were just
+    // written by the attention kernel and sit in L2)
+    for (int i0 = tid; i0 < n; i0 += 8 * 128) {
+        float v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * 128;
+            const int c = i / pw, r = i - c * pw;
+            v[u] = i < n ? __ldcg(wsb + static_cast<size_t>(c) * kMaxWarps * (R + 2) + r) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (i0 + u * 128 < n) part[i0 + u * 128] = v[u];
     }
     __syncthreads();
+    // parallel merge: block max of the partial maxima, per-partial factors,
+    // then G = 128 / R thread groups each sum a fixed residue class of the
+    // partials for every latent column (fixed order: deterministic)
+    float* fac = vt + R;             // [np]
+    float* red = fac + a.max_chunks * parts_per_chunk;  // [max(128, R)] + [4] + [4]
+    const int warp = tid >> 5, lane = tid & 31;
     float M = -INFINITY;
-    for (int p = 0; p < np; ++p) M = fmaxf(M, part[p * (R + 2) + R]);
-    float L = 0.f, acc = 0.f;
-    for (int p = 0; p < np; ++p) {
+    for (int p = tid; p < np; p += 128) M = fmaxf(M, part[p * (R + 2) + R]);
+    M = warp_max(M);
+    float* wred = red + (R > 128 ? R : 128);
+    if (lane == 0) wred[warp] = M;
+    __syncthreads();
+    M = fmaxf(fmaxf(wred[0], wred[1]), fmaxf(wred[2], wred[3]));
+    float Lp = 0.f;
+    for (int p = tid; p < np; p += 128) {
         const float m = part[p * (R + 2) + R];
-        if (m == -INFINITY) continue;  // a warp that saw no token of its chunk
-        const float f = ex2(m - M);
-        L = fmaf(part[p * (R + 2) + R + 1], f, L);
-        if (tid < R) acc = fmaf(part[p * (R + 2) + tid], f, acc);
+        const float f = m == -INFINITY ? 0.f : ex2(m - M);  // a warp that saw no token of its chunk
+        fac[p] = f;
+        Lp = fmaf(part[p * (R + 2) + R + 1], f, Lp);
     }
-    if (tid < R) {
-        vt[tid] = acc / L;
-        if (a.vlat) a.vlat[static_cast<size_t>(bh) * R + tid] = acc / L;
+    Lp = warp_sum(Lp);
+    if (lane == 0) wred[4 + warp] = Lp;
+    __syncthreads();
+    const float L = (wred[4] + wred[5]) + (wred[6] + wred[7]);
+    const int G = R >= 128 ? 1 : 128 / R;
+    for (int i = tid; i < G * R; i += 128) {
+        const int g = i / R, r = i - g * R;
+        float s = 0.f;
+        for (int p = g; p < np; p += G) s = fmaf(part[p * (R + 2) + r], fac[p], s);
+        red[i] = s;
+    }
+    __syncthreads();
+    for (int r = tid; r < R; r += 128) {
+        float acc = 0.f;
+        for (int g = 0; g < G; ++g) acc += red[g * R + r];
+        vt[r] = acc / L;
+        if (a.vlat) a.vlat[static_cast<size_t>(bh) * R + r] = acc / L;
     }
     if (a.out == nullptr) return;  // the layer step folds B_V into W_o
     __syncthreads();
@@ -764,7 +803,7 @@ cudaError_t launch_v(const AttnArgs& a, cudaStream_t s) {
         }
         cudaError_t e = launch_pdl(k, dim3(a.grid), dim3(C::THREADS), C::SMEM, s, a);
         if (e != cudaSuccess) return e;
-        const int csmem = (a.max_chunks * C::NW * (R + 2) + R) * 4;
+        const int csmem = combine_smem(a.max_chunks, C::NW, R);
         if (csmem > g_combine_smem_attr) {  // one (non-template) kernel: track its attribute globally
             e = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
             if (e != cudaSuccess) return e;
@@ -849,7 +888,7 @@ int attn_occupancy(int cdtype, int R) {
 }
 
 cudaError_t launch_attn_combine(const AttnArgs& a, int parts_per_chunk, cudaStream_t s) {
-    const int csmem = (a.max_chunks * parts_per_chunk * (a.R + 2) + a.R) * 4;
+    const int csmem = combine_smem(a.max_chunks, parts_per_chunk, a.R);
     if (csmem > g_combine_smem_attr) {
         cudaError_t e = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);
         if (e != cudaSuccess) return e;

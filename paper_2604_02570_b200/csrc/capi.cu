@@ -284,7 +284,7 @@ int check_layer(wsvd_layer_t l) {
 int run_projection(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* splits_out) {
     wsvd_layer_s* L = c->L;
     const int wd = L->d.weight_dtype;
-    const int ks = L->ks;
+    const int ks = (wd == F32 && f32_rows_path(M, L->Kp, 512)) ? 512 : L->ks;
     if (!gemm_fits(wd, M, ks))
         return set_err(WSVD_ECONFIG, std::to_string(M) + " token rows do not fit the projection kernel");
     const int splits = L->Kp / ks;

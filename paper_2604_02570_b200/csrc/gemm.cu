@@ -343,6 +343,111 @@ __global__ void __launch_bounds__(kF32Threads) skinny_f32_kernel(const GemmArgs 
     }
 }
 
+// fp32 decode GEMV (M <= kF32RowsM token rows).  Work items are (row, K split)
+// pieces of U*128 floats -- U float4 per lane, one coalesced 512-byte warp
+// load each -- dealt round-robin to the warps of a persistent grid, so every
+// SM streams the same number of bytes; each warp double-buffers its items in
+// registers (the next item is in flight while the current one is consumed,
+// the first before the grid-dependency wait: weights do not depend on the
+// previous kernel).  x sits in shared memory, staged once per CTA.  Partials
+// go to P[split][M][N] like the other projection kernels.
+constexpr int kF32RowsM = 4;
+constexpr int kF32RowsThreads = 256;
+template <int M, int U>
+__global__ void __launch_bounds__(kF32RowsThreads, 2) skinny_f32_rows_kernel(const GemmArgs a) {
+    extern __shared__ __align__(16) float xsf[];
+    const int lane = threadIdx.x & 31;
+    const float* W = reinterpret_cast<const float*>(a.W);
+    const int splits = a.Kp / (U * 128);
+    const int items = a.N * splits;
+    const int nwarps = gridDim.x * (kF32RowsThreads / 32);
+    const int gw = blockIdx.x * (kF32RowsThreads / 32) + (threadIdx.x >> 5);
+    float4 w[U], wn[U];
+    auto load = [&](int t, float4* dst) {
+        const int n = t / splits, sp = t - n * splits;
+        const float4* src = reinterpret_cast<const float4*>(W + static_cast<size_t>(n) * a.Kp + sp * U * 128) + lane;
+#pragma unroll
+        for (int u = 0; u < U; ++u) dst[u] = t < items ? __ldcs(src + u * 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+    };
+    load(gw, w);
+    griddep_wait();
+    griddep_launch_dependents();
+    if (a.commit_len && blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(a.commit_len, 1);
+    const float* X = reinterpret_cast<const float*>(a.X);
+    if ((a.K & 3) == 0 && (a.ldx & 3) == 0) {
+        const int kv = a.Kp >> 2;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < M * kv; i += kF32RowsThreads) {
+            const int m = i / kv, k = (i - m * kv) * 4;
+            reinterpret_cast<float4*>(xsf)[i] = k < a.K ? *reinterpret_cast<const float4*>(X + static_cast<size_t>(m) * a.ldx + k)
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    } else {
+        for (int i = threadIdx.x; i < M * a.Kp; i += kF32RowsThreads) {
+            const int m = i / a.Kp, k = i - m * a.Kp;
+            xsf[i] = (k < a.K) ? X[static_cast<size_t>(m) * a.ldx + k] : 0.f;
+        }
+    }
+    __syncthreads();
+    for (int t = gw; t < items; t += nwarps) {
+        load(t + nwarps, wn);
+        const int n = t / splits, sp = t - n * splits;
+        float acc[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int v = sp * U * 32 + u * 32 + lane;
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const float4 x = reinterpret_cast<const float4*>(xsf + m * a.Kp)[v];
+                acc[m] = fmaf(w[u].x, x.x, acc[m]);
+                acc[m] = fmaf(w[u].y, x.y, acc[m]);
+                acc[m] = fmaf(w[u].z, x.z, acc[m]);
+                acc[m] = fmaf(w[u].w, x.w, acc[m]);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const float sum = warp_sum(acc[m]);
+            if (lane == 0) reinterpret_cast<float*>(a.P)[(static_cast<size_t>(sp) * a.M + m) * a.N + n] = sum;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) w[u] = wn[u];
+    }
+}
+
+template <int M, int U>
+cudaError_t launch_f32_rows_u(const GemmArgs& a, cudaStream_t s) {
+    const int smem = M * a.Kp * 4;
+    auto k = skinny_f32_rows_kernel<M, U>;
+    static int attr_smem = 0;
+    if (smem > attr_smem) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_smem = smem;
+    }
+    const int wpc = kF32RowsThreads / 32;
+    static int per_sm = 0;  // resident CTAs per SM (registers / shared memory), at most 4
+    if (per_sm == 0) {
+        int nb = 1;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k, kF32RowsThreads, smem) != cudaSuccess) nb = 1;
+        per_sm = std::max(1, std::min(4, nb));
+    }
+    const int items = a.N * (a.Kp / (U * 128));
+    const int grid = std::max(1, std::min((items + wpc - 1) / wpc, a.grid * per_sm));
+    return launch_pdl(k, dim3(grid), dim3(kF32RowsThreads), smem, s, a);
+}
+
+template <int M>
+cudaError_t launch_f32_rows(const GemmArgs& a, cudaStream_t s) {
+    switch (a.KS / 128) {
+        case 2: return launch_f32_rows_u<M, 2>(a, s);
+        case 4: return launch_f32_rows_u<M, 4>(a, s);
+        default: return launch_f32_rows_u<M, 8>(a, s);
+    }
+}
+
 template <int WT, int MT>
 cudaError_t launch_stream(const GemmArgs& a, cudaStream_t s) {
     using S = StreamCfg<WT, MT>;
@@ -385,6 +490,10 @@ __global__ void reduce_partials_kernel(const float* __restrict__ P, int splits, 
 
 }  // namespace
 
+bool f32_rows_path(int M, int Kp, int KS) {
+    return M <= kF32RowsM && (KS == 256 || KS == 512 || KS == 1024) && Kp % KS == 0 && M * Kp * 4 <= 200 * 1024;
+}
+
 bool gemm_fits(int wdtype, int M, int KS) {
     const int mt = (M + 15) / 16;
     auto st = [&](auto cfg) { return decltype(cfg)::stages(KS) >= 2; };
@@ -403,6 +512,14 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s) {
         case I8: return launch_wt<I8>(a, s);
         case I4: return launch_wt<I4>(a, s);
         case F32: {
+            if (f32_rows_path(a.M, a.Kp, a.KS)) {
+                switch (a.M) {
+                    case 1: return launch_f32_rows<1>(a, s);
+                    case 2: return launch_f32_rows<2>(a, s);
+                    case 3: return launch_f32_rows<3>(a, s);
+                    default: return launch_f32_rows<4>(a, s);
+                }
+            }
             const int smem = a.M * a.KS * 4;
             static int attr_smem = 0;
             if (smem > attr_smem) {

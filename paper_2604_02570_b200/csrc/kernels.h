@@ -28,6 +28,8 @@ struct GemmArgs {
 };
 // true when M token rows with split KS fit the streaming kernel's shared memory
 bool gemm_fits(int wdtype, int M, int KS);
+// fp32 weights, M <= 4 token rows, KS in {256, 512, 1024}: the balanced row-piece GEMV
+bool f32_rows_path(int M, int Kp, int KS);
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s);
 
 // Sum split partials into fp32 y [M][N] (fixed split order).
