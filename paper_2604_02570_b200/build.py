@@ -26,6 +26,7 @@ NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CUDA_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
               "--expt-relaxed-constexpr", f"-I{os.path.join(ROOT, 'include')}"]
+CUDA_FLAGS += os.environ.get("WSVD_EXTRA_NVCC", "").split()  # experiment switches (-D...)
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall", "-Wextra", f"-I{os.path.join(ROOT, 'include')}",
              "-I/usr/local/cuda/include"]
 

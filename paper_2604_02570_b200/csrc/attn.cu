@@ -44,6 +44,10 @@
 
 using namespace wsvd_dev;
 
+#ifndef WSVD_I8_EXP
+#define WSVD_I8_EXP 0
+#endif
+
 namespace wsvd_k {
 
 namespace {
@@ -71,7 +75,11 @@ struct Cfg {
     static constexpr int THREADS = 32 * NW + 32;  // + one producer warp
     // tokens per stage: int8 rows are half as wide, so the tensor-core int8
     // consumer takes 512-token stages (the same 32 KB per stage as bf16)
-    static constexpr int ST = IMMA ? 2 * kStageTok : kStageTok;
+    // int8 tensor-core consumers take 1024-token stages (64 KB at r = 32: fewer
+    // per-stage reductions and conversions per token) when three of them fit,
+    // else 512 (the same 32 KB per stage as bf16); V bit 5 forces 512
+    static constexpr bool BIG = IMMA && !(V & 32) && 3 * (4 * kStageTok * 2 * R + 16 * kStageTok + 256) <= 218 * 1024;
+    static constexpr int ST = IMMA ? (BIG ? 4 : 2) * kStageTok : kStageTok;
     static constexpr int GPW = ST / (16 * NW);  // 16-token groups per warp per stage
     static constexpr int ROWS = ST * ROWB;
     static constexpr int SC = (CD == I8) ? 4 * ST : 0;
@@ -507,6 +515,208 @@ WSVD_DEV void consume_mma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, ui
     }
 }
 
+// ----------------------------------------------------------------------------
+// INT8 cache, both contractions on the integer tensor cores (the default at
+// r <= 32, where 1024-token stages fit; variant bit 4 swaps it with consume_mma_i8).
+// Scores as consume_mma_i8.  P.V: per stage, p' = p.s_V is split against the
+// warp's stage maximum b into two int8 columns, p' ~ s1.h + s2.l (s1 = b/127,
+// s2 = s1/254, ~15 bits of b), and the transposed product D(16 r x 8) =
+// V^T_int8(16 r x 32 tok) . [h | l](32 tok x 8) runs on mma.m16n8k32.s8 with
+// exact int32 sums -- one MMA per 16 latent columns per 32 tokens, a quarter
+// of the f16 P.V's, and no int8 -> f16 conversion of V.  The stage's sums are
+// scaled into fp32 accumulators once.  V^T fragments are byte gathers of
+// ldmatrix.trans pairs: k = 4 t4 + i of a 16-token half is token (2t4, 2t4+1,
+// 2t4+8, 2t4+9)[i], row g8 is r = 2 g8 and row g8 + 8 is r = 2 g8 + 1; the P
+// fragment uses the same token order.
+template <class C, int R>
+WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, uint64_t* full, uint64_t* empty,
+                              int& slot, uint32_t& phase, int warp, int lane) {
+    constexpr int K32 = (R + 31) / 32;
+    constexpr int UV = R / 16;
+    constexpr int GPW = C::GPW;
+    static_assert(GPW % 2 == 0, "32-token P.V k-steps pair the warp's 16-token groups");
+    const int g8 = lane >> 2, t4 = lane & 3;
+    float m_w = -INFINITY, l = 0.f;
+    const int ns = (g.ntok + C::ST - 1) / C::ST;
+    uint32_t qf[K32][2];
+    float s1 = 1.f, s2 = 1.f;
+    float acc[UV][2];               // [unit][r = 16u + 2 g8 | 16u + 2 g8 + 1] (lanes t4 = 0)
+#pragma unroll
+    for (int u = 0; u < UV; ++u) acc[u][0] = acc[u][1] = 0.f;
+    // P fragment byte gather: x = word of lane 8 t4 (tokens 2t4, 2t4+8), y = lane
+    // 8 t4 + 4 (2t4+1, 2t4+9); words are [h(t0), h(t1), l(t0), l(t1)]
+    const uint32_t asel = (g8 == 0) ? 0x5140u : 0x7362u;
+    const int src_x = 8 * t4, src_y = 8 * t4 + 4;
+    // scores of stage sl (tokens of this warp) -> sc; -INF past the unit's end
+    auto scores = [&](int s, int sl, float (&sc)[GPW][2]) {
+        const uint8_t* sp = smem + sl * C::STAGE;
+        const uint32_t sbase = smem_u32(sp);
+        const int rows = min(C::ST, g.ntok - s * C::ST);
+        const __half2* sc2 = reinterpret_cast<const __half2*>(sp + C::ROWS);
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) {
+            const int tb = (warp * GPW + grp) * 16;
+            int d[4] = {0, 0, 0, 0};
+            const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+            for (int kk = 0; kk < K32; ++kk) {
+                uint32_t a0, a1, a2 = 0u, a3 = 0u;
+                if (kk * 32 + 16 < R) {
+                    const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
+                    ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
+                } else {
+                    const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2) * 16);
+                    ldsm_x2(sbase + cache_swz(off), a0, a1);
+                }
+#if WSVD_I8_EXP & 2
+                d[0] += lane; d[2] += a0 & 3;
+#else
+                mma_s8_16832(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+#endif
+            }
+            const int t0 = tb + g8, t1 = tb + g8 + 8;
+            const float k0 = __low2float(sc2[t0]), k1 = __low2float(sc2[t1]);
+            sc[grp][0] = (t4 == 0 && t0 < rows)
+                ? fmaf(static_cast<float>(d[0]), s1, static_cast<float>(d[1]) * s2) * k0 : -INFINITY;
+            sc[grp][1] = (t4 == 0 && t1 < rows)
+                ? fmaf(static_cast<float>(d[2]), s1, static_cast<float>(d[3]) * s2) * k1 : -INFINITY;
+        }
+    };
+    mbar_wait(&full[slot], phase);
+    {
+        const float* q = reinterpret_cast<const float*>(smem + slot * C::STAGE + C::QT_OFF);
+        float mx = 0.f;
+#pragma unroll
+        for (int k = 0; k < R; ++k) mx = fmaxf(mx, fabsf(q[k]));
+        s1 = (mx == 0.f) ? 1.f : mx / 127.f;
+        s2 = s1 / 254.f;
+#pragma unroll
+        for (int kk = 0; kk < K32; ++kk)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                uint32_t w1 = 0, w2 = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    if (kk * 32 + 16 * j >= R) break;
+                    const float v = q[kk * 32 + 16 * j + 4 * t4 + e];
+                    const float h = rintf(v / s1);
+                    const float lo = rintf((v - h * s1) / s2);
+                    w1 |= (static_cast<uint32_t>(static_cast<int32_t>(h)) & 0xffu) << (8 * e);
+                    w2 |= (static_cast<uint32_t>(static_cast<int32_t>(fminf(fmaxf(lo, -127.f), 127.f))) & 0xffu) << (8 * e);
+                }
+                qf[kk][j] = (g8 == 0) ? w1 : (g8 == 1 ? w2 : 0u);
+            }
+    }
+    float sc[GPW][2];
+    scores(0, slot, sc);
+    for (int s = 0; s < ns; ++s) {
+        // software pipeline: the next stage's score MMAs are issued before this
+        // stage's softmax and P.V, so their latencies overlap
+        const int cur = slot;
+        if (++slot == C::STAGES) {
+            slot = 0;
+            phase ^= 1u;
+        }
+        float scn[GPW][2];
+        if (s + 1 < ns) {
+            mbar_wait(&full[slot], phase);
+            scores(s + 1, slot, scn);
+        }
+        const uint8_t* sp = smem + cur * C::STAGE;
+        const uint32_t sbase = smem_u32(sp);
+        const __half2* sc2 = reinterpret_cast<const __half2*>(sp + C::ROWS);
+        float lm = -INFINITY;
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) lm = fmaxf(lm, fmaxf(sc[grp][0], sc[grp][1]));
+        if (__any_sync(0xffffffffu, lm > m_w + 8.f)) {
+            const float wm = warp_max(lm);
+            const float f = ex2(m_w - wm);
+            l *= f;
+#pragma unroll
+            for (int u = 0; u < UV; ++u) {
+                acc[u][0] *= f;
+                acc[u][1] *= f;
+            }
+            m_w = wm;
+        }
+        // p' = p . s_V and the warp's stage maximum
+        float pp[GPW][2];
+        float bm = 0.f;
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) {
+            const int tb = (warp * GPW + grp) * 16;
+            const float p0 = (sc[grp][0] == -INFINITY) ? 0.f : ex2(sc[grp][0] - m_w);
+            const float p1 = (sc[grp][1] == -INFINITY) ? 0.f : ex2(sc[grp][1] - m_w);
+            l += p0 + p1;
+            pp[grp][0] = p0 * __high2float(sc2[tb + g8]);
+            pp[grp][1] = p1 * __high2float(sc2[tb + g8 + 8]);
+            bm = fmaxf(bm, fmaxf(pp[grp][0], pp[grp][1]));
+        }
+        bm = warp_max(bm);
+        const float ps1 = bm * (1.f / 127.f), ps2 = ps1 * (1.f / 254.f);
+        const float pi1 = bm > 0.f ? __fdividef(127.f, bm) : 0.f, pi2 = pi1 * 254.f;
+        uint32_t pa[GPW];
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) {
+            const int h0 = __float2int_rn(pp[grp][0] * pi1), h1 = __float2int_rn(pp[grp][1] * pi1);
+            const int l0 = max(-127, min(127, __float2int_rn(fmaf(static_cast<float>(-h0), ps1, pp[grp][0]) * pi2)));
+            const int l1 = max(-127, min(127, __float2int_rn(fmaf(static_cast<float>(-h1), ps1, pp[grp][1]) * pi2)));
+            const uint32_t w = (static_cast<uint32_t>(h0) & 0xffu) | ((static_cast<uint32_t>(h1) & 0xffu) << 8) |
+                               ((static_cast<uint32_t>(l0) & 0xffu) << 16) | (static_cast<uint32_t>(l1) << 24);
+            const uint32_t x = __shfl_sync(0xffffffffu, w, src_x), y = __shfl_sync(0xffffffffu, w, src_y);
+            pa[grp] = (g8 < 2) ? __byte_perm(x, y, asel) : 0u;
+        }
+        // P.V transposed: D(16 r x 8) = V^T(16 r x 32 tok) . [h | l](32 tok x 8),
+        // one MMA per 16-byte unit per 32 tokens; row g8 of the unit is r = 2 g8,
+        // row g8 + 8 is r = 2 g8 + 1; lane (g8, t4 = 0) gets (h, l) sums of both
+        int dI[UV][4];
+#pragma unroll
+        for (int u = 0; u < UV; ++u) dI[u][0] = dI[u][1] = dI[u][2] = dI[u][3] = 0;
+#if WSVD_I8_EXP & 1
+        dI[0][0] = pa[0] ^ pa[GPW - 1];
+        if (false)
+#endif
+#pragma unroll
+        for (int j = 0; j < GPW / 2; ++j) {
+            const int tb = (warp * GPW + 2 * j) * 16;
+            const int vtok = tb + (lane & 7) + (lane >> 3) * 8;  // matrices: tokens 0-7, 8-15, 16-23, 24-31
+#pragma unroll
+            for (int u = 0; u < UV; ++u) {
+                uint32_t m0, m1, m2, m3;
+                const uint32_t off = static_cast<uint32_t>(vtok * C::ROWB + C::PART + u * 16);
+                ldsm_x4_trans(sbase + cache_swz(off), m0, m1, m2, m3);
+                mma_s8_16832(dI[u], __byte_perm(m0, m1, 0x6420), __byte_perm(m0, m1, 0x7531),
+                             __byte_perm(m2, m3, 0x6420), __byte_perm(m2, m3, 0x7531), pa[2 * j], pa[2 * j + 1]);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UV; ++u) {
+            acc[u][0] = fmaf(static_cast<float>(dI[u][0]), ps1, fmaf(static_cast<float>(dI[u][1]), ps2, acc[u][0]));
+            acc[u][1] = fmaf(static_cast<float>(dI[u][2]), ps1, fmaf(static_cast<float>(dI[u][3]), ps2, acc[u][1]));
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[cur]);
+#pragma unroll
+        for (int grp = 0; grp < GPW; ++grp) {
+            sc[grp][0] = scn[grp][0];
+            sc[grp][1] = scn[grp][1];
+        }
+    }
+    const float lsum = warp_sum(l);
+    float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kMaxWarps + warp) * (R + 2);
+    if (t4 == 0) {
+#pragma unroll
+        for (int u = 0; u < UV; ++u) {
+            wsp[16 * u + 2 * g8] = acc[u][0];
+            wsp[16 * u + 2 * g8 + 1] = acc[u][1];
+        }
+    }
+    if (lane == 0) {
+        wsp[R] = m_w;
+        wsp[R + 1] = lsum;
+    }
+}
+
 template <int CD, int R, int V>
 __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(const AttnArgs a) {
     using C = Cfg<CD, R, V>;
@@ -601,6 +811,10 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
             }
         } else if constexpr (C::MMA) {
             consume_mma<C, R, (V & 1)>(a, g, smem, full, empty, slot, phase, warp, lane);
+        } else if constexpr (C::IMMA && (C::BIG != static_cast<bool>(V & 16))) {
+            // int8 P.V on the int8 tensor cores where 1024-token stages fit (r <= 32),
+            // else (measured faster at r = 48) the f16 P.V; bit 4 swaps them
+            consume_imma_i8<C, R>(a, g, smem, full, empty, slot, phase, warp, lane);
         } else if constexpr (C::IMMA) {
             consume_mma_i8<C, R>(a, g, smem, full, empty, slot, phase, warp, lane);
         } else {
@@ -818,7 +1032,7 @@ cudaError_t launch_v(const AttnArgs& a, cudaStream_t s) {
 int attn_variant() {
     static const int v = [] {
         const char* e = std::getenv("WSVD_ATTN_VARIANT");
-        return e ? (std::atoi(e) & 15) : kDefaultVariant;
+        return e ? (std::atoi(e) & 63) : kDefaultVariant;
     }();
     return v;
 }
@@ -829,7 +1043,14 @@ cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
         // WSVD_ATTN_VARIANT bit 3: the CUDA-core int8 consumer; bit 1: 16 consumer warps (A/B)
         if (attn_variant() & 8) return launch_v<CD, R, 8>(a, s);
         if (attn_variant() & 4) return launch_v<CD, R, 4>(a, s);  // streaming probe (no compute)
-        return (attn_variant() & 2) ? launch_v<CD, R, 2>(a, s) : launch_v<CD, R, 0>(a, s);
+        // bit 4: the f16 P.V consumer (consume_mma_i8); bit 5: 512-token stages
+        switch (attn_variant() & 50) {
+            case 0: return launch_v<CD, R, 0>(a, s);
+            case 2: return launch_v<CD, R, 2>(a, s);
+            case 16: return launch_v<CD, R, 16>(a, s);
+            case 32: return launch_v<CD, R, 32>(a, s);
+            default: return launch_v<CD, R, 18>(a, s);
+        }
     } else if constexpr (CD != BF16) {
         return launch_v<CD, R, 0>(a, s);
     } else {

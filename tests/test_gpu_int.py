@@ -8,6 +8,9 @@ q_h and the attention outputs (fp32 arithmetic on dequantised values)."""
 from __future__ import annotations
 
 import math
+import os
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -17,6 +20,7 @@ from oracle import oracle as O
 from tests.helpers import REL_TOL, rel_err_rows, to_factors
 
 pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 torch = pytest.importorskip("torch")
 
 
@@ -155,3 +159,56 @@ def test_layer_step_int8_matches_append_plus_attend():
     assert rel_err_rows(attn.cpu().numpy(), out.cpu().numpy()) <= REL_TOL
     y_ref = out.cpu().numpy().reshape(B, -1).astype(np.float64) @ w_o
     assert np.abs(y.cpu().numpy() - y_ref).max() <= 1e-2 * np.abs(y_ref).max()
+
+
+@pytest.mark.parametrize("r,L,chunk,variant", [
+    (32, 2500, None, None),     # 1024-token stages (int8 P.V on the int8 tensor cores), ragged tail
+    (32, 4100, "1024", None),   # one stage per chunk, a 4-token last chunk
+    (32, 3000, None, "16"),     # the f16 P.V consumer on 1024-token stages
+    (32, 2100, None, "32"),     # int8 P.V on 512-token stages
+    (48, 1800, None, None),     # r = 48: half k-step scores, 512-token stages
+    (16, 3000, None, None),
+])
+def test_int8_cache_attention_long_context(monkeypatch, r, L, chunk, variant):
+    """INT8-cache attention over multi-stage contexts (the short-context cases
+    above fit in one stage) against the oracle's fused_decode_step on the
+    dequantised cache rows read back from the device."""
+    if variant is not None and os.environ.get("WSVD_ATTN_VARIANT") != variant:
+        # the variant switch is read once per process: run this case in a child
+        env = dict(os.environ, WSVD_ATTN_VARIANT=variant)
+        node = f"{__file__}::test_int8_cache_attention_long_context[{r}-{L}-{chunk}-{variant}]"
+        res = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider", node],
+                             env=env, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+        return
+    if chunk is not None:
+        monkeypatch.setenv("WSVD_ATTN_CHUNK", chunk)
+    from paper_2604_02570_b200.layer import DecodeLayer
+    E, nh, H, B = 256, 4, 128, 2
+    rng = O.Rng(4000 + r + L)
+    lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
+    quant, deq_b = quant_layer(lay, 8)
+    layer = DecodeLayer(to_factors(lay), None, batch=B, capacity=L + 8, cache_dtype="i8", weight_dtype="i8",
+                        quantized=quant)
+    R = layer.rpad
+    dev = torch.device("cuda", 0)
+    layer.fill_synthetic(L - 1, seed=r + L)
+    x = torch.from_numpy(rng.normal_matrix(B, E).astype(np.float32)).to(dev)
+    q = torch.empty((B, nh, H), device=dev)
+    layer.append(x, q)
+    out = torch.empty((B, nh, H), device=dev)
+    layer.attend(q, out)
+    torch.cuda.synchronize()
+    q_dev, out = q.cpu().numpy().astype(np.float64), out.cpu().numpy().astype(np.float64)
+    deq = O.Layer(lay.A, deq_b, lay.ranks)
+    for b in range(B):
+        ck, cv = np.zeros((nh, L, r)), np.zeros((nh, L, r))
+        for h in range(nh):
+            rows, scales = layer.read_raw(b, h)
+            rows = rows.view(np.int8).astype(np.float64)
+            sk = np.array([O.f16_to_f32(s) for s in scales[:, 0]], dtype=np.float64)
+            sv = np.array([O.f16_to_f32(s) for s in scales[:, 1]], dtype=np.float64)
+            ck[h] = rows[:, :r] * sk[:, None]
+            cv[h] = rows[:, R:R + r] * sv[:, None]
+        ref = O.fused_decode_step(deq, ck, cv, L, q_dev[b], 32)
+        assert rel_err_rows(out[b], ref) <= REL_TOL, f"b={b}"
