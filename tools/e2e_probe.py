@@ -15,7 +15,7 @@ from paper_2604_02570_b200.layer import DecodeLayer  # noqa: E402
 cfg = bench.CONFIGS[bench.DEFAULT_CONFIG]
 E, B, L = cfg["E"], cfg["B"], cfg["L"]
 f, w_o = bench.synthetic_layer(cfg)
-layer = DecodeLayer(f, w_o, batch=B, capacity=L + 200, cache_dtype="bf16", weight_dtype="bf16")
+layer = DecodeLayer(f, w_o, batch=B, capacity=L + 600, cache_dtype="bf16", weight_dtype="bf16")
 dev = torch.device("cuda", 0)
 for t0 in range(0, L - 1, 256):
     layer.prefill(torch.randn((min(256, L - 1 - t0), B, E), device=dev))
@@ -61,3 +61,23 @@ t = time.perf_counter()
 for _ in range(40):
     torch.cuda.synchronize()
 print(f"empty sync: {(time.perf_counter() - t) / 40 * 1e6:.1f} us")
+# device time of the zero-copy host step (events on the layer's stream around the call)
+s = torch.cuda.current_stream()
+e0.record(s)
+for _ in range(40):
+    layer.step_host(xn, yn)
+e1.record(s)
+torch.cuda.synchronize()
+print(f"step_host device span: {e0.elapsed_time(e1) / 40 * 1e3:.1f} us/step")
+# tiny kernel + sync wall: the launch / wake-up floor
+t = time.perf_counter()
+for _ in range(40):
+    x.add_(0.0)
+    torch.cuda.synchronize()
+print(f"tiny kernel + sync: {(time.perf_counter() - t) / 40 * 1e6:.1f} us")
+import ctypes  # noqa: E402
+from paper_2604_02570_b200 import _native as N  # noqa: E402
+t = time.perf_counter()
+for _ in range(1000):
+    N.lib().wsvd_last_error()
+print(f"python->ctypes call: {(time.perf_counter() - t) / 1000 * 1e6:.2f} us")

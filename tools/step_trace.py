@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--per-sm", action="store_true")
     ap.add_argument("--attn-only", action="store_true")
     ap.add_argument("--proj-only", action="store_true")
+    ap.add_argument("--host", action="store_true", help="steps through wsvd_layer_step_host (pinned x / y)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     E, B, L = cfg["E"], cfg["B"], cfg["L"]
@@ -41,8 +42,12 @@ def main():
         layer.prefill(torch.randn((n, B, E), generator=g, device=dev))
     x = torch.randn((B, E), generator=g, device=dev)
     y = torch.empty((B, E), device=dev)
+    xh, yh = x.cpu().pin_memory(), torch.empty((B, E)).pin_memory()
     for _ in range(args.steps):
-        layer.step(x, y, graph=False)
+        if args.host:
+            layer.step_host(xh.numpy(), yh.numpy())
+        else:
+            layer.step(x, y, graph=False)
     torch.cuda.synchronize()
     raw = layer.debug_copy("trace").astype(np.int64)
     t, smid, nu = raw[:, :10], raw[:, 10], raw[:, 11]
