@@ -833,9 +833,13 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     c->sms = p.multiProcessorCount;
     c->grid = c->sms * attn_occupancy(cache_dtype, L->R);
     // split-KV: each (sequence, head) is cut into up to max_chunks equal chunks
-    // per launch (attn.cu chunking()), ~12 units per persistent CTA
+    // per launch (attn.cu chunking()), about one unit per persistent CTA when
+    // the (sequence, head) pairs alone do not fill the grid
     c->chunk = 0;
-    int units = 4;  // target units per persistent CTA (measured best: 2 chunks at B16 ctx4K)
+    // target units per CTA; measured (tools/timing.py, attention + combine):
+    // B1 ctx2K fp32 12.3 us at 1 against 26.9 at 4; B16 ctx4K bf16 and the
+    // int8 configs within 1 us of each other
+    int units = 1;
     if (const char* env = getenv("WSVD_ATTN_UNITS")) units = std::max(1, atoi(env));
     c->max_chunks = std::max(1, std::min(64, (units * c->grid + batch * nh - 1) / (batch * nh)));
     if (const char* env = getenv("WSVD_ATTN_CHUNK")) {  // fixed chunk length (tests)
