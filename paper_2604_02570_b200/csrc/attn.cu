@@ -44,10 +44,6 @@
 
 using namespace wsvd_dev;
 
-#ifndef WSVD_I8_EXP
-#define WSVD_I8_EXP 0
-#endif
-
 namespace wsvd_k {
 
 namespace {
@@ -568,11 +564,7 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
                     const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2) * 16);
                     ldsm_x2(sbase + cache_swz(off), a0, a1);
                 }
-#if WSVD_I8_EXP & 2
-                d[0] += lane; d[2] += a0 & 3;
-#else
                 mma_s8_16832(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
-#endif
             }
             const int t0 = tb + g8, t1 = tb + g8 + 8;
             const float k0 = __low2float(sc2[t0]), k1 = __low2float(sc2[t1]);
@@ -672,10 +664,6 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
         int dI[UV][4];
 #pragma unroll
         for (int u = 0; u < UV; ++u) dI[u][0] = dI[u][1] = dI[u][2] = dI[u][3] = 0;
-#if WSVD_I8_EXP & 1
-        dI[0][0] = pa[0] ^ pa[GPW - 1];
-        if (false)
-#endif
 #pragma unroll
         for (int j = 0; j < GPW / 2; ++j) {
             const int tb = (warp * GPW + 2 * j) * 16;

@@ -104,9 +104,10 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(OUT, exist_ok=True)
     summarize_launches(tag)
-    for name in ("step_full", "attn_full", "tc_full", "gemm_full"):
+    for name in ("step_full", "attn_full", "tc_full", "gemm_full", "i8_full", "f32rows_full"):
         summarize_full(name, tag)
-    for f in ("bench.json", "bench_ref.json", "timing.txt", "gpu.txt", "step_trace.txt"):
+    for f in ("bench.json", "bench_ref.json", "timing.txt", "gpu.txt", "step_trace.txt", "bench_config3.json",
+              "bench_config1.json", "timing_config3.txt", "timing_config1.txt"):
         src = os.path.join(RAW, f)
         if os.path.exists(src):
             with open(src) as a, open(os.path.join(OUT, f"{tag}_{f}"), "w") as b:
