@@ -68,7 +68,7 @@ struct Cfg {
     // tensor-core consumers: 16 warps x one 16-token group per stage (latency
     // hiding: 4 warps per SM sub-partition); CUDA-core consumers: one token per thread
     static constexpr int NW = ((MMA || IMMA) && (V & 2)) ? 16 : 8;
-    static constexpr int THREADS = 32 * NW + 32;  // + one producer warp
+    static constexpr int THREADS = 32 * NW + 64;  // + one producer warp + one merge (helper) warp
     // tokens per stage: int8 rows are half as wide, so the tensor-core int8
     // consumer takes 512-token stages (the same 32 KB per stage as bf16)
     // int8 tensor-core consumers take 1024-token stages (64 KB at r = 32: fewer
@@ -705,6 +705,46 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
     }
 }
 
+// One chunk per (sequence, head) -- max_chunks == 1, no fixed chunk length --
+// means one CTA holds every partial of a unit, so the attention kernel merges
+// them itself and the combine launch is skipped.  Latent outputs only (the
+// layer step): the operator API's B_V up-projection stays in the combine
+// kernel, whose 128 threads per head do it in parallel (one warp inside the
+// attention kernel measured 4x slower for the whole launch).
+__host__ __device__ inline bool attn_finalizes(const AttnArgs& a) {
+    return a.chunk == 0 && a.max_chunks == 1 && a.out == nullptr && !a.no_finalize;
+}
+
+// Merge of one unit's nw warp partials (fixed warp order, SoftmaxState::merge,
+// decode.cpp:59-75) by one warp into the latent output -- the combine kernel's
+// work for a single chunk.  The partials were written by this CTA's warps
+// before a CTA barrier.
+template <int R>
+WSVD_DEV void finalize_unit(const AttnArgs& a, int bh, int nw, int lane) {
+    constexpr int RI = (R + 31) / 32;  // latent columns per lane
+    const float* wsb = a.ws + static_cast<size_t>(bh) * a.max_chunks * kMaxWarps * (R + 2);
+    float M = -INFINITY;
+    for (int w = 0; w < nw; ++w) M = fmaxf(M, wsb[w * (R + 2) + R]);
+    float L = 0.f, acc[RI];
+#pragma unroll
+    for (int i = 0; i < RI; ++i) acc[i] = 0.f;
+    for (int w = 0; w < nw; ++w) {
+        const float m = wsb[w * (R + 2) + R];
+        if (m == -INFINITY) continue;  // a warp that saw no token
+        const float f = ex2(m - M);
+        L = fmaf(wsb[w * (R + 2) + R + 1], f, L);
+#pragma unroll
+        for (int i = 0; i < RI; ++i)
+            if (lane + 32 * i < R) acc[i] = fmaf(wsb[w * (R + 2) + lane + 32 * i], f, acc[i]);
+    }
+    float vt[RI];
+#pragma unroll
+    for (int i = 0; i < RI; ++i) {
+        vt[i] = acc[i] / L;
+        if (a.vlat && lane + 32 * i < R) a.vlat[static_cast<size_t>(bh) * R + lane + 32 * i] = vt[i];
+    }
+}
+
 template <int CD, int R, int V>
 __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(const AttnArgs a) {
     using C = Cfg<CD, R, V>;
@@ -713,6 +753,9 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     uint64_t* empty = full + C::STAGES;
     float* red = reinterpret_cast<float*>(smem + C::RED_OFF);
+    // in-kernel merge (attn_finalizes): unit slots between the consumers and
+    // the helper warp, 16 units deep
+    __shared__ uint64_t ufull[16], uempty[16];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const size_t cap = static_cast<size_t>(a.cap);
@@ -727,6 +770,10 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
         for (int i = 0; i < C::STAGES; ++i) {
             mbar_init(&full[i], 1);
             mbar_init(&empty[i], C::NW);
+        }
+        for (int i = 0; i < 16; ++i) {
+            mbar_init(&ufull[i], C::NW);
+            mbar_init(&uempty[i], 1);
         }
         fence_mbar_init();
     }
@@ -769,6 +816,25 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
                         slot = 0;
                         phase ^= 1u;
                     }
+                }
+            }
+        }
+        return;
+    }
+
+    // ========================================================= helper warp
+    // merges each unit's warp partials as the consumers publish them (off the
+    // consumers' path: a merge costs ~2 L2 round trips)
+    if (warp == C::NW + 1) {
+        if constexpr (!(V & 4)) {
+            if (attn_finalizes(a)) {
+                int jl = 0;
+                for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++jl) {
+                    const int us = jl & 15;
+                    mbar_wait(&ufull[us], static_cast<uint32_t>(jl >> 4) & 1u);
+                    finalize_unit<R>(a, unit_geom(u, nch, chunk, len).bh, C::NW, lane);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&uempty[us]);
                 }
             }
         }
@@ -893,7 +959,19 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
             }
             __syncwarp();  // scratch reuse by the next unit
         }
-        // each warp published its own partial (m, l, acc[R]); no CTA-wide sync
+        // each warp published its own partial (m, l, acc[R])
+        if constexpr (!(V & 4)) {
+            if (attn_finalizes(a)) {
+                // hand unit g to the helper warp (its slot must be free: the
+                // helper has merged the unit 16 before)
+                __syncwarp();
+                if (lane == 0) {
+                    const int jl = (u - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x);
+                    mbar_wait(&uempty[jl & 15], (static_cast<uint32_t>(jl >> 4) & 1u) ^ 1u);
+                    mbar_arrive(&ufull[jl & 15]);
+                }
+            }
+        }
     }
 }
 
@@ -1005,6 +1083,7 @@ cudaError_t launch_v(const AttnArgs& a, cudaStream_t s) {
         }
         cudaError_t e = launch_pdl(k, dim3(a.grid), dim3(C::THREADS), C::SMEM, s, a);
         if (e != cudaSuccess) return e;
+        if (attn_finalizes(a) && !(V & 4)) return cudaSuccess;  // merged in the kernel
         const int csmem = combine_smem(a.max_chunks, C::NW, R);
         if (csmem > g_combine_smem_attr) {  // one (non-template) kernel: track its attribute globally
             e = cudaFuncSetAttribute(attn_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem);

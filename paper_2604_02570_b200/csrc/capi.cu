@@ -429,6 +429,8 @@ int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStr
     a.cdtype = c->cdtype;
     a.row_bytes = c->row_bytes;
     a.grid = c->grid;
+    static const bool no_fin = getenv("WSVD_ATTN_COMBINE") != nullptr;
+    a.no_finalize = no_fin ? 1 : 0;
     if (c->attn_mode == WSVD_ATTN_EXPLICIT_TC) {
         // explicit key reconstruction on tcgen05 (attn_tc.cu), then the combine
         int rc = ensure_bkt(L);

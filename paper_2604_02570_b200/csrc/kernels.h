@@ -100,6 +100,7 @@ struct AttnArgs {
     int len_add;            // 1 when the step's own row is appended but not yet committed
     int B, nh, H, R, cap, chunk, max_chunks, cdtype, row_bytes;
     int grid;               // persistent CTAs
+    int no_finalize;        // A/B switch: always merge in the combine kernel (WSVD_ATTN_COMBINE=1)
     // explicit key reconstruction (attn_tc.cu): per-head B_K^T tiles and the query
     const uint8_t* bkt;     // [nh][attn_tc_btile_bytes()] bf16, MMA B-operand layout
     const float* q;         // [B][nh][H] query rows

@@ -212,3 +212,40 @@ def test_int8_cache_attention_long_context(monkeypatch, r, L, chunk, variant):
             cv[h] = rows[:, R:R + r] * sv[:, None]
         ref = O.fused_decode_step(deq, ck, cv, L, q_dev[b], 32)
         assert rel_err_rows(out[b], ref) <= REL_TOL, f"b={b}"
+
+
+@pytest.mark.parametrize("cache", ["i8", "f32"])
+def test_layer_step_single_chunk_in_kernel_merge(cache):
+    """With at least one (sequence, head) pair per CTA the split-KV attention
+    uses one chunk per pair and its helper warp merges the warp partials in the
+    kernel (no combine launch): the layer step's y must equal append + attend
+    (combine kernel, full-rank output) followed by the O-projection."""
+    from paper_2604_02570_b200.layer import DecodeLayer
+    rng = O.Rng(91)
+    E, nh, r, H, B, L = 512, 32, 32, 128, 5, 300   # 160 pairs >= 148 CTAs -> max_chunks 1
+    lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
+    f = to_factors(lay)
+    w_o = O.bf16_round(rng.normal_matrix(nh * H, E, 1.0 / np.sqrt(nh * H)))
+    kw = dict(batch=B, capacity=L + 8, cache_dtype=cache)
+    if cache == "i8":
+        quant, _ = quant_layer(lay, 8)
+        kw.update(weight_dtype="i8", quantized=quant)
+    else:
+        kw.update(weight_dtype="f32")
+    a = DecodeLayer(f, w_o, **kw)
+    b_ = DecodeLayer(f, w_o, **kw)
+    dev = torch.device("cuda", 0)
+    toks = rng.normal_matrix(L * B, E).reshape(L, B, E).astype(np.float32)
+    pre = torch.from_numpy(toks[:L - 1]).to(dev)
+    a.prefill(pre)
+    b_.prefill(pre)
+    x = torch.from_numpy(toks[-1]).to(dev)
+    y = torch.empty((B, E), device=dev)
+    a.step(x, y, graph=False)
+    q = torch.empty((B, nh, H), device=dev)
+    b_.append(x, q)
+    out = torch.empty((B, nh, H), device=dev)
+    b_.attend(q, out)
+    torch.cuda.synchronize()
+    y_ref = out.cpu().numpy().reshape(B, -1).astype(np.float64) @ w_o
+    assert np.abs(y.cpu().numpy() - y_ref).max() <= 1e-2 * np.abs(y_ref).max()
