@@ -204,6 +204,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     uint64_t* uready = emptyB + C::NB;  // [kMaxU] unit j's query / new row prepared (helper)
     uint64_t* sfull = uready + kMaxU;   // [kMaxU] unit j's warp states written (consumers)
     uint64_t* p3bar = sfull + kMaxU;    // P3: chunk states landed (one phase per staged split)
+    uint64_t* wfull = p3bar + 1;        // [2*NB] projection items parked in the attention ring
+    uint64_t* wdone = wfull + 2 * C::NB;  // [NB] those items consumed: the stage is free
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -214,6 +216,27 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[cta * 12 + 10] = smid;
     }
+    const int splits = a.Kp / kKS;
+    const int cps = G / splits;  // CTAs per projection split
+    const int ps = cta % splits, pj = cta / splits;
+    const int ptiles = a.Nrows / 16;
+    const int plo = pj < cps ? static_cast<int>(static_cast<long>(pj) * ptiles / cps) : 0;
+    const int phi = pj < cps ? static_cast<int>(static_cast<long>(pj + 1) * ptiles / cps) : 0;
+    const int np1 = phi - plo;
+    const int osplits = a.oKp / kKS;
+    // P3: this CTA owns output tiles cta + i*G with all their K splits (items
+    // (tile, split) in that order), so it sums the splits itself: y is written
+    // with plain stores, once (it may live in mapped host memory)
+    const int nt3 = cta < a.otiles ? (a.otiles - 1 - cta) / G + 1 : 0;
+    const int np3 = nt3 * osplits;  // <= kNA (host-checked)
+    // Projection items beyond the 4-slot weight ring are parked in the
+    // attention ring (2 per stage, in consumption order): the attention cannot
+    // start before grid barrier 1 anyway, and with every item in flight at
+    // once P1 costs one memory round trip instead of one per ring turn.
+    // Ring-A sequence: P1 items k < 4 or k >= 4 + nBH, then the P3 items.
+    const int nBH = min(max(np1 - kNA, 0), 2 * C::NB);
+    const int nA1 = np1 - nBH;
+    const int nWS = (nBH + 1) / 2;  // attention stages holding parked items (the first nWS)
     // prologue (overlaps the predecessor under PDL): rows past a stage's valid
     // end are read by the MMAs (times p = 0) and must be finite
     for (int i = tid; i < C::NB * C::STAGE / 16; i += kThr)
@@ -233,34 +256,38 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
             mbar_init(&sfull[i], kNW);
         }
         mbar_init(p3bar, 1);
+        for (int b = 0; b < nBH; ++b) mbar_init(&wfull[b], 1);
+        for (int st = 0; st < C::NB; ++st)  // stage st parks items 4+2st and 4+2st+1
+            mbar_init(&wdone[st], st < nWS ? min(2, nBH - 2 * st) : 1);
         fence_mbar_init();
     }
     __syncthreads();
-    const int splits = a.Kp / kKS;
-    const int cps = G / splits;  // CTAs per projection split
-    const int ps = cta % splits, pj = cta / splits;
-    const int ptiles = a.Nrows / 16;
-    const int plo = pj < cps ? static_cast<int>(static_cast<long>(pj) * ptiles / cps) : 0;
-    const int phi = pj < cps ? static_cast<int>(static_cast<long>(pj + 1) * ptiles / cps) : 0;
-    const int np1 = phi - plo;
-    const int osplits = a.oKp / kKS;
-    // P3: this CTA owns output tiles cta + i*G with all their K splits (items
-    // (tile, split) in that order), so it sums the splits itself: y is written
-    // with plain stores, once (it may live in mapped host memory)
-    const int nt3 = cta < a.otiles ? (a.otiles - 1 - cta) / G + 1 : 0;
-    const int np3 = nt3 * osplits;  // <= kNA (host-checked)
     // The weights (projection W-tiles, then the folded O-projection) are
     // constant across steps: the producer starts streaming them before the
     // predecessor has drained (programmatic dependent launch), only the token,
     // the length and the cache rows wait for it
+    // ring-A item ia -> source (P1 item k(ia), then the P3 items)
+    auto a_src = [&](int ia) -> const uint8_t* {
+        if (ia < nA1) {
+            const int k = ia < kNA ? ia : ia + nBH;
+            return a.A + (static_cast<size_t>(plo + k) * splits + ps) * kItem;
+        }
+        const int j = ia - nA1;
+        return a.Wo + (static_cast<size_t>(cta + (j / osplits) * G) * osplits + j % osplits) * kItem;
+    };
+    auto parked = [&](int b) -> uint8_t* {  // parked item b (P1 item 4 + b)
+        return ringB + (b / 2) * C::STAGE + (b & 1) * kItem;
+    };
     int ia_pre = 0;
     if (warp == kNW && lane == 0) {
-        for (; ia_pre < kNA && ia_pre < np1 + np3; ++ia_pre) {
+        for (; ia_pre < kNA && ia_pre < nA1 + np3; ++ia_pre) {
             mbar_arrive_expect_tx(&fullA[ia_pre], kItem);
-            const uint8_t* src = ia_pre < np1
-                ? a.A + (static_cast<size_t>(plo + ia_pre) * splits + ps) * kItem
-                : a.Wo + (static_cast<size_t>(cta + ((ia_pre - np1) / osplits) * G) * osplits + (ia_pre - np1) % osplits) * kItem;
-            tma_bulk_g2s(ringA + ia_pre * kItem, src, kItem, &fullA[ia_pre]);
+            tma_bulk_g2s(ringA + ia_pre * kItem, a_src(ia_pre), kItem, &fullA[ia_pre]);
+        }
+        for (int b = 0; b < nBH; ++b) {
+            mbar_arrive_expect_tx(&wfull[b], kItem);
+            tma_bulk_g2s(parked(b), a.A + (static_cast<size_t>(plo + kNA + b) * splits + ps) * kItem, kItem,
+                         &wfull[b]);
         }
     }
     griddep_wait();
@@ -283,16 +310,13 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
             int ia = ia_pre;  // the first weight items went out before griddep_wait
-            const int na = np1 + np3;
+            const int na = nA1 + np3;
             auto issue_a = [&]() {
                 const int slot = ia % kNA;
                 const uint32_t ph = static_cast<uint32_t>(ia / kNA) & 1u;
                 mbar_wait(&emptyA[slot], ph ^ 1u);
                 mbar_arrive_expect_tx(&fullA[slot], kItem);
-                const uint8_t* src = ia < np1
-                    ? a.A + (static_cast<size_t>(plo + ia) * splits + ps) * kItem
-                    : a.Wo + (static_cast<size_t>(cta + ((ia - np1) / osplits) * G) * osplits + (ia - np1) % osplits) * kItem;
-                tma_bulk_g2s(ringA + slot * kItem, src, kItem, &fullA[slot]);
+                tma_bulk_g2s(ringA + slot * kItem, a_src(ia), kItem, &fullA[slot]);
                 ++ia;
             };
             int u = cta, st = 0, ib = 0;
@@ -304,6 +328,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 const uint32_t rbytes = static_cast<uint32_t>(min(C::STAGE, ((rows * C::ROWB + 1023) / 1024) * 1024));
                 const int slot = ib % C::NB;
                 const uint32_t ph = static_cast<uint32_t>(ib / C::NB) & 1u;
+                if (ib < nWS) mbar_wait(&wdone[slot], 0u);  // its parked projection items are consumed
                 mbar_wait(&emptyB[slot], ph ^ 1u);
                 mbar_arrive_expect_tx(&fullB[slot], rbytes);
                 const uint8_t* src = a.cache + (static_cast<size_t>(bh) * cap + t0) * C::ROWB + static_cast<size_t>(st) * C::STAGE;
@@ -315,10 +340,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 }
                 return true;
             };
-            while (ia < na && ia < kNA) issue_a();            // fill the weight ring
-            for (int k = 0; k < C::NB && issue_b(); ++k) {}   // and the attention ring
-            while (ia < na) issue_a();                        // projection rest, O-proj weights
-            while (issue_b()) {}                              // cache stream
+            while (ia < na) issue_a();  // projection rest, O-proj weights (as the weight ring frees)
+            while (issue_b()) {}        // cache stream; stages with parked items wait for them first
         }
         return;
     }
@@ -357,14 +380,26 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid);
         named_bar_sync(2, 32 * kNW);
         if (warp < kNA) {
-            // weight-ring slot s is always consumed by warp s (items k = s mod kNA)
-            for (int k = warp; k < np1; k += kNA) {
-                const int slot = k % kNA;
-                mbar_wait(&fullA[slot], static_cast<uint32_t>(k / kNA) & 1u);
+            // items k = warp mod kNA: the ones parked in the attention ring first
+            // (their stages then refill with cache rows during the rest of P1),
+            // the weight ring's last
+            for (int kk = warp + kNA; kk < np1 + kNA; kk += kNA) {
+                const int k = kk < np1 ? kk : warp;
+                if (k >= np1) break;
                 float facc[MT][2][4];
-                item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(xbuf), lane, facc);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyA[slot]);
+                if (k >= kNA && k < kNA + nBH) {
+                    const int b = k - kNA;
+                    mbar_wait(&wfull[b], 0u);
+                    item_mma<MT>(smem_u32(parked(b)), smem_u32(xbuf), lane, facc);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&wdone[b / 2]);
+                } else {
+                    const int ia = k < kNA ? k : k - nBH, slot = ia % kNA;
+                    mbar_wait(&fullA[slot], static_cast<uint32_t>(ia / kNA) & 1u);
+                    item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(xbuf), lane, facc);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&emptyA[slot]);
+                }
                 const int tile = plo + k;
                 float* P = a.P + static_cast<size_t>(ps) * a.B * a.Nrows;
 #pragma unroll
@@ -389,7 +424,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
 #pragma unroll
         for (int jj = 0; jj < R; ++jj) mq0[jj] = __ldg(mq + jj * R);
     }
-    STEP_MARK(2);
+    named_bar_sync(1, kSync);
+    STEP_MARK(2);  // every P1 warp of this CTA is done
     grid_sync(a.bar, (2u * epoch + 1u) * G);  // consumers + helper
     STEP_MARK(3);
 
@@ -668,7 +704,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     // shared memory, then the splits are summed in split order
     float* part = reinterpret_cast<float*>(ringB + osplits * C::XB);  // [np3][16 rows][MT*16 tokens]
     for (int j = 0; j < np3; ++j) {
-        const int k = np1 + j, slot = k % kNA;
+        const int k = nA1 + j, slot = k % kNA;
         if (slot != warp) continue;
         mbar_wait(&fullA[slot], static_cast<uint32_t>(k / kNA) & 1u);
         const int s = j % osplits;
