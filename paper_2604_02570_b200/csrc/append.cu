@@ -247,14 +247,22 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
                 hs = __float2half_rn(1.f);
                 s = 1.f;
             }
-            for (int i = lane; i < R; i += 32)
-                reinterpret_cast<int8_t*>(region)[cache_swz(row0 + warp * R + i)] =
-                    static_cast<int8_t>(fminf(fmaxf(roundf(__fdiv_rn(src[i], s)), -127.f), 127.f));
+            // four values per lane and one 32-bit store (R % 4 == 0; the 16-byte
+            // swizzle keeps 4-byte groups contiguous): no byte-store tail
+            for (int i = 4 * lane; i < R; i += 128) {
+                uint32_t w = 0;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const int8_t q = static_cast<int8_t>(fminf(fmaxf(roundf(__fdiv_rn(src[i + e], s)), -127.f), 127.f));
+                    w |= static_cast<uint32_t>(static_cast<uint8_t>(q)) << (8 * e);
+                }
+                *reinterpret_cast<uint32_t*>(region + cache_swz(row0 + warp * R + i)) = w;
+            }
             if (lane == 0) reinterpret_cast<__half*>(a.cscale + bh * a.cap + pos)[warp] = hs;
         }
     } else if (a.cdtype == BF16) {
-        for (int i = threadIdx.x; i < 2 * R; i += kEpThreads)
-            *reinterpret_cast<__nv_bfloat16*>(region + cache_swz(row0 + 2 * i)) = __float2bfloat16_rn(c[R + i]);
+        for (int i = 2 * threadIdx.x; i < 2 * R; i += 2 * kEpThreads)  // two values per 32-bit store
+            *reinterpret_cast<uint32_t*>(region + cache_swz(row0 + 2 * i)) = pack_bf16x2(c[R + i], c[R + i + 1]);
     } else {
         for (int i = threadIdx.x; i < 2 * R; i += kEpThreads)
             *reinterpret_cast<float*>(region + cache_swz(row0 + 4 * i)) = c[R + i];

@@ -22,6 +22,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
     ap.add_argument("--reps", type=int, default=20)
+    ap.add_argument("--synthetic", action="store_true",
+                    help="fill the cache with synthetic rows instead of a prefill (no prefill launches)")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     E, H, B, L = cfg["E"], cfg["H"], cfg["B"], cfg["L"]
@@ -32,9 +34,12 @@ def main():
     dev = torch.device("cuda", 0)
     g = torch.Generator(device=dev)
     g.manual_seed(0)
-    for t0 in range(0, L - 1, 256):
-        n = min(256, L - 1 - t0)
-        layer.prefill(torch.randn((n, B, E), generator=g, device=dev))
+    if args.synthetic:
+        layer.fill_synthetic(L - 1)
+    else:
+        for t0 in range(0, L - 1, 256):
+            n = min(256, L - 1 - t0)
+            layer.prefill(torch.randn((n, B, E), generator=g, device=dev))
     x = torch.randn((B, E), generator=g, device=dev)
     y = torch.empty((B, E), device=dev)
     q = torch.empty((B, cfg["nh"], H), device=dev)
