@@ -760,12 +760,10 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const size_t cap = static_cast<size_t>(a.cap);
 
-    // Zero the stage ring once: rows past a stage's valid end are read by the
-    // MMAs (times p = 0) and must hold finite values.  This prologue overlaps
-    // the previous kernel (programmatic dependent launch).
-    for (int i = tid; i < C::STAGES * C::STAGE / 16; i += C::THREADS)
-        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // Rows (and int8 scales) past a stage's valid end are read by the MMAs
+    // (times p = 0) and must be finite: each slot's first stage is copied
+    // whole (the cache and scale allocations carry a stage of padding), so
+    // later partial stages leave finite stale rows -- no ring zeroing.
     if (tid == 0) {
         for (int i = 0; i < C::STAGES; ++i) {
             mbar_init(&full[i], 1);
@@ -790,7 +788,7 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
     if (warp == C::NW) {
         if (lane == 0) {
             const uint64_t pol = policy_evict_first();
-            int slot = 0;
+            int slot = 0, issued = 0;
             uint32_t phase = 0;
             for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
                 const Unit g = unit_geom(u, nch, chunk, len);
@@ -800,8 +798,12 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
                     const int rows = min(C::ST, g.ntok - s * C::ST);
                     // whole 16-byte units; the swizzle only permutes within 1 KB blocks,
                     // so copy the covering blocks (rows past the end are masked)
-                    const uint32_t rbytes = static_cast<uint32_t>(min(C::ST * C::ROWB, ((rows * C::ROWB + 1023) / 1024) * 1024));
-                    const uint32_t sbytes = (CD == I8) ? static_cast<uint32_t>((rows * 4 + 15) & ~15) : 0u;
+                    const bool first = issued++ < C::STAGES;  // the slot's first use: copy it whole
+                    const uint32_t rbytes = first ? static_cast<uint32_t>(C::ST * C::ROWB)
+                        : static_cast<uint32_t>(min(C::ST * C::ROWB, ((rows * C::ROWB + 1023) / 1024) * 1024));
+                    const uint32_t sbytes = (CD == I8) ? (first ? static_cast<uint32_t>(C::ST * 4)
+                                                                : static_cast<uint32_t>((rows * 4 + 15) & ~15))
+                                                       : 0u;
                     const uint32_t qbytes = (s == 0) ? static_cast<uint32_t>(R * 4) : 0u;
                     mbar_wait(&empty[slot], phase ^ 1u);
                     uint8_t* dst = smem + slot * C::STAGE;

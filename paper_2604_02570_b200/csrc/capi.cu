@@ -863,8 +863,9 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
         while (c->fmax_chunks > 1 && (pairs * c->fmax_chunks + c->sms - 1) / c->sms > mu) --c->fmax_chunks;
     }
     const size_t rows = static_cast<size_t>(batch) * nh * c->cap_alloc;
-    cudaError_t e = c->data.alloc(rows * c->row_bytes);
-    if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4);
+    // + 128 KB: the attention rings copy a slot's first stage whole, which may run past the last row
+    cudaError_t e = c->data.alloc(rows * c->row_bytes + (128u << 10));
+    if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4 + (16u << 10));  // + a stage of scales
     if (e == cudaSuccess) e = c->ctrl.alloc(256);  // [0] len [1] done [2] step epoch [4,5] barrier [16..32) x-fetch counters
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     if (e == cudaSuccess)

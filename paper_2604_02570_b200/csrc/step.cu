@@ -237,11 +237,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     const int nBH = min(max(np1 - kNA, 0), 2 * C::NB);
     const int nA1 = np1 - nBH;
     const int nWS = (nBH + 1) / 2;  // attention stages holding parked items (the first nWS)
-    // prologue (overlaps the predecessor under PDL): rows past a stage's valid
-    // end are read by the MMAs (times p = 0) and must be finite
-    for (int i = tid; i < C::NB * C::STAGE / 16; i += kThr)
-        reinterpret_cast<uint4*>(ringB)[i] = make_uint4(0, 0, 0, 0);
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // Rows past a stage's valid end are read by the MMAs (times p = 0) and must
+    // be finite: every slot's first attention stage is copied whole (the cache
+    // allocation has a stage of padding), so later partial stages leave finite
+    // stale rows -- no zeroing of the ring in the prologue
     if (tid == 0) {
         for (int i = 0; i < kNA; ++i) {
             mbar_init(&fullA[i], 1);
@@ -325,7 +324,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 const int bh = u / nch, ck = u - bh * nch;
                 const int t0 = ck * chunk, ntok = min(chunk, len - t0);
                 const int rows = min(kST, ntok - st * kST);
-                const uint32_t rbytes = static_cast<uint32_t>(min(C::STAGE, ((rows * C::ROWB + 1023) / 1024) * 1024));
+                const uint32_t rbytes = ib < C::NB ? static_cast<uint32_t>(C::STAGE)
+                                                   : static_cast<uint32_t>(min(C::STAGE, ((rows * C::ROWB + 1023) / 1024) * 1024));
                 const int slot = ib % C::NB;
                 const uint32_t ph = static_cast<uint32_t>(ib / C::NB) & 1u;
                 if (ib < nWS) mbar_wait(&wdone[slot], 0u);  // its parked projection items are consumed
