@@ -520,21 +520,25 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                     while (ld_acquire(reinterpret_cast<const unsigned*>(a.counters + bh)) < static_cast<unsigned>(nch - 1)) {
                     }
                 __syncwarp();
+                // one pass over the other chunks in chunk order (online merge):
+                // each chunk's (m, l, acc) is one L2 round trip, loaded together
                 const float* wb = a.ws + static_cast<size_t>(bh) * a.max_chunks * kWS;
-                float M2 = M;
-                for (int c = 0; c < nch - 1; ++c) M2 = fmaxf(M2, __ldcg(wb + c * kWS + R));
-                float L2 = 0.f, a2 = 0.f;
+                float M2 = -INFINITY, L2 = 0.f, a2 = 0.f;
                 for (int c = 0; c < nch - 1; ++c) {
-                    const float mc = __ldcg(wb + c * kWS + R);
+                    const float mc = __ldcg(wb + c * kWS + R), lc = __ldcg(wb + c * kWS + R + 1);
+                    const float ac = __ldcg(wb + c * kWS + lane);
                     if (mc == -INFINITY) continue;
-                    const float f = ex2(mc - M2);
-                    L2 = fmaf(__ldcg(wb + c * kWS + R + 1), f, L2);
-                    a2 = fmaf(__ldcg(wb + c * kWS + lane), f, a2);
+                    const float Mn = fmaxf(M2, mc);
+                    const float fo = ex2(M2 - Mn), fc = ex2(mc - Mn);  // fo = 0 while M2 = -inf
+                    L2 = fmaf(lc, fc, L2 * fo);
+                    a2 = fmaf(ac, fc, a2 * fo);
+                    M2 = Mn;
                 }
                 if (M != -INFINITY) {
-                    const float f = ex2(M - M2);
-                    L2 = fmaf(L, f, L2);
-                    a2 = fmaf(av, f, a2);
+                    const float Mn = fmaxf(M2, M);
+                    const float fo = ex2(M2 - Mn), fc = ex2(M - Mn);
+                    L2 = fmaf(L, fc, L2 * fo);
+                    a2 = fmaf(av, fc, a2 * fo);
                 }
                 av = a2;
                 L = L2;
