@@ -245,6 +245,7 @@ struct wsvd_cache_s {
     DevBuf qfull;                     // [B][nh][H] query of the last append (explicit mode)
     int chunk = 512, max_chunks = 1, grid = 148;
     int fmax_chunks = 1;              // split-KV chunks of the fused step kernel
+    int pair_ok = -1;                 // the fused step can run as resident CTA pairs (-1: not probed)
     int sms = 148;
     cudaGraphExec_t gexec = nullptr;
     cudaGraph_t graph = nullptr;
@@ -537,6 +538,10 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bo
     a.chunk = c->chunk;
     a.max_chunks = c->chunk > 0 ? c->max_chunks : c->fmax_chunks;
     a.grid = c->sms;
+    // CTA pairs when the split-KV uses two chunks per (sequence, head)
+    static const bool no_cluster = getenv("WSVD_STEP_NOCLUSTER") != nullptr;  // A/B switch
+    if (c->pair_ok < 0) c->pair_ok = step_pair_clusters_ok(c->B, c->sms);
+    a.cluster = (!no_cluster && a.chunk == 0 && a.max_chunks == 2 && c->pair_ok == 1) ? 2 : 1;
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
     if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 12 * 8));
     a.trace = trace ? c->trace.as<uint64_t>() : nullptr;

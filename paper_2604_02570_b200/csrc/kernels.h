@@ -142,11 +142,13 @@ struct StepArgs {
     uint64_t* trace;       // [grid][8] %globaltimer at the phase marks, or null
     int B, nh, E, Kp, Nrows, e_out, oKp, otiles, cap;
     int chunk, max_chunks, grid;
+    int cluster;           // 2: CTA pairs; a 2-chunk (sequence, head)'s chunks meet through DSMEM
 };
 bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp, int oKp, int otiles, int grid);
 int step_item_k();
 size_t step_xo_bytes(int B, int oKp);  // bytes of StepArgs::xo
 int step_max_units();  // attention units one CTA of the fused step can hold
 cudaError_t launch_layer_step(const StepArgs& a, cudaStream_t s);
+int step_pair_clusters_ok(int B, int grid);  // 1 when the grid can run as resident CTA pairs
 
 }  // namespace wsvd_k

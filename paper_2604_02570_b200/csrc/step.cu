@@ -57,7 +57,8 @@ struct SC {
     static constexpr int STAGE = kST * ROWB;
     static constexpr int XB = MT * 16 * kXS;               // one staged X slice
     // per-unit scratch: absorbed queries, the new token's row, the warp states
-    static constexpr int RED = kMaxU * (R * 4 + 4 * R + kNW * (R + 2) * 4);
+    // + [kMaxU][R+2] chunk states a cluster peer writes through DSMEM
+    static constexpr int RED = kMaxU * (R * 4 + 4 * R + kNW * (R + 2) * 4 + (R + 2) * 4);
     static constexpr int FIXED = kNA * kItem + XB + RED + 768;
     static constexpr int NB_RAW = (225 * 1024 - FIXED) / STAGE;
     static constexpr int NB = NB_RAW > 6 ? 6 : NB_RAW;
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     float* qts = reinterpret_cast<float*>(smem + C::RED_OFF);                // [kMaxU][R]
     __nv_bfloat16* nrow = reinterpret_cast<__nv_bfloat16*>(qts + kMaxU * R);  // [kMaxU][2R]
     float* wst = qts + 2 * kMaxU * R;                                         // [kMaxU][kNW][R+2]
+    float* pst = wst + kMaxU * kNW * (R + 2);                                 // [kMaxU][R+2] peer chunk states
     uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     uint64_t* emptyA = fullA + kNA;
     uint64_t* fullB = emptyA + kNA;
@@ -206,6 +208,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     uint64_t* p3bar = sfull + kMaxU;    // P3: chunk states landed (one phase per staged split)
     uint64_t* wfull = p3bar + 1;        // [2*NB] projection items parked in the attention ring
     uint64_t* wdone = wfull + 2 * C::NB;  // [NB] those items consumed: the stage is free
+    uint64_t* pbar = wdone + C::NB;       // [kMaxU] unit j's peer chunk state landed (CTA pairs)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -258,9 +261,11 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         for (int b = 0; b < nBH; ++b) mbar_init(&wfull[b], 1);
         for (int st = 0; st < C::NB; ++st)  // stage st parks items 4+2st and 4+2st+1
             mbar_init(&wdone[st], st < nWS ? min(2, nBH - 2 * st) : 1);
+        for (int j = 0; j < kMaxU; ++j) mbar_init(&pbar[j], 1);
         fence_mbar_init();
     }
     __syncthreads();
+    if (a.cluster > 1) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
     // The weights (projection W-tiles, then the folded O-projection) are
     // constant across steps: the producer starts streaming them before the
     // predecessor has drained (programmatic dependent launch), only the token,
@@ -504,6 +509,22 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 L = fmaf(rb[w * (R + 2) + R + 1], f, L);
                 av = fmaf(rb[w * (R + 2) + lane], f, av);
             }
+            // CTA pairs (cluster of 2, nch == 2): chunk 0 of a (sequence, head) runs
+            // on the even CTA and its home chunk 1 on the odd one in the same round
+            // j, so the state crosses through distributed shared memory with one
+            // remote mbarrier arrive instead of an L2 publish / poll / load
+            const bool pair = a.cluster == 2 && nch == 2;
+            if (pair && ck == 0) {
+                const uint32_t dst = cluster_map(smem_u32(pst + j * (R + 2)), 1u);
+                st_cluster_f32(dst + 4u * lane, av);
+                if (lane == 0) {
+                    st_cluster_f32(dst + 4u * R, M);
+                    st_cluster_f32(dst + 4u * (R + 1), L);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(cluster_map(smem_u32(&pbar[j]), 1u));
+                continue;
+            }
             if (ck < nch - 1) {
                 float* wsp = a.ws + (static_cast<size_t>(bh) * a.max_chunks + ck) * kWS;
                 wsp[lane] = av;
@@ -515,7 +536,22 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 if (lane == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(a.counters + bh) : "memory");
                 continue;
             }
-            if (nch > 1) {
+            if (pair) {
+                mbar_wait_cluster(&pbar[j], 0u);
+                const float* ps = pst + j * (R + 2);
+                const float mc = ps[R], lc = ps[R + 1], ac = ps[lane];
+                float M2 = M, L2 = L, a2 = av;
+                if (mc != -INFINITY) {  // chunk 0 first, then this chunk (the chunk order of the L2 path)
+                    const float Mn = fmaxf(mc, M);
+                    const float fc = ex2(mc - Mn), fo = ex2(M - Mn);  // fo = 0 when M = -inf
+                    L2 = fmaf(L, fo, lc * fc);
+                    a2 = fmaf(av, fo, ac * fc);
+                    M2 = Mn;
+                }
+                av = a2;
+                L = L2;
+                (void)M2;
+            } else if (nch > 1) {
                 if (lane == 0)
                     while (ld_acquire(reinterpret_cast<const unsigned*>(a.counters + bh)) < static_cast<unsigned>(nch - 1)) {
                     }
@@ -752,7 +788,35 @@ cudaError_t launch_mt(const StepArgs& a, cudaStream_t s) {
             if (e != cudaSuccess) return e;
             attr = true;
         }
-        return launch_pdl(k, dim3(a.grid), dim3(kThr), C::SMEM, s, a);
+        return launch_pdl_cluster(k, dim3(a.grid), dim3(kThr), C::SMEM, s, a.cluster, a);
+    }
+}
+
+template <int MT>
+int pair_ok(int grid) {
+    using C = SC<32, MT>;
+    if constexpr (!C::OK) {
+        return 0;
+    } else {
+        auto k = layer_step_kernel<32, MT>;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess) return 0;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kThr);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            return 0;
+        }
+        return 2 * n >= grid ? 1 : 0;
     }
 }
 
@@ -774,6 +838,11 @@ bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp,
 }
 
 int step_item_k() { return kKS; }
+
+int step_pair_clusters_ok(int B, int grid) {
+    if (grid % 2 != 0) return 0;
+    return (B + 15) / 16 == 1 ? pair_ok<1>(grid) : pair_ok<2>(grid);
+}
 
 size_t step_xo_bytes(int B, int oKp) { return static_cast<size_t>(oKp / kKS) * ((B + 15) / 16) * 16 * kXS; }
 

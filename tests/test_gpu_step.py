@@ -13,6 +13,7 @@ from tests.helpers import REL_TOL, rel_err_rows, to_factors
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
+ROOT = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
 
 
 def _twin(E, nh, H, r, B, cap, seed, **kw):
@@ -25,7 +26,10 @@ def _twin(E, nh, H, r, B, cap, seed, **kw):
     return rng, lay, wo, mk
 
 
-@pytest.mark.parametrize("E,nh,B,L", [(512, 16, 1, 300), (512, 16, 5, 77), (1024, 16, 16, 600), (512, 16, 32, 130)])
+@pytest.mark.parametrize("E,nh,B,L", [(512, 16, 1, 300), (512, 16, 5, 77), (1024, 16, 16, 600), (512, 16, 32, 130),
+                                      # 512 (sequence, head) pairs -> two chunks each: the CTA-pair
+                                      # (cluster) merge through distributed shared memory
+                                      (1024, 32, 16, 300)])
 def test_fused_step_matches_oracle(E, nh, B, L):
     H, r = 128, 32
     rng, lay, wo, mk = _twin(E, nh, H, r, B, L + 8, 8000 + B)
@@ -152,3 +156,42 @@ def test_fused_step_short_caches_and_ragged_ranks(B, L):
         ref = O.fused_decode_step(lb, dev_k, dev_v, L, q, 32)
         y_ref = ref.reshape(-1) @ wo
         assert rel_err_rows(y[b:b + 1], y_ref[None]) <= 1e-2, f"b={b}"
+
+
+def test_cluster_pair_merge_matches_l2_merge():
+    """The CTA-pair merge (chunk 0's state crosses to the home chunk through
+    DSMEM) is bit-identical to the L2 publish / poll path (WSVD_STEP_NOCLUSTER,
+    run in a child process: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    code = r"""
+import numpy as np, torch, sys
+sys.path.insert(0, %r)
+from oracle import oracle as O
+from tests.helpers import to_factors
+from paper_2604_02570_b200.layer import DecodeLayer
+rng = O.Rng(8300)
+E, nh, H, r, B, L = 1024, 32, 128, 32, 16, 400
+lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
+wo = O.bf16_round(rng.normal_matrix(nh * H, E, 1.0 / np.sqrt(E)))
+layer = DecodeLayer(to_factors(lay), wo, batch=B, capacity=L + 8, cache_dtype="bf16", weight_dtype="bf16")
+dev = torch.device("cuda", 0)
+toks = torch.from_numpy(O.bf16_round(rng.normal_matrix((L + 2) * B, E)).reshape(L + 2, B, E).astype(np.float32)).to(dev)
+layer.prefill(toks[:L])
+ys = []
+for t in range(2):
+    y = torch.empty((B, E), device=dev)
+    layer.step(toks[L + t], y)
+    ys.append(y.cpu().numpy())
+np.save(sys.argv[1], np.stack(ys))
+""" % (ROOT,)
+    outs = []
+    for i, env_extra in enumerate(({}, {"WSVD_STEP_NOCLUSTER": "1"})):
+        path = os.path.join(ROOT, "gpurun_out", f"pair_merge_{i}.npy")
+        os.makedirs(os.path.dirname(path), exist_ok=True)
+        res = subprocess.run([sys.executable, "-c", code, path], env=dict(os.environ, **env_extra),
+                             capture_output=True, text=True, timeout=600, cwd=ROOT)
+        assert res.returncode == 0, res.stderr[-3000:]
+        outs.append(np.load(path))
+    assert np.array_equal(outs[0], outs[1])
