@@ -542,6 +542,10 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bo
     static const bool no_cluster = getenv("WSVD_STEP_NOCLUSTER") != nullptr;  // A/B switch
     if (c->pair_ok < 0) c->pair_ok = step_pair_clusters_ok(c->B, c->sms);
     a.cluster = (!no_cluster && a.chunk == 0 && a.max_chunks == 2 && c->pair_ok == 1) ? 2 : 1;
+    // parked stages refill after grid barrier 1: TMA loads in flight make the
+    // barrier's release slow (10.7 -> 9.0 us; WSVD_STEP_GATE_B1=0 is the A/B switch)
+    static const bool gate_off = getenv("WSVD_STEP_GATE_B1") && std::string(getenv("WSVD_STEP_GATE_B1")) == "0";
+    a.gate_b1 = gate_off ? 0 : 1;
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
     if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 12 * 8));
     a.trace = trace ? c->trace.as<uint64_t>() : nullptr;

@@ -142,6 +142,7 @@ struct StepArgs {
     uint64_t* trace;       // [grid][8] %globaltimer at the phase marks, or null
     int B, nh, E, Kp, Nrows, e_out, oKp, otiles, cap;
     int chunk, max_chunks, grid;
+    int gate_b1;           // parked stages refill only after grid barrier 1
     int cluster;           // 2: CTA pairs; a 2-chunk (sequence, head)'s chunks meet through DSMEM
 };
 bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp, int oKp, int otiles, int grid);

@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     uint64_t* wfull = p3bar + 1;        // [2*NB] projection items parked in the attention ring
     uint64_t* wdone = wfull + 2 * C::NB;  // [NB] those items consumed: the stage is free
     uint64_t* pbar = wdone + C::NB;       // [kMaxU] unit j's peer chunk state landed (CTA pairs)
+    uint64_t* b1bar = pbar + kMaxU;       // grid barrier 1 passed (gates the parked stages' refill)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
@@ -262,6 +263,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         for (int st = 0; st < C::NB; ++st)  // stage st parks items 4+2st and 4+2st+1
             mbar_init(&wdone[st], st < nWS ? min(2, nBH - 2 * st) : 1);
         for (int j = 0; j < kMaxU; ++j) mbar_init(&pbar[j], 1);
+        mbar_init(b1bar, 1);
         fence_mbar_init();
     }
     __syncthreads();
@@ -323,6 +325,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 tma_bulk_g2s(ringA + slot * kItem, a_src(ia), kItem, &fullA[slot]);
                 ++ia;
             };
+            const bool gate_b1 = a.gate_b1 != 0;
             int u = cta, st = 0, ib = 0;
             auto issue_b = [&]() -> bool {
                 if (u >= n_units) return false;
@@ -333,7 +336,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                                                    : static_cast<uint32_t>(min(C::STAGE, ((rows * C::ROWB + 1023) / 1024) * 1024));
                 const int slot = ib % C::NB;
                 const uint32_t ph = static_cast<uint32_t>(ib / C::NB) & 1u;
-                if (ib < nWS) mbar_wait(&wdone[slot], 0u);  // its parked projection items are consumed
+                if (ib < nWS) {
+                    mbar_wait(&wdone[slot], 0u);  // its parked projection items are consumed
+                    if (gate_b1) mbar_wait(b1bar, 0u);
+                }
                 mbar_wait(&emptyB[slot], ph ^ 1u);
                 mbar_arrive_expect_tx(&fullB[slot], rbytes);
                 const uint8_t* src = a.cache + (static_cast<size_t>(bh) * cap + t0) * C::ROWB + static_cast<size_t>(st) * C::STAGE;
@@ -432,6 +438,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     named_bar_sync(1, kSync);
     STEP_MARK(2);  // every P1 warp of this CTA is done
     grid_sync(a.bar, (2u * epoch + 1u) * G);  // consumers + helper
+    if (tid == 0) mbar_arrive(b1bar);
     STEP_MARK(3);
 
     if (warp == kNW + 1) {
