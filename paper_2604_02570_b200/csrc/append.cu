@@ -193,9 +193,17 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
     extern __shared__ float sm[];
     float* c = sm;                 // [3][R] latents q, k, v
     float* qh = sm + 3 * a.R;      // [H]
+    float* mqs = qh + a.H;         // [R][R] this head's M_QK (layer-step mode)
     const int h = blockIdx.x, m = blockIdx.y;
     const int b = m % a.B, tpos = m / a.B;  // rows are token-major: m = tpos * B + b
     const int R = a.R, H = a.H;
+    const bool fold = a.q_out == nullptr && a.qt != nullptr;
+    if (fold) {
+        // M_QK is a layer constant: staged before the grid-dependency wait, so
+        // its loads overlap the predecessor instead of following the split sums
+        const float4* src = reinterpret_cast<const float4*>(a.mqk + static_cast<size_t>(h) * R * R);
+        for (int i = threadIdx.x; i < R * R / 4; i += kEpThreads) reinterpret_cast<float4*>(mqs)[i] = __ldg(src + i);
+    }
     griddep_wait();
     griddep_launch_dependents();
     const int pos = *a.d_len + tpos;
@@ -287,11 +295,10 @@ __global__ void __launch_bounds__(kEpThreads) append_epilogue_kernel(const Appen
     } else if (a.qt != nullptr) {
         // layer step: q_h is never materialised; qt = c_Q . M_QK with
         // M_QK = scale * B_Q . B_K^T (R x R, folded on the host in fp64)
-        const float* mq = a.mqk + static_cast<size_t>(h) * R * R;
         for (int i = threadIdx.x; i < R; i += kEpThreads) {
             float acc = 0.f;
 #pragma unroll 16
-            for (int j = 0; j < R; ++j) acc = fmaf(c[j], __ldg(mq + j * R + i), acc);
+            for (int j = 0; j < R; ++j) acc = fmaf(c[j], mqs[j * R + i], acc);
             a.qt[(static_cast<size_t>(m) * a.nh + h) * R + i] = acc;
         }
     }
@@ -428,7 +435,14 @@ cudaError_t launch_act_quant(const float* x, int M, int E, int Kp, int rot, int 
 }
 
 cudaError_t launch_append_epilogue(const AppendArgs& a, cudaStream_t s) {
-    const int smem = (3 * a.R + a.H) * 4;
+    const bool fold = a.q_out == nullptr && a.qt != nullptr;
+    const int smem = (3 * a.R + a.H + (fold ? a.R * a.R : 0)) * 4;  // R*R*4 <= 64 KB for R <= 128
+    static int attr_smem = 0;
+    if (smem > 48 * 1024 && smem > attr_smem) {
+        cudaError_t e = cudaFuncSetAttribute(append_epilogue_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_smem = smem;
+    }
     return launch_pdl(append_epilogue_kernel, dim3(a.nh, a.M), dim3(kEpThreads), smem, s, a);
 }
 
