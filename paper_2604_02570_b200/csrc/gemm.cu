@@ -61,6 +61,7 @@ __host__ __device__ __forceinline__ int x_stride(int KS) {
 // so staging costs one memory latency per batch rather than one per item.
 template <int WT>
 WSVD_DEV void stage_x(const GemmArgs& a, uint8_t* xs, int k0, int Mp) {
+    if (threadIdx.x >= kXThreads) return;  // the first kXThreads threads stage the slice
     const int stride = x_stride<WT>(a.KS);
     constexpr int BATCH = 8;
     if (WT == BF16) {
@@ -134,8 +135,12 @@ WSVD_DEV void stage_x(const GemmArgs& a, uint8_t* xs, int k0, int Mp) {
 // the slot's mbarrier); consumer warp w takes items w, w+4, ... and runs the
 // MMAs straight from the slot.  One CTA per SM, deep bytes-in-flight, no wave
 // quantisation.
-constexpr int kStreamConsumers = 4;
-constexpr int kStreamThreads = 32 * (kStreamConsumers + 1);
+// consumer warps: 4, or 8 for 64+ token rows (MMA issue then dominates an item)
+template <int MT>
+struct StreamWarps {
+    static constexpr int C = MT >= 4 ? 8 : 4;
+    static constexpr int THREADS = 32 * (C + 1);
+};
 
 template <int WT, int MT>
 struct StreamCfg {
@@ -152,7 +157,8 @@ struct StreamCfg {
 };
 
 template <int WT, int MT>
-__global__ void __launch_bounds__(kStreamThreads, 1) skinny_stream_kernel(const GemmArgs a) {
+__global__ void __launch_bounds__(StreamWarps<MT>::THREADS, 1) skinny_stream_kernel(const GemmArgs a) {
+    constexpr int kStreamConsumers = StreamWarps<MT>::C;
     using G = GT<WT>;
     using S = StreamCfg<WT, MT>;
     extern __shared__ __align__(128) uint8_t smem[];
@@ -462,7 +468,7 @@ cudaError_t launch_stream(const GemmArgs& a, cudaStream_t s) {
     }
     const int splits = a.Kp / a.KS;
     const int grid = splits <= a.grid ? (a.grid / splits) * splits : splits;
-    return launch_pdl(k, dim3(grid), dim3(kStreamThreads), smem, s, a);
+    return launch_pdl(k, dim3(grid), dim3(StreamWarps<MT>::THREADS), smem, s, a);
 }
 
 template <int WT>
