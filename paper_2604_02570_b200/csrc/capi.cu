@@ -849,15 +849,31 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     c->sms = p.multiProcessorCount;
     c->grid = c->sms * attn_occupancy(cache_dtype, L->R);
     // split-KV: each (sequence, head) is cut into up to max_chunks equal chunks
-    // per launch (attn.cu chunking()), about one unit per persistent CTA when
-    // the (sequence, head) pairs alone do not fill the grid
+    // per launch (attn.cu chunking()).  Fewer pairs than CTAs: about one unit
+    // per CTA (B1 ctx2K fp32: attention + combine 12.3 us against 26.9 at four
+    // units per CTA).  Otherwise the fewest chunks whose units spread over the
+    // persistent grid at >= 90 % balance (units / (grid * rounds)): B16 x 32
+    // heads -> 2 chunks (1 chunk leaves 3.46 units per CTA on 4 rounds; the
+    // 32-layer B128 stack measured 13.1 ms at 2 against 13.3+ at 1);
+    // B32 / B64 int8 configs -> 1
     c->chunk = 0;
-    // target units per CTA; measured (tools/timing.py, attention + combine):
-    // B1 ctx2K fp32 12.3 us at 1 against 26.9 at 4; B16 ctx4K bf16 and the
-    // int8 configs within 1 us of each other
-    int units = 1;
-    if (const char* env = getenv("WSVD_ATTN_UNITS")) units = std::max(1, atoi(env));
-    c->max_chunks = std::max(1, std::min(64, (units * c->grid + batch * nh - 1) / (batch * nh)));
+    {
+        const int pairs = batch * nh;
+        int nchk = 1;
+        if (pairs < c->grid) {
+            nchk = (c->grid + pairs - 1) / pairs;
+        } else {
+            while (nchk < 8) {
+                const long u = static_cast<long>(pairs) * nchk;
+                const long rounds = (u + c->grid - 1) / c->grid;
+                if (u * 10 >= rounds * c->grid * 9) break;
+                ++nchk;
+            }
+        }
+        if (const char* env = getenv("WSVD_ATTN_UNITS"))  // A/B: target units per CTA
+            nchk = (std::max(1, atoi(env)) * c->grid + pairs - 1) / pairs;
+        c->max_chunks = std::max(1, std::min(64, nchk));
+    }
     if (const char* env = getenv("WSVD_ATTN_CHUNK")) {  // fixed chunk length (tests)
         c->chunk = std::max(32, round_up(atoi(env), 32));
         c->max_chunks = (c->cap_alloc + c->chunk - 1) / c->chunk;

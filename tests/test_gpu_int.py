@@ -222,7 +222,7 @@ def test_layer_step_single_chunk_in_kernel_merge(cache):
     (combine kernel, full-rank output) followed by the O-projection."""
     from paper_2604_02570_b200.layer import DecodeLayer
     rng = O.Rng(91)
-    E, nh, r, H, B, L = 512, 32, 32, 128, 5, 300   # 160 pairs >= 148 CTAs -> max_chunks 1
+    E, nh, r, H, B, L = 512, 4, 32, 128, 37, 300   # 148 pairs = one per CTA -> max_chunks 1
     lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
     f = to_factors(lay)
     w_o = O.bf16_round(rng.normal_matrix(nh * H, E, 1.0 / np.sqrt(nh * H)))
