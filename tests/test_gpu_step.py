@@ -79,10 +79,12 @@ def test_fused_step_is_deterministic_and_matches_attention_path():
         assert torch.equal(ya, yb)
 
 
-def test_step_host_replays_match_device_step():
-    """wsvd_layer_step_host: eager call, capture, then graph replays -- every
+@pytest.mark.parametrize("E,nh,B,L", [(512, 16, 16, 200),
+                                      (1024, 32, 16, 200)])  # 2 chunks per pair: the CTA-pair path
+def test_step_host_replays_match_device_step(E, nh, B, L):
+    """wsvd_layer_step_host (pinned x / y moved by the kernel itself) -- every
     step bit-identical to the device-buffer step of a twin cache"""
-    E, nh, H, r, B, L = 512, 16, 128, 32, 16, 200
+    H, r = 128, 32
     rng, lay, wo, mk = _twin(E, nh, H, r, B, L + 16, 8200)
     dev_l, host_l = mk(), mk()
     dev = torch.device("cuda", 0)
