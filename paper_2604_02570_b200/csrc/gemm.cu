@@ -135,15 +135,20 @@ WSVD_DEV void stage_x(const GemmArgs& a, uint8_t* xs, int k0, int Mp) {
 // the slot's mbarrier); consumer warp w takes items w, w+4, ... and runs the
 // MMAs straight from the slot.  One CTA per SM, deep bytes-in-flight, no wave
 // quantisation.
-// consumer warps: 4, or 8 for 64+ token rows (MMA issue then dominates an item)
+// consumer warps: 4, or 8 for 64 token rows (MMA issue then dominates an item).
+// Consumer warp w takes items w, w + C, ... of one ring, so the ring needs at
+// least C slots: a slot's previous fill must be complete before its next
+// waiter arrives (parity waits cannot tell phase u from u - 2).  MT = 8 keeps
+// 4 consumers (its 128-row token slice leaves room for 5 slots).
 template <int MT>
 struct StreamWarps {
-    static constexpr int C = MT >= 4 ? 8 : 4;
+    static constexpr int C = MT == 4 ? 8 : 4;
     static constexpr int THREADS = 32 * (C + 1);
 };
 
 template <int WT, int MT>
 struct StreamCfg {
+    static constexpr int MTV = MT;
     static constexpr int XROWS = MT * 16;
     __host__ __device__ static int ksb(int KS) { return WT == I4 ? KS / 2 : KS * (WT == BF16 ? 2 : 1); }
     __host__ __device__ static int item_bytes(int KS) { return 16 * ksb(KS); }
@@ -457,7 +462,7 @@ cudaError_t launch_f32_rows(const GemmArgs& a, cudaStream_t s) {
 template <int WT, int MT>
 cudaError_t launch_stream(const GemmArgs& a, cudaStream_t s) {
     using S = StreamCfg<WT, MT>;
-    if (S::stages(a.KS) < 2) return cudaErrorInvalidConfiguration;
+    if (S::stages(a.KS) < StreamWarps<MT>::C) return cudaErrorInvalidConfiguration;  // see StreamWarps
     const int smem = S::smem(a.KS);
     auto k = skinny_stream_kernel<WT, MT>;
     static int attr_smem = 0;
@@ -502,7 +507,7 @@ bool f32_rows_path(int M, int Kp, int KS) {
 
 bool gemm_fits(int wdtype, int M, int KS) {
     const int mt = (M + 15) / 16;
-    auto st = [&](auto cfg) { return decltype(cfg)::stages(KS) >= 2; };
+    auto st = [&](auto cfg) { return decltype(cfg)::stages(KS) >= StreamWarps<decltype(cfg)::MTV>::C; };
     switch (wdtype) {
         case BF16: return mt <= 1 ? st(StreamCfg<BF16, 1>{}) : mt <= 2 ? st(StreamCfg<BF16, 2>{}) : mt <= 4 ? st(StreamCfg<BF16, 4>{}) : st(StreamCfg<BF16, 8>{});
         case I8: return mt <= 1 ? st(StreamCfg<I8, 1>{}) : mt <= 2 ? st(StreamCfg<I8, 2>{}) : mt <= 4 ? st(StreamCfg<I8, 4>{}) : st(StreamCfg<I8, 8>{});

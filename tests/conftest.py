@@ -13,6 +13,13 @@ def pytest_configure(config):
     config.addinivalue_line("markers", "slow: full-size (BASELINE config) parity checks")
 
 
+def pytest_collection_modifyitems(config, items):
+    # a kernel that never finishes must fail the test, not hang the GPU box
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(600))
+
+
 @pytest.fixture(scope="session", autouse=True)
 def _oracle_built():
     # the CPU oracle is test infrastructure; build it on first use

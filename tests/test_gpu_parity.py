@@ -249,3 +249,31 @@ def test_bf16_append_and_decode(E, nh, r, H, B, L):
         # and against the unrounded-latent fp64 reference
         ref64 = O.fused_decode_step(lb, ck_ref, cv_ref, L, q_ref, 32)
         assert rel_err_rows(out[b], ref64) <= 2e-2
+
+
+def test_prefill_large_matches_token_by_token_appends():
+    """Prefill at the 7B width with 128-row GEMM chunks (8 K splits, many
+    W-tiles per CTA, the 128-row consumer configuration) writes the same cache
+    rows as one-token appends (16-row configuration)."""
+    from paper_2604_02570_b200.layer import DecodeLayer
+    from oracle import oracle as O
+    from tests.helpers import to_factors
+    rng = O.Rng(4242)
+    E, nh, H, r, B, T = 4096, 32, 128, 32, 16, 16
+    lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
+    f = to_factors(lay)
+    a = DecodeLayer(f, None, batch=B, capacity=T + 8, cache_dtype="bf16", weight_dtype="bf16")
+    b = DecodeLayer(f, None, batch=B, capacity=T + 8, cache_dtype="bf16", weight_dtype="bf16")
+    dev = torch.device("cuda", 0)
+    toks = torch.from_numpy(rng.normal_matrix(T * B, E).reshape(T, B, E).astype(np.float32)).to(dev)
+    a.prefill(toks)                 # 256 rows -> two 128-row GEMM chunks
+    for t in range(T):
+        b.append(toks[t])           # 16 rows each
+    torch.cuda.synchronize()
+    assert a.length() == b.length() == T
+    for bb in (0, 7, 15):
+        for h in (0, 13, 31):
+            ka, va = a.read_latents(bb, h)
+            kb, vb = b.read_latents(bb, h)
+            assert np.abs(ka - kb).max() <= 1e-2 * np.abs(kb).max()
+            assert np.abs(va - vb).max() <= 1e-2 * np.abs(vb).max()
