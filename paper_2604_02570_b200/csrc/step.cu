@@ -397,13 +397,11 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         }
         if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid);
         named_bar_sync(2, 32 * kNW);
-        if (warp < kNA) {
-            // items k = warp mod kNA: the ones parked in the attention ring first
-            // (their stages then refill with cache rows during the rest of P1),
-            // the weight ring's last
-            for (int kk = warp + kNA; kk < np1 + kNA; kk += kNA) {
-                const int k = kk < np1 ? kk : warp;
-                if (k >= np1) break;
+        {
+            // all kNW consumer warps take items k = warp mod kNW in item order:
+            // the weight ring's four (in flight first) and then the parked
+            // ones as they land, at most two per warp
+            for (int k = warp; k < np1; k += kNW) {
                 float facc[MT][2][4];
                 if (k >= kNA && k < kNA + nBH) {
                     const int b = k - kNA;
