@@ -25,6 +25,7 @@ C3=7b-r32-b32-ctx4k-w8a8-i8cache
 C1=7b-r32-b1-ctx2k-f32
 python bench.py --config $C3 --no-baselines > gpurun_out/bench_config3.json 2> /dev/null
 python bench.py --config $C1 --no-baselines > gpurun_out/bench_config1.json 2> /dev/null
+python bench.py --config 7b-stack32-r32-b128-ctx32k-bf16 > gpurun_out/bench_stack_config5.json 2> /dev/null
 python tools/timing.py --config $C3 > gpurun_out/timing_config3.txt 2>&1
 python tools/timing.py --config $C1 > gpurun_out/timing_config1.txt 2>&1
 ncu --set full --clock-control none --import-source on -k regex:decode_attn -s 1 -c 1 \

@@ -107,7 +107,7 @@ def main():
     for name in ("step_full", "attn_full", "tc_full", "gemm_full", "i8_full", "f32rows_full"):
         summarize_full(name, tag)
     for f in ("bench.json", "bench_ref.json", "timing.txt", "gpu.txt", "step_trace.txt", "bench_config3.json",
-              "bench_config1.json", "timing_config3.txt", "timing_config1.txt"):
+              "bench_config1.json", "timing_config3.txt", "timing_config1.txt", "bench_stack_config5.json"):
         src = os.path.join(RAW, f)
         if os.path.exists(src):
             with open(src) as a, open(os.path.join(OUT, f"{tag}_{f}"), "w") as b:
