@@ -29,7 +29,8 @@ def _twin(E, nh, H, r, B, cap, seed, **kw):
 @pytest.mark.parametrize("E,nh,B,L", [(512, 16, 1, 300), (512, 16, 5, 77), (1024, 16, 16, 600), (512, 16, 32, 130),
                                       # 512 (sequence, head) pairs -> two chunks each: the CTA-pair
                                       # (cluster) merge through distributed shared memory
-                                      (1024, 32, 16, 300)])
+                                      (1024, 32, 16, 300), (1024, 32, 16, 33), (1024, 32, 16, 65),
+                                      (1024, 32, 16, 2)])
 def test_fused_step_matches_oracle(E, nh, B, L):
     H, r = 128, 32
     rng, lay, wo, mk = _twin(E, nh, H, r, B, L + 8, 8000 + B)
