@@ -10,25 +10,28 @@
 // and two grid-wide barriers:
 //
 //   P1  latent projection  P[split][b][n] = x_b . A_all[:, n] over one K split
-//       (swap-AB mma.sync over W-tiles streamed by TMA, as gemm.cu);
+//       (swap-AB mma.sync over W-tiles streamed by TMA, as gemm.cu), on all
+//       eight consumer warps;
 //   --  grid barrier 1 (all projection partials written)
 //   P2  attention units (sequence, head, chunk) exactly as attn.cu's
-//       tensor-core consumer; each unit derives its absorbed query from the
-//       partials itself (qt = (sum_split c_Q) . M_QK, the append epilogue's
-//       fold), the unit holding the new token writes the token's latent row
-//       into the cache and patches it into the shared-memory stage; each
-//       unit's 8 warp states are merged (fixed order) into a unit state;
-//   --  grid barrier 2 (unit states complete; the cache length is committed)
-//   P3  folded O-projection y = vlat . (B_V . W_o) over W-tiles that were
-//       prefetched into shared memory during P2; the CTA builds the vlat rows
-//       it needs by merging each (sequence, head)'s chunk states in chunk
-//       order (SoftmaxState::merge, decode.cpp:59-75) -- no atomics, and the
-//       result is run-to-run deterministic.
+//       tensor-core consumer; the helper warp derives each unit's absorbed
+//       query from the partials (qt = (sum_split c_Q) . M_QK, the append
+//       epilogue's fold), writes the new token's latent row into the cache
+//       for the unit holding it (patched into the shared-memory stage), merges
+//       each unit's 8 warp states (fixed order) and, for the last chunk of a
+//       (sequence, head), merges the chunks in chunk order
+//       (SoftmaxState::merge, decode.cpp:59-75) into the bf16 rows of the
+//       O-projection input -- through distributed shared memory when the grid
+//       runs as 2-CTA clusters (two chunks per pair), else through L2;
+//   --  grid barrier 2 (every row complete; the cache length is committed)
+//   P3  folded O-projection y = vlat . (B_V . W_o) over W-tiles prefetched
+//       into shared memory during P2; each CTA owns whole output tiles and
+//       sums their K splits itself -- no atomics, run-to-run deterministic.
 //
-// One producer warp keeps HBM busy across the phase boundaries: it first
-// fills the weight ring and the attention ring (the cache rows are ready
-// before the step starts), then streams the rest of the projection weights,
-// the O-projection weights and the remaining cache stages.
+// One producer warp issues every projection item of the CTA before the
+// grid-dependency wait (a 4-slot weight ring plus items parked in the
+// attention ring), then the O-projection weights and, once barrier 1 has
+// passed, the cache stream.
 #include "common.cuh"
 #include "kernels.h"
 
