@@ -150,6 +150,11 @@ struct Unit {
 // fixes the chunk length (tests); otherwise up to a.max_chunks chunks of equal
 // length (a multiple of 32 tokens), so every unit carries real work.
 WSVD_DEV void chunking(const AttnArgs& a, int len, int& nch, int& chunk) {
+    if (a.cluster > 1) {  // exactly one chunk per cluster CTA (trailing ones may be empty)
+        nch = a.cluster;
+        chunk = (((len + nch - 1) / nch) + 31) & ~31;
+        return;
+    }
     if (a.chunk > 0) {
         chunk = a.chunk;
     } else {
@@ -712,13 +717,81 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
 // kernel, whose 128 threads per head do it in parallel (one warp inside the
 // attention kernel measured 4x slower for the whole launch).
 __host__ __device__ inline bool attn_finalizes(const AttnArgs& a) {
-    return a.chunk == 0 && a.max_chunks == 1 && a.out == nullptr && !a.no_finalize;
+    return a.chunk == 0 && (a.max_chunks == 1 || a.cluster > 1) && a.out == nullptr && !a.no_finalize;
 }
 
 // Merge of one unit's nw warp partials (fixed warp order, SoftmaxState::merge,
 // decode.cpp:59-75) by one warp into the latent output -- the combine kernel's
 // work for a single chunk.  The partials were written by this CTA's warps
 // before a CTA barrier.
+// Merged (m, l, acc) of one unit's nw warp partials, fixed warp order.
+template <int R>
+WSVD_DEV void unit_state(const AttnArgs& a, int bh, int ck, int nw, int lane, float& M, float& L,
+                         float (&acc)[(R + 31) / 32]) {
+    constexpr int RI = (R + 31) / 32;
+    const float* wsb = a.ws + (static_cast<size_t>(bh) * a.max_chunks + ck) * kMaxWarps * (R + 2);
+    M = -INFINITY;
+    for (int w = 0; w < nw; ++w) M = fmaxf(M, wsb[w * (R + 2) + R]);
+    L = 0.f;
+#pragma unroll
+    for (int i = 0; i < RI; ++i) acc[i] = 0.f;
+    for (int w = 0; w < nw; ++w) {
+        const float m = wsb[w * (R + 2) + R];
+        if (m == -INFINITY) continue;
+        const float f = ex2(m - M);
+        L = fmaf(wsb[w * (R + 2) + R + 1], f, L);
+#pragma unroll
+        for (int i = 0; i < RI; ++i)
+            if (lane + 32 * i < R) acc[i] = fmaf(wsb[w * (R + 2) + lane + 32 * i], f, acc[i]);
+    }
+}
+
+// Cluster merge (a.cluster = C CTAs = the C chunks of one (sequence, head),
+// one unit per CTA): chunk ck < C-1 writes its merged state into the last
+// CTA's shared memory (DSMEM) and arrives on its barrier; the last CTA merges
+// the chunks in chunk order and writes the latent output -- no combine launch.
+template <int R>
+WSVD_DEV void cluster_merge_unit(const AttnArgs& a, int bh, int ck, int nw, int lane, float* cst, uint64_t* cbar) {
+    constexpr int RI = (R + 31) / 32;
+    const int C = a.cluster;
+    float M, L, acc[RI];
+    unit_state<R>(a, bh, ck, nw, lane, M, L, acc);
+    if (ck < C - 1) {
+        const uint32_t dst = cluster_map(smem_u32(cst + ck * (R + 2)), static_cast<uint32_t>(C - 1));
+#pragma unroll
+        for (int i = 0; i < RI; ++i)
+            if (lane + 32 * i < R) st_cluster_f32(dst + 4u * (lane + 32 * i), acc[i]);
+        if (lane == 0) {
+            st_cluster_f32(dst + 4u * R, M);
+            st_cluster_f32(dst + 4u * (R + 1), L);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(cluster_map(smem_u32(cbar), static_cast<uint32_t>(C - 1)));
+        return;
+    }
+    mbar_wait_cluster(cbar, 0u);
+    float M2 = -INFINITY, L2 = 0.f, a2[RI];
+#pragma unroll
+    for (int i = 0; i < RI; ++i) a2[i] = 0.f;
+    for (int c = 0; c < C; ++c) {  // chunk order; the last chunk is this CTA's own state
+        const float mc = c < C - 1 ? cst[c * (R + 2) + R] : M;
+        const float lc = c < C - 1 ? cst[c * (R + 2) + R + 1] : L;
+        if (mc == -INFINITY) continue;
+        const float Mn = fmaxf(M2, mc);
+        const float fo = ex2(M2 - Mn), fc = ex2(mc - Mn);
+        L2 = fmaf(lc, fc, L2 * fo);
+#pragma unroll
+        for (int i = 0; i < RI; ++i) {
+            const float ac = c < C - 1 ? (lane + 32 * i < R ? cst[c * (R + 2) + lane + 32 * i] : 0.f) : acc[i];
+            a2[i] = fmaf(ac, fc, a2[i] * fo);
+        }
+        M2 = Mn;
+    }
+#pragma unroll
+    for (int i = 0; i < RI; ++i)
+        if (a.vlat && lane + 32 * i < R) a.vlat[static_cast<size_t>(bh) * R + lane + 32 * i] = a2[i] / L2;
+}
+
 template <int R>
 WSVD_DEV void finalize_unit(const AttnArgs& a, int bh, int nw, int lane) {
     constexpr int RI = (R + 31) / 32;  // latent columns per lane
@@ -756,6 +829,8 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
     // in-kernel merge (attn_finalizes): unit slots between the consumers and
     // the helper warp, 16 units deep
     __shared__ uint64_t ufull[16], uempty[16];
+    __shared__ uint64_t cbar;                  // cluster merge: the other chunks' states landed
+    __shared__ float cst[8 * (R + 2)];         // cluster merge: chunk states written by the peers
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const size_t cap = static_cast<size_t>(a.cap);
@@ -773,9 +848,11 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
             mbar_init(&ufull[i], C::NW);
             mbar_init(&uempty[i], 1);
         }
+        mbar_init(&cbar, a.cluster > 1 ? a.cluster - 1 : 1);
         fence_mbar_init();
     }
     __syncthreads();
+    if (a.cluster > 1) cluster_sync_all();  // every CTA's cbar is initialised before a remote arrive
     griddep_wait();  // the appended row, qt and the length come from the predecessor
     griddep_launch_dependents();
     const int len = *a.d_len + a.len_add;
@@ -834,7 +911,11 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
                 for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++jl) {
                     const int us = jl & 15;
                     mbar_wait(&ufull[us], static_cast<uint32_t>(jl >> 4) & 1u);
-                    finalize_unit<R>(a, unit_geom(u, nch, chunk, len).bh, C::NW, lane);
+                    const Unit ug = unit_geom(u, nch, chunk, len);
+                    if (a.cluster > 1)
+                        cluster_merge_unit<R>(a, ug.bh, ug.chunk, C::NW, lane, cst, &cbar);
+                    else
+                        finalize_unit<R>(a, ug.bh, C::NW, lane);
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&uempty[us]);
                 }
@@ -852,7 +933,16 @@ __global__ void __launch_bounds__(Cfg<CD, R, V>::THREADS, 1) decode_attn_kernel(
         float m_w = -INFINITY, l = 0.f;
         const int ns = (g.ntok + C::ST - 1) / C::ST;
 
-        if constexpr ((C::MMA || C::IMMA) && (V & 4)) {
+        if (g.ntok <= 0) {
+            // an empty trailing chunk (cluster mode at short lengths): no stage
+            // was issued for it; publish an empty state
+            float* wsp = a.ws + ((static_cast<size_t>(g.bh) * a.max_chunks + g.chunk) * kMaxWarps + warp) * (R + 2);
+            for (int j = lane; j < R; j += 32) wsp[j] = 0.f;
+            if (lane == 0) {
+                wsp[R] = -INFINITY;
+                wsp[R + 1] = 0.f;
+            }
+        } else if constexpr ((C::MMA || C::IMMA) && (V & 4)) {
             // pipeline probe (WSVD_ATTN_VARIANT bit 2): drain the stages without
             // computing -- the streaming ceiling of this producer structure
             const int ns = (g.ntok + C::ST - 1) / C::ST;
@@ -1083,7 +1173,7 @@ cudaError_t launch_v(const AttnArgs& a, cudaStream_t s) {
             if (e != cudaSuccess) return e;
             attr_set = true;
         }
-        cudaError_t e = launch_pdl(k, dim3(a.grid), dim3(C::THREADS), C::SMEM, s, a);
+        cudaError_t e = launch_pdl_cluster(k, dim3(a.grid), dim3(C::THREADS), C::SMEM, s, a.cluster, a);
         if (e != cudaSuccess) return e;
         if (attn_finalizes(a) && !(V & 4)) return cudaSuccess;  // merged in the kernel
         const int csmem = combine_smem(a.max_chunks, C::NW, R);
@@ -1187,6 +1277,48 @@ cudaError_t launch_attn_combine(const AttnArgs& a, int parts_per_chunk, cudaStre
     return launch_pdl(attn_combine_kernel, dim3(a.B * a.nh), dim3(128), csmem, s, a, parts_per_chunk);
 }
 
+template <int CD, int R>
+bool cluster_ok_t(int Cn) {
+    using C = Cfg<CD, R, 0>;
+    if constexpr (!C::OK) {
+        return false;
+    } else {
+        auto k = decode_attn_kernel<CD, R, 0>;
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = static_cast<unsigned>(Cn);
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(Cn);
+        cfg.blockDim = dim3(C::THREADS);
+        cfg.dynamicSmemBytes = C::SMEM;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        int n = 0;
+        if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        return n >= 1;
+    }
+}
+
+template <int CD>
+bool cluster_ok_cd(int R, int Cn) {
+    switch (R) {
+        case 16: return cluster_ok_t<CD, 16>(Cn);
+        case 32: return cluster_ok_t<CD, 32>(Cn);
+        case 48: return cluster_ok_t<CD, 48>(Cn);
+        case 64: return cluster_ok_t<CD, 64>(Cn);
+    }
+    return false;
+}
+
 cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s) {
     switch (a.cdtype) {
         case F32: return launch_cd<F32>(a, s);
@@ -1194,6 +1326,23 @@ cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s) {
         case I8: return launch_cd<I8>(a, s);
     }
     return cudaErrorInvalidValue;
+}
+
+bool attn_cluster_ok(int cdtype, int R, int Cn) {
+    static int memo[3][5][4] = {};  // 0 unknown, 1 yes, 2 no; [dtype][R/16][log2 C - 1]
+    const int ri = R / 16, ci = Cn == 2 ? 0 : Cn == 4 ? 1 : Cn == 8 ? 2 : 3;
+    if (R % 16 || ri < 1 || ri > 4 || ci > 2 || cdtype < 0 || cdtype > 2) return false;
+    int& m = memo[cdtype][ri][ci];
+    if (m == 0) {
+        bool ok = false;
+        switch (cdtype) {
+            case F32: ok = cluster_ok_cd<F32>(R, Cn); break;
+            case BF16: ok = cluster_ok_cd<BF16>(R, Cn); break;
+            case I8: ok = cluster_ok_cd<I8>(R, Cn); break;
+        }
+        m = ok ? 1 : 2;
+    }
+    return m == 1;
 }
 
 }  // namespace wsvd_k

@@ -407,6 +407,21 @@ int run_append(wsvd_cache_s* c, const float* x, int T, float* q_out, float* qt, 
 
 // out: per-head outputs (B_V applied) or null; vlat: latent outputs or null;
 // len_add: rows appended by this step but not yet committed to *d_len
+// Cluster size of the layer step's attention (latent outputs): few (sequence,
+// head) pairs get clusters of C CTAs, one unit each, C chunks per pair merged
+// through DSMEM in the kernel (no combine launch); 1 = not used.
+int attn_cluster_for(const wsvd_cache_s* c) {
+    static const bool no_cl = getenv("WSVD_ATTN_NOCLUSTER") != nullptr;  // A/B switch
+    static const bool no_fin = getenv("WSVD_ATTN_COMBINE") != nullptr;
+    const wsvd_layer_s* L = c->L;
+    if (no_cl || no_fin || c->chunk != 0 || c->attn_mode == WSVD_ATTN_EXPLICIT_TC) return 1;
+    const int pairs = c->B * L->d.n_heads;
+    for (int C = 8; C >= 2; C /= 2)
+        if (pairs * C <= c->grid)
+            return (C <= c->max_chunks && attn_cluster_ok(c->cdtype, L->R, C)) ? C : 1;
+    return 1;
+}
+
 int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStream_t s,
                   const float* q = nullptr) {
     wsvd_layer_s* L = c->L;
@@ -435,6 +450,18 @@ int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStr
     a.grid = c->grid;
     static const bool no_fin = getenv("WSVD_ATTN_COMBINE") != nullptr;
     a.no_finalize = no_fin ? 1 : 0;
+    // Few (sequence, head) pairs (e.g. one sequence): clusters of C CTAs, one
+    // unit each, C chunks per pair merged through DSMEM inside the kernel
+    // instead of the combine launch (layer step: latent outputs only)
+    a.cluster = 1;
+    if (out == nullptr && vlat != nullptr) {
+        const int cl = attn_cluster_for(c);
+        if (cl > 1) {
+            a.cluster = cl;
+            a.max_chunks = cl;  // <= the cache's max_chunks: every (sequence, head) ws slot exists
+            a.grid = c->B * L->d.n_heads * cl;
+        }
+    }
     if (c->attn_mode == WSVD_ATTN_EXPLICIT_TC) {
         // explicit key reconstruction on tcgen05 (attn_tc.cu), then the combine
         int rc = ensure_bkt(L);
@@ -1011,7 +1038,11 @@ int wsvd_cache_step_info(wsvd_cache_t c, int32_t* fused, int32_t* launches) {
         return WSVD_OK;
     }
     const int wd = L->d.weight_dtype;
-    int n = 4;                                               // projection, epilogue, attention, combine
+    int n = 3;                                               // projection, epilogue, attention
+    static const bool no_fin = getenv("WSVD_ATTN_COMBINE") != nullptr;
+    const bool merged = c->attn_mode != WSVD_ATTN_EXPLICIT_TC && c->chunk == 0 && !no_fin &&
+                        (c->max_chunks == 1 || attn_cluster_for(c) > 1);
+    if (!merged) n += 1;                                     // the split-KV combine
     if (wd == WSVD_I8 || wd == WSVD_I4) n += 1;              // activation quantiser
     n += 1;                                                  // O-projection GEMM
     if (L->oKp > 0 && L->oKp / L->oks > 1) n += 1;           // its split reduction

@@ -101,6 +101,8 @@ struct AttnArgs {
     int B, nh, H, R, cap, chunk, max_chunks, cdtype, row_bytes;
     int grid;               // persistent CTAs
     int no_finalize;        // A/B switch: always merge in the combine kernel (WSVD_ATTN_COMBINE=1)
+    int cluster;            // > 1: clusters of that many CTAs, one unit per CTA and exactly `cluster`
+                            // chunks per (sequence, head); the chunks merge through DSMEM
     // explicit key reconstruction (attn_tc.cu): per-head B_K^T tiles and the query
     const uint8_t* bkt;     // [nh][attn_tc_btile_bytes()] bf16, MMA B-operand layout
     const float* q;         // [B][nh][H] query rows
@@ -109,6 +111,8 @@ int attn_smem_bytes(int cdtype, int R);
 int attn_occupancy(int cdtype, int R);  // resident CTAs per SM (0 if unsupported)
 int attn_parts_per_chunk();             // warp partials published per unit
 cudaError_t launch_decode_attn(const AttnArgs& a, cudaStream_t s);
+// clusters of C attention CTAs can be scheduled (the cluster-merge mode)
+bool attn_cluster_ok(int cdtype, int R, int C);
 // split-KV combine alone (attn.cu): merges parts_per_chunk warp partials per chunk
 cudaError_t launch_attn_combine(const AttnArgs& a, int parts_per_chunk, cudaStream_t s);
 
