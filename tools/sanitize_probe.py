@@ -48,12 +48,15 @@ il.step(x, y, graph=False)
 torch.cuda.synchronize()
 print("int8 step ok", float(y.abs().max()))
 
-# fp32 weights, one token row: the row GEMV
-E, nh, B, L = 512, 8, 1, 200
+# fp32 weights, one sequence: the row GEMV and the 4-CTA-cluster attention
+# (chunks merged through DSMEM), at a length with empty trailing chunks too
+E, nh, B = 512, 32, 1
 lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
-fl = DecodeLayer(to_factors(lay), None, batch=B, capacity=L + 4, cache_dtype="f32", weight_dtype="f32")
-fl.fill_synthetic(L - 1)
-q = torch.empty((B, nh, H), device=dev)
-fl.append(torch.randn((B, E), device=dev), q)
-torch.cuda.synchronize()
-print("fp32 append ok", float(q.abs().max()))
+wo = O.bf16_round(rng.normal_matrix(nh * H, E, 1.0 / np.sqrt(nh * H)))
+for L in (200, 40):
+    fl = DecodeLayer(to_factors(lay), wo, batch=B, capacity=L + 4, cache_dtype="f32", weight_dtype="f32")
+    fl.fill_synthetic(L - 1)
+    y = torch.empty((B, E), device=dev)
+    fl.step(torch.randn((B, E), device=dev), y, graph=False)
+    torch.cuda.synchronize()
+    print("fp32 step ok", L, float(y.abs().max()))
