@@ -28,7 +28,6 @@ namespace wsvd_k {
 
 namespace {
 
-constexpr int kXThreads = 128;  // threads that stage the token slice
 
 template <int WT>
 struct GT;
@@ -59,7 +58,7 @@ __host__ __device__ __forceinline__ int x_stride(int KS) {
 // Stage X[:, k0:k0+KS] into shared memory (bf16 or int8), zero-padded to Mp
 // rows.  Loads are issued in batches of 8 per thread before any is consumed,
 // so staging costs one memory latency per batch rather than one per item.
-template <int WT>
+template <int WT, int kXThreads>
 WSVD_DEV void stage_x(const GemmArgs& a, uint8_t* xs, int k0, int Mp) {
     if (threadIdx.x >= kXThreads) return;  // the first kXThreads threads stage the slice
     const int stride = x_stride<WT>(a.KS);
@@ -222,7 +221,7 @@ __global__ void __launch_bounds__(StreamWarps<MT>::THREADS, 1) skinny_stream_ker
     // token slice, the partial outputs and the length commit do
     griddep_wait();
     griddep_launch_dependents();
-    stage_x<WT>(a, xbuf, s * KS, S::XROWS);
+    stage_x<WT, 32 * kStreamConsumers>(a, xbuf, s * KS, S::XROWS);  // every consumer thread stages
     named_bar_sync(1, 32 * kStreamConsumers);
 
     const int g = lane >> 2, t = lane & 3;
