@@ -214,19 +214,21 @@ def test_int8_cache_attention_long_context(monkeypatch, r, L, chunk, variant):
         assert rel_err_rows(out[b], ref) <= REL_TOL, f"b={b}"
 
 
-@pytest.mark.parametrize("cache,B,nh,L", [
-    ("i8", 37, 4, 300), ("f32", 37, 4, 300),   # 148 pairs = one per CTA: one chunk, helper-warp merge
-    ("f32", 1, 32, 300), ("i8", 1, 32, 300),   # 32 pairs: 4-CTA clusters, chunks merged through DSMEM
-    ("f32", 1, 32, 40),                        # ... with two empty trailing chunks
+@pytest.mark.parametrize("cache,B,nh,L,r", [
+    ("i8", 37, 4, 300, 32), ("f32", 37, 4, 300, 32),   # 148 pairs = one per CTA: one chunk, helper-warp merge
+    ("f32", 1, 32, 300, 32), ("i8", 1, 32, 300, 32),   # 32 pairs: 4-CTA clusters, chunks merged through DSMEM
+    ("f32", 1, 32, 40, 32),                            # ... with two empty trailing chunks
+    ("i8", 2, 8, 500, 48),                             # 16 pairs: 8-CTA clusters, r = 48
+    ("f32", 3, 16, 257, 16),                           # 48 pairs: 2-CTA clusters, r = 16
 ])
-def test_layer_step_in_kernel_merge(cache, B, nh, L):
+def test_layer_step_in_kernel_merge(cache, B, nh, L, r):
     """The layer step's attention merges its split-KV partials inside the
     kernel -- one chunk per pair (helper warp), or one cluster of CTAs per pair
     (DSMEM) -- with no combine launch: the layer step's y must equal append +
     attend (combine kernel, full-rank output) followed by the O-projection."""
     from paper_2604_02570_b200.layer import DecodeLayer
     rng = O.Rng(91 + B + L)
-    E, r, H = 512, 32, 128
+    E, H = 512, 128
     lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
     f = to_factors(lay)
     w_o = O.bf16_round(rng.normal_matrix(nh * H, E, 1.0 / np.sqrt(nh * H)))
