@@ -213,6 +213,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     uint64_t* wdone = wfull + 2 * C::NB;  // [NB] those items consumed: the stage is free
     uint64_t* pbar = wdone + C::NB;       // [kMaxU] unit j's peer chunk state landed (CTA pairs)
     uint64_t* b1bar = pbar + kMaxU;       // grid barrier 1 passed (gates the parked stages' refill)
+    static_assert((2 * kNA + 2 * C::NB + 2 * kMaxU + 1 + 2 * C::NB + C::NB + kMaxU + 1) * 8 <= C::SMEM - C::BAR_OFF,
+                  "mbarriers overflow their shared-memory region");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
