@@ -198,3 +198,32 @@ np.save(sys.argv[1], np.stack(ys))
         assert res.returncode == 0, res.stderr[-3000:]
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("E,nh,B,L", [(512, 8, 32, 700), (1024, 32, 8, 129), (512, 32, 16, 1030),
+                                      (1536, 24, 12, 333), (512, 4, 29, 95), (1024, 16, 31, 2049)])
+def test_fused_step_matches_multi_kernel_step(E, nh, B, L):
+    """Assorted shapes (different split-KV chunk counts, cluster and non-cluster
+    merges, parked-item counts, ragged batches): the fused step's y equals the
+    multi-kernel step's (attn_out forces the operator path) within the bf16
+    O-projection tolerance, and the caches agree row for row."""
+    H, r = 128, 32
+    rng, lay, wo, mk = _twin(E, nh, H, r, B, L + 4, 9000 + E + nh + B)
+    a, b = mk(), mk()
+    dev = torch.device("cuda", 0)
+    toks = torch.from_numpy(O.bf16_round(rng.normal_matrix(L * B, E)).reshape(L, B, E).astype(np.float32)).to(dev)
+    a.prefill(toks[:-1])
+    b.prefill(toks[:-1])
+    ya, yb = torch.empty((B, E), device=dev), torch.empty((B, E), device=dev)
+    attn = torch.empty((B, nh, H), device=dev)
+    a.step(toks[-1], ya)                  # fused persistent kernel
+    b.step(toks[-1], yb, attn_out=attn)   # multi-kernel operator path
+    torch.cuda.synchronize()
+    assert a.length() == b.length() == L
+    ya, yb = ya.cpu().numpy(), yb.cpu().numpy()
+    assert np.abs(ya - yb).max() <= 1e-2 * np.abs(yb).max()
+    for bb in (0, B - 1):
+        for h in (0, nh - 1):
+            ka, va = a.read_latents(bb, h)
+            kb, vb = b.read_latents(bb, h)
+            assert np.array_equal(ka, kb) and np.array_equal(va, vb)
