@@ -277,3 +277,28 @@ def test_prefill_large_matches_token_by_token_appends():
             kb, vb = b.read_latents(bb, h)
             assert np.abs(ka - kb).max() <= 1e-2 * np.abs(kb).max()
             assert np.abs(va - vb).max() <= 1e-2 * np.abs(vb).max()
+
+
+def test_attend_two_chunk_shape_matches_oracle():
+    """The operator-API attention (q -> full-rank head outputs) at a shape whose
+    split-KV uses two chunks per (sequence, head) (512 pairs over the grid),
+    merged by the combine kernel with the B_V up-projection."""
+    from paper_2604_02570_b200.layer import DecodeLayer
+    rng = O.Rng(777)
+    E, nh, H, r, B, L = 1024, 32, 128, 32, 16, 300
+    lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
+    layer = DecodeLayer(to_factors(lay), None, batch=B, capacity=L + 4, cache_dtype="bf16", weight_dtype="bf16")
+    dev = torch.device("cuda", 0)
+    toks = O.bf16_round(rng.normal_matrix(L * B, E)).reshape(L, B, E)
+    layer.prefill(torch.from_numpy(toks.astype(np.float32)).to(dev))
+    q = torch.from_numpy(rng.normal_matrix(B * nh, H).reshape(B, nh, H).astype(np.float32)).to(dev)
+    out = torch.empty((B, nh, H), device=dev)
+    layer.attend(q, out)
+    torch.cuda.synchronize()
+    out = out.cpu().numpy().astype(np.float64)
+    lb = lay.map(O.bf16_round)
+    for b in (0, 7, 15):
+        ck = np.stack([layer.read_latents(b, h)[0][:, :r] for h in range(nh)])
+        cv = np.stack([layer.read_latents(b, h)[1][:, :r] for h in range(nh)])
+        ref = O.fused_decode_step(lb, ck, cv, L, q[b].cpu().numpy().astype(np.float64), 32)
+        assert rel_err_rows(out[b], ref) <= REL_TOL, f"b={b}"
