@@ -257,26 +257,30 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     // be finite: every slot's first attention stage is copied whole (the cache
     // allocation has a stage of padding), so later partial stages leave finite
     // stale rows -- no zeroing of the ring in the prologue
-    if (tid == 0) {
-        for (int i = 0; i < kNA; ++i) {
-            mbar_init(&fullA[i], 1);
-            mbar_init(&emptyA[i], 1);
+    if (warp == 0) {
+        // the ~50 barrier inits spread over warp 0's lanes (serially they cost
+        // ~0.5 us in front of the first weight TMA)
+        if (lane < kNA) {
+            mbar_init(&fullA[lane], 1);
+            mbar_init(&emptyA[lane], 1);
         }
-        for (int i = 0; i < C::NB; ++i) {
-            mbar_init(&fullB[i], 1);
-            mbar_init(&emptyB[i], kNW);
+        if (lane < C::NB) {
+            mbar_init(&fullB[lane], 1);
+            mbar_init(&emptyB[lane], kNW);
+            // stage `lane` parks items 4 + 2 lane and 4 + 2 lane + 1
+            mbar_init(&wdone[lane], lane < nWS ? min(2, nBH - 2 * lane) : 1);
         }
-        for (int i = 0; i < kMaxU; ++i) {
-            mbar_init(&uready[i], 1);
-            mbar_init(&sfull[i], kNW);
+        if (lane < kMaxU) {
+            mbar_init(&uready[lane], 1);
+            mbar_init(&sfull[lane], kNW);
+            mbar_init(&pbar[lane], 1);
         }
-        mbar_init(p3bar, 1);
-        for (int b = 0; b < nBH; ++b) mbar_init(&wfull[b], 1);
-        for (int st = 0; st < C::NB; ++st)  // stage st parks items 4+2st and 4+2st+1
-            mbar_init(&wdone[st], st < nWS ? min(2, nBH - 2 * st) : 1);
-        for (int j = 0; j < kMaxU; ++j) mbar_init(&pbar[j], 1);
-        mbar_init(b1bar, 1);
-        fence_mbar_init();
+        if (lane < nBH) mbar_init(&wfull[lane], 1);
+        if (lane == 0) {
+            mbar_init(p3bar, 1);
+            mbar_init(b1bar, 1);
+        }
+        fence_mbar_init();  // every lane: the fence covers the executing thread's inits
     }
     __syncthreads();
     if (a.cluster > 1) cluster_sync_all();  // the peer's barriers are initialised before any remote arrive
