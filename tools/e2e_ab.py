@@ -1,8 +1,19 @@
-import os, sys, time
-sys.path.insert(0, "/root/repo")
-import numpy as np, torch
-import bench
-from paper_2604_02570_b200.layer import DecodeLayer
+"""Wall time per host-buffer layer step (wsvd_layer_step_host) at the headline
+shape: 5 trials x 200 steps, min and median -- for A/B runs of the host path
+through environment switches (MODE=<label> names the line).
+
+    MODE=zc WSVD_HOST_ZEROCOPY=1 python tools/e2e_ab.py
+"""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2604_02570_b200.layer import DecodeLayer  # noqa: E402
 cfg = bench.CONFIGS[bench.DEFAULT_CONFIG]
 E, B, L = cfg["E"], cfg["B"], cfg["L"]
 f, w_o = bench.synthetic_layer(cfg)
