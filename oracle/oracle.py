@@ -87,6 +87,8 @@ def lib():
                                          C.c_int]
         L.orc_batched_decode.argtypes = [C.POINTER(OrcLayer), _dp, _dp, _sz, _sz, _sz, _dp, _sz,
                                          _dp, C.c_int]
+        L.orc_batched_decode_latent.argtypes = [C.POINTER(OrcLayer), _dp, _dp, _sz, _sz, _sz, _dp,
+                                                _sz, _dp, _dp, C.c_int]
         L.orc_bf16_bits.restype = C.c_uint16
         L.orc_bf16_bits.argtypes = [C.c_float]
         L.orc_f16_bits.restype = C.c_uint16
@@ -287,6 +289,37 @@ def batched_decode(layer: Layer, ck, cv, length: int, q, tile: int = 32, threads
                                   ck.shape[2], length, _ptr(q, _dp), tile, _ptr(out, _dp), threads)
     assert rc == 0
     return out
+
+
+def batched_decode_latent(layer: Layer, ck, cv, length: int, q, tile: int = 32, threads: int = 1):
+    """As batched_decode, also returning the latent outputs v~ = acc/denom
+    (decode.cpp:198) [B,nh,rmax] -- what the folded O-projection multiplies."""
+    Bn = ck.shape[0]
+    out = np.zeros((Bn, layer.nh, layer.H))
+    lat = np.zeros((Bn, layer.nh, layer.rmax))
+    q = np.ascontiguousarray(q, dtype=np.float64)
+    ck = np.ascontiguousarray(ck, dtype=np.float64)
+    cv = np.ascontiguousarray(cv, dtype=np.float64)
+    rc = lib().orc_batched_decode_latent(C.byref(layer.c()), _ptr(ck, _dp), _ptr(cv, _dp), Bn,
+                                         ck.shape[2], length, _ptr(q, _dp), tile, _ptr(out, _dp),
+                                         _ptr(lat, _dp), threads)
+    assert rc == 0
+    return out, lat
+
+
+def fold_oproj(layer: Layer, w_o, rpad: int, storage=None):
+    """W'_o = blockdiag_h(B_V,h) . W_o  ((nh*rpad) x e_out) from the factor
+    values the device stores, as wsvd_layer_set_oproj folds it (fp64 sums),
+    then the device's storage rounding (bf16_round for a bf16 O-projection).
+    heads_row . W_o (pipeline.cpp:323-329) = v~ . W'_o exactly in real
+    arithmetic: the fold only moves where the bf16 weight rounding happens."""
+    nh, H = layer.nh, layer.H
+    w_o = np.asarray(w_o, dtype=np.float64)
+    fold = np.zeros((nh * rpad, w_o.shape[1]))
+    for h in range(nh):
+        rv = int(layer.ranks[h, 2])
+        fold[h * rpad:h * rpad + rv] = layer.B[h, 2, :rv, :] @ w_o[h * H:(h + 1) * H]
+    return storage(fold) if storage is not None else fold
 
 
 def batched_append(layer: Layer, ck, cv, pos: int, x, threads: int = 1):

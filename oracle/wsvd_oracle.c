@@ -218,7 +218,7 @@ int orc_append_token(const orc_layer* f, double* ck, double* cv, size_t cap, siz
 /* One head of fused_decode_step (decode.cpp:168-204). */
 static void decode_head(const orc_layer* f, size_t h, const double* ck_h, const double* cv_h,
                         size_t len, const double* q_h, size_t tile, double* out_h,
-                        orc_counter* c, double* scratch) {
+                        orc_counter* c, double* scratch, double* latent_h) {
     const size_t H = f->H, R = f->rmax;
     const size_t rk = rank_of(f, h, 1), rv = rank_of(f, h, 2);
     const double* bk = fb(f, h, 1);
@@ -248,6 +248,9 @@ static void decode_head(const orc_layer* f, size_t h, const double* ck_h, const 
         orc_softmax_merge(&state, &local);
     }
     for (size_t i = 0; i < rv; ++i) latent_out[i] = state.acc[i] / state.denom;
+    if (latent_h) { /* the latent output v~ = acc / denom (decode.cpp:198), before B_V */
+        for (size_t i = 0; i < R; ++i) latent_h[i] = i < rv ? latent_out[i] : 0.0;
+    }
     vec_mat(latent_out, rv, bv, H, H, out_h);
     counter_add(c, 2, ORC_OUTPUT, rv * H);
     counter_add(c, 1, ORC_OUTPUT, H);
@@ -261,7 +264,7 @@ int orc_fused_decode_step(const orc_layer* f, const double* ck, const double* cv
     double* scratch = (double*)malloc((f->H + 3 * f->rmax) * sizeof(double));
     for (size_t h = 0; h < f->nh; ++h) {
         decode_head(f, h, ck + h * cap * f->rmax, cv + h * cap * f->rmax, len, q + h * f->H, tile,
-                    out + h * f->H, c, scratch);
+                    out + h * f->H, c, scratch, NULL);
     }
     free(scratch);
     return 0;
@@ -327,6 +330,7 @@ typedef struct {
     const double* q;
     double* qo;
     double* out;
+    double* lat; /* decode: [B][nh][rmax] latent outputs, or NULL */
     size_t next;
     pthread_mutex_t mu;
     int mode; /* 0 append, 1 decode */
@@ -350,7 +354,7 @@ static void* batch_worker(void* arg) {
         } else {
             decode_head(f, h, j->ckc + cache_off, j->cvc + cache_off, j->len,
                         j->q + (b * f->nh + h) * H, j->tile, j->out + (b * f->nh + h) * H, NULL,
-                        scratch);
+                        scratch, j->lat ? j->lat + (b * f->nh + h) * R : NULL);
         }
     }
     free(scratch);
@@ -387,6 +391,20 @@ int orc_batched_decode(const orc_layer* f, const double* ck, const double* cv, s
     batch_job j;
     memset(&j, 0, sizeof j);
     j.f = f; j.ckc = ck; j.cvc = cv; j.B = B; j.cap = cap; j.len = len; j.q = q; j.out = out;
+    j.tile = tile > len ? len : tile;
+    j.mode = 1;
+    return run_batch(&j, threads);
+}
+
+int orc_batched_decode_latent(const orc_layer* f, const double* ck, const double* cv, size_t B,
+                              size_t cap, size_t len, const double* q, size_t tile, double* out,
+                              double* latent, int threads) {
+    if (len == 0) return -1;
+    if (tile == 0) return -2;
+    batch_job j;
+    memset(&j, 0, sizeof j);
+    j.f = f; j.ckc = ck; j.cvc = cv; j.B = B; j.cap = cap; j.len = len; j.q = q; j.out = out;
+    j.lat = latent;
     j.tile = tile > len ? len : tile;
     j.mode = 1;
     return run_batch(&j, threads);

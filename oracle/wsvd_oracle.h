@@ -109,6 +109,12 @@ int orc_batched_append(const orc_layer* f, double* ck, double* cv, size_t B, siz
 int orc_batched_decode(const orc_layer* f, const double* ck, const double* cv, size_t B,
                        size_t cap, size_t len, const double* q, size_t tile, double* out,
                        int threads);
+/* the same, also returning every (sequence, head)'s latent output
+ * v~ = acc / denom (decode.cpp:198, before the B_V up-projection),
+ * latent [B][nh][rmax] (zero past the head's V rank) */
+int orc_batched_decode_latent(const orc_layer* f, const double* ck, const double* cv, size_t B,
+                              size_t cap, size_t len, const double* q, size_t tile, double* out,
+                              double* latent, int threads);
 
 /* ------------------------------------------------- storage-format rules ---
  * The device stores factors, tokens and latents in narrower formats; the

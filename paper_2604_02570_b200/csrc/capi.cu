@@ -479,33 +479,41 @@ int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStr
 
 // y = vlat . (B_V W_o): the V-path up-projection folded into the output
 // projection (SPEC section 3.4, "B_Vh is fused into the output projection").
+// bf16 W'_o: the fp32 latents enter the tensor cores as hi + lo bf16 token
+// tiles (xsplit), 64 sequences per GEMM launch.
 int run_oproj(wsvd_cache_s* c, const float* vlat, float* y, int* commit_len, cudaStream_t s) {
     wsvd_layer_s* L = c->L;
     if (!L->Wo.p) return set_err(WSVD_ECONFIG, "layer has no O-projection (wsvd_layer_set_oproj)");
     const int K = L->d.n_heads * L->R;
-    // the folded O-projection is short (K = nh*R <= 1024 at 7B): one K split,
-    // each 16-row tile is one work item and the GEMM writes y directly
+    const bool split = L->o_dtype == BF16;
+    const int mchunk = split ? 64 : c->B;
     const int ks = L->oks;
-    if (!gemm_fits(L->o_dtype, c->B, ks))
+    if (!gemm_fits(L->o_dtype, split ? 2 * std::min(c->B, mchunk) : c->B, ks))
         return set_err(WSVD_ECONFIG, "batch of " + std::to_string(c->B) + " does not fit the O-projection kernel");
     const int splits = L->oKp / ks;
     const size_t need = static_cast<size_t>(splits) * c->B * L->e_out * 4;
     if (c->oP.n < need) CUDA_TRY(c->oP.alloc(need));
-    GemmArgs g{};
-    g.W = L->Wo.p;
-    g.X = vlat;
-    g.P = splits == 1 ? static_cast<void*>(y) : c->oP.p;
-    g.commit_len = commit_len;
-    g.M = c->B;
-    g.N = L->e_out;
-    g.K = K;
-    g.Kp = L->oKp;
-    g.KS = ks;
-    g.ldx = K;
-    g.wdtype = L->o_dtype;
-    g.grid = c->sms;
-    CUDA_TRY(launch_gemm(g, s));
-    if (splits > 1) CUDA_TRY(launch_reduce_partials(c->oP.as<float>(), splits, c->B, L->e_out, y, s));
+    for (int m0 = 0; m0 < c->B; m0 += mchunk) {
+        const int M = std::min(mchunk, c->B - m0);
+        GemmArgs g{};
+        g.W = L->Wo.p;
+        g.X = vlat + static_cast<size_t>(m0) * K;
+        float* yc = y + static_cast<size_t>(m0) * L->e_out;
+        float* pc = c->oP.as<float>() + static_cast<size_t>(splits) * m0 * L->e_out;  // [splits][M][N] per chunk
+        g.P = splits == 1 ? static_cast<void*>(yc) : static_cast<void*>(pc);
+        g.commit_len = m0 == 0 ? commit_len : nullptr;
+        g.M = M;
+        g.N = L->e_out;
+        g.K = K;
+        g.Kp = L->oKp;
+        g.KS = ks;
+        g.ldx = K;
+        g.wdtype = L->o_dtype;
+        g.grid = c->sms;
+        g.xsplit = split ? 1 : 0;
+        CUDA_TRY(launch_gemm(g, s));
+        if (splits > 1) CUDA_TRY(launch_reduce_partials(pc, splits, M, L->e_out, yc, s));
+    }
     return WSVD_OK;
 }
 
@@ -517,8 +525,47 @@ bool fused_step_ok(wsvd_cache_s* c) {
     if (L->ks != step_item_k() || L->oks != step_item_k()) return false;
     // the chunk count never exceeds max_chunks (adaptive) or the capacity split (fixed chunk)
     const int mc = c->chunk > 0 ? c->max_chunks : c->fmax_chunks;
+    // one CTA per SM must be resident (grid barriers): probed once per batch tile
+    static int occ[3] = {-1, -1, -1};
+    const int mt = (c->B + 15) / 16;
+    if (mt >= 1 && mt <= 2 && occ[mt] < 0) occ[mt] = step_resident_ctas_per_sm(c->B);
+    if (mt >= 1 && mt <= 2 && occ[mt] < 1) return false;
     return step_supported(L->R, c->B, L->d.n_heads, c->B * L->d.n_heads * mc, mc, L->Kp, L->oKp,
                           round_up(L->e_out, 16) / 16, c->sms);
+}
+
+// The fused step's grid barriers need all of its CTAs (one per SM) resident
+// at once, so two fused steps must never run concurrently on one device (each
+// would hold some SMs and wait for the other's).  Steps on one stream are
+// ordered anyway; when a fused step is issued on a different stream than the
+// device's previous one, the new stream first waits for everything issued on
+// the old one.  Nothing is recorded in the steady state (one stream), so the
+// PDL overlap of back-to-back steps is untouched.
+struct FusedOrder {
+    std::mutex mu;
+    cudaStream_t last = nullptr;
+    bool any = false;
+    cudaEvent_t ev = nullptr;
+};
+
+int fused_serialize(int device, cudaStream_t s) {
+    static FusedOrder order[64];
+    if (device < 0 || device >= 64) return WSVD_OK;
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) {
+        cudaGetLastError();
+        return WSVD_OK;  // inside a caller's graph: the graph's own edges order it
+    }
+    FusedOrder& o = order[device];
+    std::lock_guard<std::mutex> lk(o.mu);
+    if (o.any && o.last != s) {
+        if (!o.ev) CUDA_TRY(cudaEventCreateWithFlags(&o.ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(o.ev, o.last));
+        CUDA_TRY(cudaStreamWaitEvent(s, o.ev, 0));
+    }
+    o.last = s;
+    o.any = true;
+    return WSVD_OK;
 }
 
 // the whole step as one persistent kernel (step.cu)
@@ -576,6 +623,8 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bo
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
     if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 12 * 8));
     a.trace = trace ? c->trace.as<uint64_t>() : nullptr;
+    rc = fused_serialize(L->d.device, s);
+    if (rc) return rc;
     CUDA_TRY(launch_layer_step(a, s));
     c->P_M = c->B;
     c->P_splits = splits;
@@ -756,7 +805,14 @@ static int upload_head(wsvd_layer_t L, int head, int role, const std::vector<int
             }
     }
     L->mqk_ready = false;
+    L->bkt_ready = false;
     L->gen += 1;
+    if (role == 2 && L->Wo.p) {
+        // W'_o = B_V . W_o was folded from the previous V factors: drop it, so
+        // a layer step fails with ECONFIG until wsvd_layer_set_oproj refolds
+        L->Wo.alloc(0);
+        L->e_out = 0;
+    }
     CUDA_TRY(cudaMemcpy(L->B[role].as<uint8_t>() + static_cast<size_t>(head) * R * H * bel, bh.data(), bh.size(),
                         cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(L->b_scale[role].as<float>() + static_cast<size_t>(head) * H, bsc.data(), H * 4,
@@ -1044,8 +1100,9 @@ int wsvd_cache_step_info(wsvd_cache_t c, int32_t* fused, int32_t* launches) {
                         (c->max_chunks == 1 || attn_cluster_for(c) > 1);
     if (!merged) n += 1;                                     // the split-KV combine
     if (wd == WSVD_I8 || wd == WSVD_I4) n += 1;              // activation quantiser
-    n += 1;                                                  // O-projection GEMM
-    if (L->oKp > 0 && L->oKp / L->oks > 1) n += 1;           // its split reduction
+    const int ochunks = L->o_dtype == BF16 ? (c->B + 63) / 64 : 1;  // run_oproj: 64 sequences per GEMM
+    n += ochunks;                                            // O-projection GEMM
+    if (L->oKp > 0 && L->oKp / L->oks > 1) n += ochunks;     // its split reduction
     *fused = 0;
     *launches = n;
     return WSVD_OK;
@@ -1222,6 +1279,7 @@ int wsvd_layer_step(wsvd_cache_t c, const float* x, float* attn_out, float* y, v
     if (!c || !x || !y) return set_err(WSVD_ECONFIG, "null argument");
     int rc = check_layer(c->L);
     if (rc) return rc;
+    if (!c->L->Wo.p) return set_err(WSVD_ECONFIG, "layer has no O-projection folded from its current V factors (wsvd_layer_set_oproj)");
     if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
     CUDA_TRY(cudaSetDevice(c->L->d.device));
     rc = layer_step_impl(c, x, attn_out, y, static_cast<cudaStream_t>(stream));
@@ -1234,6 +1292,7 @@ int wsvd_layer_step_graph(wsvd_cache_t c, const float* x, float* y, void* stream
     if (!c || !x || !y) return set_err(WSVD_ECONFIG, "null argument");
     int rc = check_layer(c->L);
     if (rc) return rc;
+    if (!c->L->Wo.p) return set_err(WSVD_ECONFIG, "layer has no O-projection folded from its current V factors (wsvd_layer_set_oproj)");
     if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
     CUDA_TRY(cudaSetDevice(c->L->d.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1248,7 +1307,9 @@ int wsvd_layer_step_graph(wsvd_cache_t c, const float* x, float* y, void* stream
     const bool same = c->gkey.x == x && c->gkey.y == y && c->gkey.s == s &&
                       c->ggen == c->L->gen && c->gmode == c->attn_mode;
     if (c->gexec && same) {
-        CUDA_TRY(cudaGraphLaunch(c->gexec, c->gstream ? c->gstream : s));
+        // replay on the caller's stream (the graph was captured on it); the
+        // owned stream only stands in for the legacy default stream
+        CUDA_TRY(cudaGraphLaunch(c->gexec, s ? s : c->gstream));
         c->len += 1;
         return WSVD_OK;
     }

@@ -419,7 +419,15 @@ int wsvd_layer_load_checkpoint(const char* dir, int32_t layer, int32_t head_begi
             const JVal* wb = m.j.find("weight_bits");
             const long long bits = wb ? wb->integer() : 0;
             if (!m.j.find("quantized")) throw IoErr("checkpoint holds no quantised factors");
-            if ((weight_dtype == WSVD_I8) != (bits == 8)) throw IoErr("requested weight format differs from the checkpoint's bits");
+            const long long want = weight_dtype == WSVD_I8 ? 8 : 4;
+            if (bits != want)
+                throw IoErr("requested " + std::to_string(want) + "-bit weights, the checkpoint holds " +
+                            std::to_string(bits) + "-bit ones");
+            // the device quantises activations per token to 8 bits (quant.cpp:131-150)
+            const JVal* ab = m.j.find("activation_bits");
+            if (ab && ab->integer() != 8)
+                throw IoErr("checkpoint expects " + std::to_string(ab->integer()) +
+                            "-bit activations; the device path quantises activations to 8 bits");
         }
         const int nh = head_end - head_begin;
         std::vector<int32_t> ranks(static_cast<size_t>(nh) * 3);

@@ -95,6 +95,42 @@ inline cudaError_t launch_pdl_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// the same with every CTA guaranteed co-resident (cooperative launch): for
+// persistent kernels that wait at a grid-wide barrier.  The launch fails with
+// cudaErrorCooperativeLaunchTooLarge instead of hanging when the grid cannot
+// be resident at once (SMs held by another context, MPS / green-context
+// limits).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_coop_cluster(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                       int cluster, Args&&... args) {
+    cudaLaunchAttribute attr[3];
+    int n = 0;
+    if (cluster > 1) {
+        attr[n].id = cudaLaunchAttributeClusterDimension;
+        attr[n].val.clusterDim.x = static_cast<unsigned>(cluster);
+        attr[n].val.clusterDim.y = 1;
+        attr[n].val.clusterDim.z = 1;
+        ++n;
+    }
+    attr[n].id = cudaLaunchAttributeCooperative;
+    attr[n].val.cooperative = 1;
+    ++n;
+    static const bool off = std::getenv("WSVD_NO_PDL") != nullptr;
+    if (!off) {
+        attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cfg.attrs = attr;
+    cfg.numAttrs = n;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // ---------------------------------------------------------- cache swizzle
 // Latent-cache rows are stored with the 128-byte XOR swizzle applied to the
 // byte offset inside each (sequence, head) region: 16-byte unit u of every

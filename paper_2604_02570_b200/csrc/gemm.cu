@@ -58,6 +58,16 @@ __host__ __device__ __forceinline__ int x_stride(int KS) {
 // Stage X[:, k0:k0+KS] into shared memory (bf16 or int8), zero-padded to Mp
 // rows.  Loads are issued in batches of 8 per thread before any is consumed,
 // so staging costs one memory latency per batch rather than one per item.
+// With a.xsplit (bf16 mode, O-projection input): rows [0, Mp/2) hold
+// hi = bf16(x) of token rows 0.., rows [Mp/2, Mp) lo = bf16(x - hi) of the
+// same tokens; the epilogue adds the two products (~16 mantissa bits of the
+// fp32 activation reach the tensor cores).
+WSVD_DEV uint32_t pack_lo_bf16x2(float a, float b) {
+    const float ha = __bfloat162float(__float2bfloat16_rn(a));
+    const float hb = __bfloat162float(__float2bfloat16_rn(b));
+    return pack_bf16x2(a - ha, b - hb);
+}
+
 template <int WT, int kXThreads>
 WSVD_DEV void stage_x(const GemmArgs& a, uint8_t* xs, int k0, int Mp) {
     if (threadIdx.x >= kXThreads) return;  // the first kXThreads threads stage the slice
@@ -75,9 +85,10 @@ WSVD_DEV void stage_x(const GemmArgs& a, uint8_t* xs, int k0, int Mp) {
                 const int i = i0 + u * kXThreads;
                 const int m = i / per_row, kk = (i - m * per_row) * 8;
                 const int k = k0 + kk;
+                const int ms = (a.xsplit && m >= Mp / 2) ? m - Mp / 2 : m;  // source token row
                 p[u][0] = p[u][1] = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (i < n && m < a.M) {
-                    const float* src = X + static_cast<size_t>(m) * a.ldx + k;
+                if (i < n && ms < a.M && (!a.xsplit || ms < Mp / 2)) {
+                    const float* src = X + static_cast<size_t>(ms) * a.ldx + k;
                     if (k + 8 <= a.K && vec) {
                         p[u][0] = __ldg(reinterpret_cast<const float4*>(src));
                         p[u][1] = __ldg(reinterpret_cast<const float4*>(src + 4));
@@ -96,8 +107,13 @@ WSVD_DEV void stage_x(const GemmArgs& a, uint8_t* xs, int k0, int Mp) {
                 if (i >= n) break;
                 const int m = i / per_row, kk = (i - m * per_row) * 8;
                 uint4 o;
-                o.x = pack_bf16x2(p[u][0].x, p[u][0].y); o.y = pack_bf16x2(p[u][0].z, p[u][0].w);
-                o.z = pack_bf16x2(p[u][1].x, p[u][1].y); o.w = pack_bf16x2(p[u][1].z, p[u][1].w);
+                if (a.xsplit && m >= Mp / 2) {
+                    o.x = pack_lo_bf16x2(p[u][0].x, p[u][0].y); o.y = pack_lo_bf16x2(p[u][0].z, p[u][0].w);
+                    o.z = pack_lo_bf16x2(p[u][1].x, p[u][1].y); o.w = pack_lo_bf16x2(p[u][1].z, p[u][1].w);
+                } else {
+                    o.x = pack_bf16x2(p[u][0].x, p[u][0].y); o.y = pack_bf16x2(p[u][0].z, p[u][0].w);
+                    o.z = pack_bf16x2(p[u][1].x, p[u][1].y); o.w = pack_bf16x2(p[u][1].z, p[u][1].w);
+                }
                 *reinterpret_cast<uint4*>(xs + m * stride + kk * 2) = o;
             }
         }
@@ -287,6 +303,22 @@ __global__ void __launch_bounds__(StreamWarps<MT>::THREADS, 1) skinny_stream_ker
         if (lane == 0) mbar_arrive(&empty[slot]);
         // D fragment: (row g | g+8, token 2t | 2t+1) of each m16n8 tile
         const size_t pbase = static_cast<size_t>(s) * a.M * a.N;
+        if (WT == BF16 && MT % 2 == 0 && a.xsplit) {
+            // token tile mt holds hi, mt + MT/2 lo of the same tokens
+#pragma unroll
+            for (int mt = 0; mt < MT / 2; ++mt)
+#pragma unroll
+                for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int n = tile * 16 + g + ((i & 2) ? 8 : 0);
+                        const int m = mt * 16 + hh * 8 + 2 * t + (i & 1);
+                        if (n < a.N && m < a.M)
+                            reinterpret_cast<float*>(a.P)[pbase + static_cast<size_t>(m) * a.N + n] =
+                                facc[mt][hh][i] + facc[mt + MT / 2][hh][i];
+                    }
+            continue;
+        }
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -477,6 +509,15 @@ cudaError_t launch_stream(const GemmArgs& a, cudaStream_t s) {
 
 template <int WT>
 cudaError_t launch_wt(const GemmArgs& a, cudaStream_t s) {
+    if (a.xsplit) {  // hi and lo token tiles: twice the token rows (M <= 64)
+        if (WT != BF16) return cudaErrorInvalidValue;
+        switch ((a.M + 15) / 16) {
+            case 1: return launch_stream<WT, 2>(a, s);
+            case 2: return launch_stream<WT, 4>(a, s);
+            case 3: case 4: return launch_stream<WT, 8>(a, s);
+        }
+        return cudaErrorInvalidValue;
+    }
     switch ((a.M + 15) / 16) {
         case 1: return launch_stream<WT, 1>(a, s);
         case 2: return launch_stream<WT, 2>(a, s);

@@ -25,6 +25,7 @@ struct GemmArgs {
     int wdtype;      // DType
     int grid;        // SM count: the streaming kernel runs floor(grid/splits)*splits CTAs
     int* commit_len; // non-null: one thread adds 1 to it (the layer step's length commit)
+    int xsplit;      // bf16 only: X as hi + lo bf16 token tiles (fp32-grade activations), M <= 64
 };
 // true when M token rows with split KS fit the streaming kernel's shared memory
 bool gemm_fits(int wdtype, int M, int KS);
@@ -153,6 +154,7 @@ bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp,
 int step_item_k();
 size_t step_xo_bytes(int B, int oKp);  // bytes of StepArgs::xo
 int step_max_units();  // attention units one CTA of the fused step can hold
+int step_resident_ctas_per_sm(int B);  // occupancy of the fused step kernel (>= 1 to run)
 cudaError_t launch_layer_step(const StepArgs& a, cudaStream_t s);
 int step_pair_clusters_ok(int B, int grid);  // 1 when the grid can run as resident CTA pairs
 

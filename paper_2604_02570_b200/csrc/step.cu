@@ -59,6 +59,7 @@ struct SC {
     static constexpr int PART = 2 * R;
     static constexpr int STAGE = kST * ROWB;
     static constexpr int XB = MT * 16 * kXS;               // one staged X slice
+    static constexpr int XB2 = 2 * XB;                     // an O-projection X slice: hi rows, then lo rows
     // per-unit scratch: absorbed queries, the new token's row, the warp states
     // + [kMaxU][R+2] chunk states a cluster peer writes through DSMEM
     static constexpr int RED = kMaxU * (R * 4 + 4 * R + kNW * (R + 2) * 4 + (R + 2) * 4);
@@ -601,11 +602,17 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 L = L2;
                 if (lane == 0) a.counters[bh] = 0;  // self-resetting for the next step
             }
-            // latent output -> X row of the O-projection (bf16, K index h*R + lane)
+            // latent output -> X rows of the O-projection, K index h*R + lane:
+            // hi = bf16(v) in row b, lo = bf16(v - hi) in row MT*16 + b (~16
+            // mantissa bits of the fp32 latent reach the tensor cores)
             const int b = bh / a.nh, h = bh - b * a.nh;
             const int k = h * R + lane, s = k / kKS;
-            __nv_bfloat16* xr = reinterpret_cast<__nv_bfloat16*>(a.xo + (static_cast<size_t>(s) * MT * 16 + b) * kXS);
-            xr[k - s * kKS] = __float2bfloat16_rn(av / L);
+            const float vo = av / L;
+            const __nv_bfloat16 vh = __float2bfloat16_rn(vo);
+            const __nv_bfloat16 vl = __float2bfloat16_rn(vo - __bfloat162float(vh));
+            uint8_t* xs = a.xo + static_cast<size_t>(s) * C::XB2;
+            reinterpret_cast<__nv_bfloat16*>(xs + static_cast<size_t>(b) * kXS)[k - s * kKS] = vh;
+            reinterpret_cast<__nv_bfloat16*>(xs + static_cast<size_t>(MT * 16 + b) * kXS)[k - s * kKS] = vl;
         }
     } else {
         // ========================================================= consumer warps
@@ -754,23 +761,24 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         // xo was written by other CTAs' generic stores (ordered by barrier 2);
         // order them before this thread's async-proxy reads
         asm volatile("fence.proxy.async.global;" ::: "memory");
-        mbar_arrive_expect_tx(p3bar, static_cast<uint32_t>(osplits * C::XB));
+        mbar_arrive_expect_tx(p3bar, static_cast<uint32_t>(osplits * C::XB2));
         for (int s = 0; s < osplits; ++s)
-            tma_bulk_g2s(ringB + s * C::XB, a.xo + static_cast<size_t>(s) * C::XB, C::XB, p3bar);
+            tma_bulk_g2s(ringB + s * C::XB2, a.xo + static_cast<size_t>(s) * C::XB2, C::XB2, p3bar);
     }
     mbar_wait(p3bar, 0u);
     named_bar_sync(2, 32 * kNW);
     STEP_MARK(8);
     // item j = (tile i = j / osplits, split s = j % osplits) -> partial tile in
     // shared memory, then the splits are summed in split order
-    float* part = reinterpret_cast<float*>(ringB + osplits * C::XB);  // [np3][16 rows][MT*16 tokens]
+    float* part = reinterpret_cast<float*>(ringB + osplits * C::XB2);  // [np3][16 rows][MT*16 tokens]
     for (int j = 0; j < np3; ++j) {
         const int k = nA1 + j, slot = k % kNA;
         if (slot != warp) continue;
         mbar_wait(&fullA[slot], static_cast<uint32_t>(k / kNA) & 1u);
         const int s = j % osplits;
-        float facc[MT][2][4];
-        item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(ringB + s * C::XB), lane, facc);
+        // token columns 0..MT*16-1 are the hi rows, MT*16.. the lo rows
+        float facc[2 * MT][2][4];
+        item_mma<2 * MT>(smem_u32(ringA + slot * kItem), smem_u32(ringB + s * C::XB2), lane, facc);
         float* pj = part + j * 16 * MT * 16;
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
@@ -780,7 +788,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
                 for (int i = 0; i < 4; ++i) {
                     const int n = g8 + ((i & 2) ? 8 : 0);
                     const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
-                    pj[n * MT * 16 + m] = facc[mt][hh][i];
+                    pj[n * MT * 16 + m] = facc[mt][hh][i] + facc[mt + MT][hh][i];
                 }
     }
     named_bar_sync(2, 32 * kNW);
@@ -832,6 +840,13 @@ cudaError_t launch_mt(const StepArgs& a, cudaStream_t s) {
             if (e != cudaSuccess) return e;
             attr = true;
         }
+        // grid barriers need every CTA resident: one CTA per SM fits (the host
+        // checks occupancy once and serialises fused steps of different
+        // streams, capi.cu fused_serialize).  A cooperative launch would
+        // guarantee it in hardware but costs ~3.5 us per step on B200
+        // (59.0 vs 55.5 us, r02_coop.txt); WSVD_STEP_COOP=1 selects it.
+        static const bool coop = std::getenv("WSVD_STEP_COOP") != nullptr;
+        if (coop) return launch_coop_cluster(k, dim3(a.grid), dim3(kThr), C::SMEM, s, a.cluster, a);
         return launch_pdl_cluster(k, dim3(a.grid), dim3(kThr), C::SMEM, s, a.cluster, a);
     }
 }
@@ -878,7 +893,7 @@ bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp,
     const int mt = (B + 15) / 16;
     const int ring = (mt == 1 ? SC<32, 1>::NB * SC<32, 1>::STAGE : SC<32, 2>::NB * SC<32, 2>::STAGE);
     (void)max_chunks;
-    return osplits * mt * 16 * kXS + kNA * 16 * mt * 16 * 4 <= ring;
+    return osplits * 2 * mt * 16 * kXS + kNA * 16 * mt * 16 * 4 <= ring;
 }
 
 int step_item_k() { return kKS; }
@@ -888,9 +903,23 @@ int step_pair_clusters_ok(int B, int grid) {
     return (B + 15) / 16 == 1 ? pair_ok<1>(grid) : pair_ok<2>(grid);
 }
 
-size_t step_xo_bytes(int B, int oKp) { return static_cast<size_t>(oKp / kKS) * ((B + 15) / 16) * 16 * kXS; }
+size_t step_xo_bytes(int B, int oKp) { return static_cast<size_t>(oKp / kKS) * 2 * ((B + 15) / 16) * 16 * kXS; }
 
 int step_max_units() { return kMaxU; }
+
+int step_resident_ctas_per_sm(int B) {
+    int n = 0;
+    auto probe = [&](auto k, int smem) {
+        if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k, kThr, smem) != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+    };
+    if ((B + 15) / 16 == 1) probe(layer_step_kernel<32, 1>, SC<32, 1>::SMEM);
+    else probe(layer_step_kernel<32, 2>, SC<32, 2>::SMEM);
+    return n;
+}
 
 cudaError_t launch_layer_step(const StepArgs& a, cudaStream_t s) {
     switch ((a.B + 15) / 16) {

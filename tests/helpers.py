@@ -38,3 +38,18 @@ def pad_latents(lat: np.ndarray, rmax: int) -> np.ndarray:
     out = np.zeros((lat.shape[0], rmax))
     out[:, : lat.shape[1]] = lat
     return out
+
+
+def oracle_step_y(lb: O.Layer, ck, cv, length: int, q, w_o, rpad: int, tile: int = 32):
+    """The oracle's O-projection output of one sequence's layer step:
+    fused_decode_step (decode.cpp:155-206) over ck/cv [nh,L,rmax] with q
+    [nh,H], keeping the latent output v~ (decode.cpp:198), times the folded
+    W'_o = blockdiag(B_V) . W_o rounded to the device's bf16 storage
+    (oracle.fold_oproj) -- heads_row . W_o of pipeline.cpp:323-329 with the
+    weight rounding moved onto the stored product.  Returns y [e_out]."""
+    ck = np.ascontiguousarray(ck, dtype=np.float64)[None]
+    cv = np.ascontiguousarray(cv, dtype=np.float64)[None]
+    _, lat = O.batched_decode_latent(lb, ck, cv, length, np.asarray(q)[None], tile, 1)
+    lat_p = np.zeros((lb.nh, rpad))
+    lat_p[:, :lb.rmax] = lat[0]
+    return lat_p.reshape(-1) @ O.fold_oproj(lb, w_o, rpad, O.bf16_round)

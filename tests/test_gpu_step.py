@@ -9,7 +9,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from tests.helpers import REL_TOL, rel_err_rows, to_factors
+from tests.helpers import REL_TOL, oracle_step_y, rel_err_rows, to_factors
 
 pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
@@ -55,10 +55,9 @@ def test_fused_step_matches_oracle(E, nh, B, L):
         dev_v = np.stack([layer.read_latents(b, h)[1] for h in range(nh)])
         # the step's own row was written by the fused kernel (bf16 of the fp32 latent)
         assert np.abs(dev_k[:, L - 1] - ck[:, L - 1]).max() <= 2 ** -7 * np.abs(ck[:, L - 1]).max()
-        ref = O.fused_decode_step(lb, dev_k, dev_v, L, q, 32)
-        y_ref = ref.reshape(-1) @ wo
-        # bf16 latent outputs feed the O-projection (as in the multi-kernel path)
-        assert rel_err_rows(y[b:b + 1], y_ref[None]) <= 1e-2, f"b={b}"
+        y_ref = oracle_step_y(lb, dev_k, dev_v, L, q, wo, layer.rpad)
+        # hi + lo bf16 latent outputs feed the O-projection: north_star tolerance
+        assert rel_err_rows(y[b:b + 1], y_ref[None]) <= REL_TOL, f"b={b}"
 
 
 def test_fused_step_is_deterministic_and_matches_attention_path():
@@ -156,9 +155,8 @@ def test_fused_step_short_caches_and_ragged_ranks(B, L):
         dev_v = np.stack([layer.read_latents(b, h)[1][:, :lay.rmax] for h in range(nh)])
         for h in range(nh):  # zero-padded latent columns stay zero
             assert not layer.read_latents(b, h)[0][:, lay.ranks[h, 1]:R].any()
-        ref = O.fused_decode_step(lb, dev_k, dev_v, L, q, 32)
-        y_ref = ref.reshape(-1) @ wo
-        assert rel_err_rows(y[b:b + 1], y_ref[None]) <= 1e-2, f"b={b}"
+        y_ref = oracle_step_y(lb, dev_k, dev_v, L, q, wo, R)
+        assert rel_err_rows(y[b:b + 1], y_ref[None]) <= REL_TOL, f"b={b}"
 
 
 def test_cluster_pair_merge_matches_l2_merge():
@@ -205,8 +203,8 @@ np.save(sys.argv[1], np.stack(ys))
 def test_fused_step_matches_multi_kernel_step(E, nh, B, L):
     """Assorted shapes (different split-KV chunk counts, cluster and non-cluster
     merges, parked-item counts, ragged batches): the fused step's y equals the
-    multi-kernel step's (attn_out forces the operator path) within the bf16
-    O-projection tolerance, and the caches agree row for row."""
+    multi-kernel step's (attn_out forces the operator path) up to fp32
+    reassociation, and the caches agree row for row."""
     H, r = 128, 32
     rng, lay, wo, mk = _twin(E, nh, H, r, B, L + 4, 9000 + E + nh + B)
     a, b = mk(), mk()
@@ -221,7 +219,7 @@ def test_fused_step_matches_multi_kernel_step(E, nh, B, L):
     torch.cuda.synchronize()
     assert a.length() == b.length() == L
     ya, yb = ya.cpu().numpy(), yb.cpu().numpy()
-    assert np.abs(ya - yb).max() <= 1e-2 * np.abs(yb).max()
+    assert np.abs(ya - yb).max() <= 1e-4 * np.abs(yb).max()  # both paths: hi + lo latents, fp32 sums
     for bb in (0, B - 1):
         for h in (0, nh - 1):
             ka, va = a.read_latents(bb, h)
