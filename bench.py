@@ -16,7 +16,13 @@ and one NCCL all-reduce sums the O-projection partials.
   torchrun --nproc-per-node N bench.py --gpus N ...
 
 Scaling is weak: global batch = 16 * N sequences, heads sharded N ways, so
-every GPU streams the same 268 MB of latent cache per step.
+every GPU streams the same 268 MB of latent cache per step.  The line also
+carries ``strong_scaling``: north_star config 4 (13B, r48, W4A8, INT8 cache)
+at a FIXED global batch of 64 with its 40 heads sharded over the N GPUs.
+
+Steps rotate over ``--layers`` (default 8) independent layers, each with its
+own factors, W_o and latent cache, so a step's weights were last read 8 steps
+(2.4 GB of traffic) earlier and cannot be served from L2.
 """
 from __future__ import annotations
 
@@ -192,27 +198,38 @@ def run_ours(args, cfg_name, cfg):
     E, H = cfg["E"], cfg["H"]
     L = cfg["L"]
     W, K = args.warmup, args.steps
-    cap = L + W + 2 * K + 120  # timed steps, then the e2e steps (+ their warm-ups)
+    cap = L + W + 2 * K + 120  # timed steps, then the e2e steps (+ their warm-ups), per layer at most
 
     t0 = time.time()
-    f, w_o = synthetic_layer(cfg, seed=args.seed)
-    fs = shard_factors(f, world, rank)
-    wo_s = shard_oproj(w_o, cfg["nh"], H, world, rank)
-    layer = DecodeLayer(fs, wo_s, batch=B, capacity=cap, cache_dtype=cfg["cache"],
-                        weight_dtype=cfg["weights"], oproj_dtype="bf16", device=local,
-                        head_offset=rank * nh_g)
+    # args.layers rotating layers (own factors, W_o and cache each), step i on
+    # layer i mod n: the weights of a step were last touched n steps earlier,
+    # so neither they nor the cache can be served from the 126 MB L2
+    NL = max(1, args.layers)
+    layers = []
     dev = torch.device("cuda", local)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1000 + args.seed)
-    # prefill L-1-W tokens per sequence on the device (untimed setup)
-    pre = L - 1 - W
-    chunk = 256
-    for t0_ in range(0, pre, chunk):
-        n = min(chunk, pre - t0_)
-        xs = torch.randn((n, B, E), generator=gen, device=dev, dtype=torch.float32)
-        layer.prefill(xs)
+    pre = L - 2 - W  # every layer holds ~L - 1 tokens when the timed steps run
+    for li in range(NL):
+        f, w_o = synthetic_layer(cfg, seed=args.seed + 7919 * li)
+        fs = shard_factors(f, world, rank)
+        wo_s = shard_oproj(w_o, cfg["nh"], H, world, rank)
+        lay = DecodeLayer(fs, wo_s, batch=B, capacity=cap, cache_dtype=cfg["cache"],
+                          weight_dtype=cfg["weights"], oproj_dtype="bf16", device=local,
+                          head_offset=rank * nh_g)
+        if li == 0:
+            # prefill through the projection on the device (untimed setup)
+            chunk = 256
+            for t0_ in range(0, pre, chunk):
+                n = min(chunk, pre - t0_)
+                xs = torch.randn((n, B, E), generator=gen, device=dev, dtype=torch.float32)
+                lay.prefill(xs)
+        else:
+            lay.fill_synthetic(pre, seed=li)  # synthetic N(0,1) latents, same length
+        layers.append(lay)
+    layer = layers[0]
     torch.cuda.synchronize()
-    log(f"[rank {rank}] setup {time.time() - t0:.1f}s, cache length {layer.length()}")
+    log(f"[rank {rank}] setup {time.time() - t0:.1f}s, {NL} layers, cache length {layer.length()}")
 
     comm = NcclComm(world, rank, local) if world > 1 else None
     xs = torch.randn((W + K + 2, B, E), generator=gen, device=dev, dtype=torch.float32)
@@ -222,10 +239,15 @@ def run_ours(args, cfg_name, cfg):
 
     def step(i):
         # the step's tokens are resident in HBM (xs[i]); one launch per step
-        layer.step(xs[i], y)
+        layers[i % NL].step(xs[i], y)
         if comm is not None:
             comm.allreduce_(y)
 
+    # setup, untimed: each layer's first step sizes its workspaces and folds
+    # its M_QK (host work with synchronising allocations)
+    for li in range(NL):
+        layers[li].step(xs[0], y)
+    torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
     for i in range(W):
@@ -252,7 +274,7 @@ def run_ours(args, cfg_name, cfg):
     torch.cuda.synchronize()
     ms_total = ev0.elapsed_time(ev1)
     clocks = sampler.stop()
-    L_mid = layer.length() - K // 2
+    L_mid = pre + 1 + (W + K // 2) // NL + 1  # mean context of the timed steps (rows attended)
     ms_t = torch.tensor([ms_total], device=dev)
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
@@ -272,7 +294,7 @@ def run_ours(args, cfg_name, cfg):
     a1.record(stream)
     torch.cuda.synchronize()
     attn_ms = a0.elapsed_time(a1) / R
-    attn_bytes, step_bytes = algorithmic_bytes(cfg, B, nh_g, layer.length())
+    attn_bytes, step_bytes = algorithmic_bytes(cfg, B, nh_g, L_mid)
     peak, peak_kind = measured_peak()
     achieved = attn_bytes / (attn_ms / 1e3) / 1e9
     fused = layer.launches_per_step() == 1
@@ -293,24 +315,25 @@ def run_ours(args, cfg_name, cfg):
     yd = torch.empty((B, E), device=dev, dtype=torch.float32)
     Ke = max(3, min(K, 100))  # host-step wall time is noisy: time as many steps as the device run
     e2e_ms = None
-    if layer.length() + Ke + 4 < cap:
-        def e2e_step():
+    if max(lay.length() for lay in layers) + Ke // NL + NL + 4 < cap:
+        def e2e_step(i):
+            lay = layers[i % NL]
             if comm is None:
-                layer.step_host(xh.numpy(), yh.numpy())
+                lay.step_host(xh.numpy(), yh.numpy())
             else:
                 xd.copy_(xh, non_blocking=True)
-                layer.step(xd, yd)
+                lay.step(xd, yd)
                 comm.allreduce_(yd)
                 yh.copy_(yd, non_blocking=True)
                 stream.synchronize()
-        for _ in range(3):  # first calls size workspaces / resolve the mapped pointers
-            e2e_step()
+        for i in range(NL):  # first calls size workspaces / resolve the mapped pointers
+            e2e_step(i)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t_e = time.perf_counter()
-        for _ in range(Ke):
-            e2e_step()
+        for i in range(Ke):
+            e2e_step(i)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t_e) * 1e3 / Ke
         et = torch.tensor([e2e_ms], device=dev)
@@ -354,7 +377,10 @@ def run_ours(args, cfg_name, cfg):
                        "weight_dtype": cfg["weights"], "parallelism": f"heads/{world}",
                        "step": "append(x.A_qkv) + fused decode attention + O-proj"
                                + (" + NCCL all-reduce" if world > 1 else ""),
-                       "l2": f"inputs larger than L2: {attn_bytes / 1e6:.0f} MB latent cache per GPU per step",
+                       "l2": f"inputs larger than L2: {NL} rotating layers, each step reads its layer's "
+                             f"{attn_bytes / 1e6:.0f} MB latent cache and {(step_bytes - attn_bytes) / 1e6:.0f} MB "
+                             f"of weights last touched {NL} steps earlier ({NL * step_bytes / 1e9:.2f} GB cycle)",
+                       "layers": NL,
                        "launch": layer.step_kind()},
             "roofline": ({"bound": "hbm", "kernel": "layer_step_kernel (whole step: projection, append, "
                                                     "attention, merge, O-projection)",
@@ -386,11 +412,76 @@ def run_ours(args, cfg_name, cfg):
                             "bus loads/stores)" if fused else "wsvd_layer_step_host (C ABI; copy engine)")
                            if world == 1 else "DecodeLayer.step + NCCL"},
         }
-    del layer
+    if not args.no_strong:
+        strong = strong_scaling_point(args, world, rank, local, comm)
+        if res is not None:
+            res["strong_scaling"] = strong
+    del layer, layers
+    return res
+
+
+STRONG_CONFIG = "13b-r48-b64-ctx8k-w4a8-i8cache"
+
+
+def strong_scaling_point(args, world, rank, local, comm, steps=20, warmup=5):
+    """north_star config 4 with a FIXED global batch: the 40 heads of the 13B
+    layer (r48, W4A8, INT8 cache, B = 64, ctx 8K) sharded over the N GPUs of
+    this run, one NCCL all-reduce of the O-projection partials per step; per
+    GPU 2.1 GB / N of cache (1057 / 529 / 265 MB at
+    N = 2 / 4 / 8).  Timed like the headline (CUDA events, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2604_02570_b200.layer import DecodeLayer
+    from paper_2604_02570_b200.sharding import shard_factors, shard_oproj
+    cfg = CONFIGS[STRONG_CONFIG]
+    E, H, B, L = cfg["E"], cfg["H"], cfg["B"], cfg["L"]
+    nh_g = cfg["nh"] // world
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    f, w_o = synthetic_layer(cfg, seed=args.seed + 1)
+    lay = DecodeLayer(shard_factors(f, world, rank), shard_oproj(w_o, cfg["nh"], H, world, rank), batch=B,
+                      capacity=L + steps + warmup + 8, cache_dtype=cfg["cache"], weight_dtype=cfg["weights"],
+                      oproj_dtype="bf16", device=local, head_offset=rank * nh_g)
+    lay.fill_synthetic(L - 1 - warmup, seed=3)
+    g = torch.Generator(device=dev)
+    g.manual_seed(77 + args.seed)
+    xs = torch.randn((warmup + steps, B, E), generator=g, device=dev)
+    y = torch.empty((B, E), device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        lay.step(xs[i], y)
+        if comm is not None:
+            comm.allreduce_(y)
+
+    for i in range(warmup):
+        step(i)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-        dist.destroy_process_group()
-    return res
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(steps):
+        step(warmup + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = torch.tensor([e0.elapsed_time(e1) / steps], device=dev)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    _, step_bytes = algorithmic_bytes(cfg, B, nh_g, L)
+    peak, peak_kind = measured_peak()
+    out = {"workload": STRONG_CONFIG, "scaling": "strong", "global_batch": B, "heads_per_gpu": nh_g,
+           "n_gpus": world, "ctx": L, "us_per_layer": round(ms * 1e3, 2),
+           "tokens_per_s": round(B / (ms / 1e3), 1),
+           "hbm_frac_per_gpu": round(step_bytes / (ms / 1e3) / 1e9 / peak, 4), "peak_kind": peak_kind,
+           "algorithmic_bytes_per_gpu": int(step_bytes), "launches_per_step": lay.launches_per_step(),
+           "step": "append + attention + O-proj" + (" + NCCL all-reduce" if world > 1 else ""),
+           "setup_s": round(time.time() - t0, 1)}
+    del lay
+    torch.cuda.empty_cache()
+    return out
 
 
 def shared_latent_baseline(cfg, B, nh_g, L, dev, steps=5):
@@ -650,6 +741,10 @@ def main():
     ap.add_argument("--soak-ms", type=float, default=1500.0,
                     help="untimed attention load before the timed region while clocks are sampled")
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-strong", action="store_true",
+                    help="skip the config-4 strong-scaling point (fixed B = 64, heads over the N GPUs)")
+    ap.add_argument("--layers", type=int, default=8,
+                    help="rotating layers (own weights and cache each): step i runs layer i mod n")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-seqs", type=int, default=2)
     ap.add_argument("--no-baselines", action="store_true", help="skip the Flash Decoding (SDPA) comparison")
@@ -674,6 +769,10 @@ def main():
         return
 
     res = run_ours(args, args.config, cfg)
+    if dist_env()[0] > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
     if res is None:
         return
     if args.gpus == 1 and not args.no_cpu_baseline:

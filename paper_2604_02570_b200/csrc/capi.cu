@@ -241,6 +241,7 @@ struct wsvd_cache_s {
     DevBuf x_dev, y_dev;              // staging for the host-buffer step
     DevBuf trace;                     // fused-step phase timeline (WSVD_STEP_TRACE)
     DevBuf xo;                        // fused step: bf16 X rows of the O-projection
+    DevBuf fws;                       // fused step: per-CTA segment states
     int attn_mode = 0;                // WSVD_ATTN_ABSORBED or WSVD_ATTN_EXPLICIT_TC
     DevBuf qfull;                     // [B][nh][H] query of the last append (explicit mode)
     int chunk = 512, max_chunks = 1, grid = 148;
@@ -530,8 +531,8 @@ bool fused_step_ok(wsvd_cache_s* c) {
     const int mt = (c->B + 15) / 16;
     if (mt >= 1 && mt <= 2 && occ[mt] < 0) occ[mt] = step_resident_ctas_per_sm(c->B);
     if (mt >= 1 && mt <= 2 && occ[mt] < 1) return false;
-    return step_supported(L->R, c->B, L->d.n_heads, c->B * L->d.n_heads * mc, mc, L->Kp, L->oKp,
-                          round_up(L->e_out, 16) / 16, c->sms);
+    (void)mc;
+    return step_supported(L->R, c->B, L->d.n_heads, L->Kp, L->oKp, round_up(L->e_out, 16) / 16, c->sms);
 }
 
 // The fused step's grid barriers need all of its CTAs (one per SM) resident
@@ -589,17 +590,19 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bo
     a.P = c->P.as<float>();
     a.mqk = L->mqk.as<float>();
     a.cache = c->data.as<uint8_t>();
-    a.ws = c->attn_ws.as<float>();
     a.counters = c->attn_cnt.as<int>();
-    a.vlat = c->vlat.as<float>();
     a.Wo = L->Wo.as<uint8_t>();
     a.d_len = c->d_len();
+    // ctrl: [0] len [1] done [2] step epoch [4] grid barrier [16..32) x-fetch counters
     a.bar = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 4);
     a.epoch = c->ctrl.as<int>() + 2;
     a.xcnt = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 16);
     const size_t xob = step_xo_bytes(c->B, L->oKp);
     if (c->xo.n < xob) CUDA_TRY(c->xo.alloc(xob));  // zeroed: rows past the batch stay 0
     a.xo = c->xo.as<uint8_t>();
+    const size_t wsb = step_ws_bytes(c->sms);
+    if (c->fws.n < wsb) CUDA_TRY(c->fws.alloc(wsb));
+    a.ws = c->fws.as<float>();
     a.B = c->B;
     a.nh = L->d.n_heads;
     a.E = L->d.embed_dim;
@@ -609,19 +612,24 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bo
     a.oKp = L->oKp;
     a.otiles = round_up(L->e_out, 16) / 16;
     a.cap = c->cap_alloc;
-    a.chunk = c->chunk;
-    a.max_chunks = c->chunk > 0 ? c->max_chunks : c->fmax_chunks;
     a.grid = c->sms;
-    // CTA pairs when the split-KV uses two chunks per (sequence, head)
-    static const bool no_cluster = getenv("WSVD_STEP_NOCLUSTER") != nullptr;  // A/B switch
+    // CTA pairs: the region a pair shares meets through DSMEM (WSVD_STEP_NOCLUSTER=1: through L2)
+    static const bool no_cluster = getenv("WSVD_STEP_NOCLUSTER") != nullptr;
     if (c->pair_ok < 0) c->pair_ok = step_pair_clusters_ok(c->B, c->sms);
-    a.cluster = (!no_cluster && a.chunk == 0 && a.max_chunks == 2 && c->pair_ok == 1) ? 2 : 1;
-    // parked stages refill after grid barrier 1: TMA loads in flight make the
-    // barrier's release slow (10.7 -> 9.0 us; WSVD_STEP_GATE_B1=0 is the A/B switch)
-    static const bool gate_off = getenv("WSVD_STEP_GATE_B1") && std::string(getenv("WSVD_STEP_GATE_B1")) == "0";
-    a.gate_b1 = gate_off ? 0 : 1;
+    a.cluster = (!no_cluster && c->pair_ok == 1) ? 2 : 1;
+    // L2 prefetch of the first cache stages before the grid-dependency wait, at
+    // the host mirror's length (unknown inside a caller's graph capture)
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap_st) != cudaSuccess) cudaGetLastError();
+    a.pos_hint = cap_st == cudaStreamCaptureStatusNone ? c->len : -1;
+    static const int pre = getenv("WSVD_STEP_PRE") ? atoi(getenv("WSVD_STEP_PRE")) : 0;  // A/B: stages (measured: 0 best)
+    a.pre_stages = std::max(0, pre);
+    static const bool p3_tma = getenv("WSVD_STEP_P3TMA") && std::string(getenv("WSVD_STEP_P3TMA")) == "1";
+    a.p3_tma = p3_tma ? 1 : 0;
+    static const bool x_first = !(getenv("WSVD_STEP_XFIRST") && std::string(getenv("WSVD_STEP_XFIRST")) == "0");
+    a.x_first = x_first ? 1 : 0;
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
-    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 12 * 8));
+    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 24 * 8));
     a.trace = trace ? c->trace.as<uint64_t>() : nullptr;
     rc = fused_serialize(L->d.device, s);
     if (rc) return rc;

@@ -252,6 +252,12 @@ WSVD_DEV void tma_bulk_g2s_stream(void* smem_dst, const void* gmem_src, uint32_t
         : "memory");
 }
 
+// L2 prefetch of a global range (no shared-memory destination): a later TMA
+// load of the range then hits L2
+WSVD_DEV void prefetch_l2_bulk(const void* gmem_src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
+}
+
 WSVD_DEV uint64_t policy_evict_first() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));

@@ -124,7 +124,7 @@ size_t attn_tc_btile_offset(int d, int r);
 cudaError_t launch_decode_attn_tc(const AttnArgs& a, cudaStream_t s);  // + launch_attn_combine(a, 8)
 
 // ------------------------------------------------- fused layer step (step.cu) --
-// projection -> append -> attention -> combine -> folded O-projection as one
+// projection -> append -> attention -> merge -> folded O-projection as one
 // persistent kernel (bf16 weights / cache, rank 32, batch <= 32).
 struct StepArgs {
     const float* x;        // [B][E] fp32 tokens (device, or mapped host memory when x_host)
@@ -137,25 +137,29 @@ struct StepArgs {
     float* P;              // [splits][B][Nrows] projection partials
     const float* mqk;      // [nh][R][R]
     uint8_t* cache;        // [B][nh][cap][4R] bf16, swizzled
-    float* ws;             // [B*nh][max_chunks][R+2] per-unit states
-    int* counters;         // [B*nh] self-resetting
-    float* vlat;           // [B][nh*R]
+    float* ws;             // [grid][kMaxU][36] segment states (step_ws_bytes)
+    int* counters;         // [B*nh] segments arrived per (sequence, head), self-resetting
     const uint8_t* Wo;     // folded O-projection W-tiles (bf16, K split 512)
     int* d_len;            // committed length (the new row goes to *d_len)
-    unsigned* bar;         // [2] grid barrier (count, generation)
-    uint8_t* xo;           // [osplits][MT*16][1088] bf16 X rows of the O-projection
-    uint64_t* trace;       // [grid][8] %globaltimer at the phase marks, or null
+    unsigned* bar;         // grid barrier count (monotone: two barriers per step)
+    uint8_t* xo;           // [osplits][2][MT*16][1088] bf16 hi / lo X rows of the O-projection
+    uint64_t* trace;       // [grid][16] %globaltimer at the phase marks, or null
     int B, nh, E, Kp, Nrows, e_out, oKp, otiles, cap;
-    int chunk, max_chunks, grid;
-    int gate_b1;           // parked stages refill only after grid barrier 1
-    int cluster;           // 2: CTA pairs; a 2-chunk (sequence, head)'s chunks meet through DSMEM
+    int grid;
+    int cluster;           // 2: CTA pairs (the region a pair shares meets through DSMEM), else 1
+    int pos_hint;          // the host's expected length (-1: unknown, e.g. graph replays)
+    int pre_stages;        // cache stages per CTA prefetched into L2 before the grid-dependency wait
+    int p3_tma;            // O-projection input rows staged by TMA (1) or by plain loads (0)
+    int x_first;           // parked projection weights go out after the token slice is requested
 };
-bool step_supported(int R, int B, int nh, int max_units, int max_chunks, int Kp, int oKp, int otiles, int grid);
+bool step_supported(int R, int B, int nh, int Kp, int oKp, int otiles, int grid);
 int step_item_k();
 size_t step_xo_bytes(int B, int oKp);  // bytes of StepArgs::xo
-int step_max_units();  // attention units one CTA of the fused step can hold
+size_t step_ws_bytes(int grid);        // bytes of StepArgs::ws
+int step_max_units();  // (sequence, head) segments one CTA of the fused step can hold
+int step_ring_stages(int B);  // attention-ring stages of the fused step
 int step_resident_ctas_per_sm(int B);  // occupancy of the fused step kernel (>= 1 to run)
-cudaError_t launch_layer_step(const StepArgs& a, cudaStream_t s);
 int step_pair_clusters_ok(int B, int grid);  // 1 when the grid can run as resident CTA pairs
+cudaError_t launch_layer_step(const StepArgs& a, cudaStream_t s);
 
 }  // namespace wsvd_k

@@ -174,7 +174,7 @@ class DecodeLayer:
         if what == "xq":
             return raw.view(np.int8)
         if what == "trace":
-            return raw.view(np.uint64).reshape(-1, 12)
+            return raw.view(np.uint64).reshape(-1, 24)
         if what == "acc":
             return raw.view(np.int32 if self.layer.weight_dtype in ("i8", "i4") else np.float32)
         return raw.view(np.float32)

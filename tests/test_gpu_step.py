@@ -27,10 +27,10 @@ def _twin(E, nh, H, r, B, cap, seed, **kw):
 
 
 @pytest.mark.parametrize("E,nh,B,L", [(512, 16, 1, 300), (512, 16, 5, 77), (1024, 16, 16, 600), (512, 16, 32, 130),
-                                      # 512 (sequence, head) pairs -> two chunks each: the CTA-pair
-                                      # (cluster) merge through distributed shared memory
+                                      # 512 (sequence, head) regions over 148 byte-balanced ranges:
+                                      # segments split across CTAs, last-arriver merges
                                       (1024, 32, 16, 300), (1024, 32, 16, 33), (1024, 32, 16, 65),
-                                      (1024, 32, 16, 2)])
+                                      (1024, 32, 16, 2), (512, 16, 1, 3000)])
 def test_fused_step_matches_oracle(E, nh, B, L):
     H, r = 128, 32
     rng, lay, wo, mk = _twin(E, nh, H, r, B, L + 8, 8000 + B)
@@ -160,9 +160,10 @@ def test_fused_step_short_caches_and_ragged_ranks(B, L):
 
 
 def test_cluster_pair_merge_matches_l2_merge():
-    """The CTA-pair merge (chunk 0's state crosses to the home chunk through
-    DSMEM) is bit-identical to the L2 publish / poll path (WSVD_STEP_NOCLUSTER,
-    run in a child process: the switch is read once)."""
+    """The region a CTA pair shares meets through distributed shared memory;
+    with WSVD_STEP_NOCLUSTER (child process: the switch is read once) every
+    shared region merges through L2 instead.  Both merge the parts in range
+    order with the same arithmetic: bit-identical y."""
     import os
     import subprocess
     import sys
@@ -196,6 +197,39 @@ np.save(sys.argv[1], np.stack(ys))
         assert res.returncode == 0, res.stderr[-3000:]
         outs.append(np.load(path))
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.timeout(120)
+def test_fused_steps_on_two_streams_do_not_overlap():
+    """Two caches stepping on two non-blocking streams with no host sync in
+    between: the fused step holds every SM at its barrier, so the library
+    orders fused steps of different streams (capi.cu fused_serialize) --
+    without that, two concurrent grids would each wait for SMs the other
+    holds.  Results equal the same steps run one stream at a time."""
+    E, nh, H, r, B, L = 1024, 32, 128, 32, 16, 300
+    rng, lay, wo, mk = _twin(E, nh, H, r, B, L + 16, 8500)
+    a, b, a2, b2 = mk(), mk(), mk(), mk()
+    dev = torch.device("cuda", 0)
+    toks = torch.from_numpy(O.bf16_round(rng.normal_matrix((L + 6) * B, E)).reshape(L + 6, B, E)
+                            .astype(np.float32)).to(dev)
+    for lay_ in (a, b, a2, b2):
+        lay_.prefill(toks[:L])
+    torch.cuda.synchronize()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    ya = [torch.empty((B, E), device=dev) for _ in range(6)]
+    yb = [torch.empty((B, E), device=dev) for _ in range(6)]
+    s1.wait_stream(torch.cuda.current_stream())
+    s2.wait_stream(torch.cuda.current_stream())
+    for t in range(6):
+        a.step(toks[L + t], ya[t], stream=s1)
+        b.step(toks[L + t], yb[t], stream=s2)
+    torch.cuda.synchronize()
+    for t in range(6):
+        ra, rb_ = torch.empty((B, E), device=dev), torch.empty((B, E), device=dev)
+        a2.step(toks[L + t], ra)
+        b2.step(toks[L + t], rb_)
+        torch.cuda.synchronize()
+        assert torch.equal(ya[t], ra) and torch.equal(yb[t], rb_), f"step {t}"
 
 
 @pytest.mark.parametrize("E,nh,B,L", [(512, 8, 32, 700), (1024, 32, 8, 129), (512, 32, 16, 1030),

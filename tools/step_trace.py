@@ -17,8 +17,9 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2604_02570_b200.layer import DecodeLayer  # noqa: E402
 
-MARKS = ["entry", "griddep", "P1 done", "barrier1", "qt ready", "attn done", "merged", "barrier2",
-         "P3 staged", "end"]
+MARKS = ["entry", "griddep", "P1 done", "q count", "qt ready", "attn done", "merged", "barrier",
+         "P3 staged", "end", "P3 mma", "attn start", "kv done", "1st merge",
+         "prep0 done", "w0 start", "w7 start", "stage0 in"]
 
 
 def main():
@@ -26,6 +27,8 @@ def main():
     ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--per-sm", action="store_true")
+    ap.add_argument("--save", default=None)
+    ap.add_argument("--dump", action="store_true", help="every CTA's marks")
     ap.add_argument("--attn-only", action="store_true")
     ap.add_argument("--proj-only", action="store_true")
     ap.add_argument("--host", action="store_true", help="steps through wsvd_layer_step_host (pinned x / y)")
@@ -50,7 +53,8 @@ def main():
             layer.step(x, y, graph=False)
     torch.cuda.synchronize()
     raw = layer.debug_copy("trace").astype(np.int64)
-    t, smid, nu = raw[:, :10], raw[:, 10], raw[:, 11]
+    t = np.concatenate([raw[:, :10], raw[:, 12:20]], axis=1)
+    smid, nu = raw[:, 10], raw[:, 11]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
     if args.attn_only:  # attention CTAs only (nu > 0): the projection CTAs skip marks 3-5
@@ -61,13 +65,22 @@ def main():
     for k, name in enumerate(MARKS):
         col = rel[:, k]
         print(f"{name:10s} {col.min():8.2f} {np.median(col):8.2f} {col.max():8.2f}")
+    if args.dump:
+        print("cta smid " + " ".join(f"{n[:9]:>9s}" for n in MARKS))
+        for i in range(rel.shape[0]):
+            print(f"{i:3d} {smid[i]:4d} " + " ".join(f"{v:9.2f}" for v in rel[i]))
     if args.per_sm:
-        # per-SM attention-phase duration (qt ready -> attn done) and units, by SM id
-        dur = rel[:, 5] - rel[:, 4]
+        # per-SM attention-phase duration (first segment's query -> attention
+        # done) and segment count, by SM id; --save appends them for
+        # cross-run comparisons (is a slow SM slow every step?)
+        dur = rel[:, 5] - rel[:, 11]
         order = np.argsort(smid)
-        print("smid units attn_us")
+        print("smid segs attn_us")
         for i in order:
             print(f"{smid[i]:4d} {nu[i]:5d} {dur[i]:7.2f}")
+        if args.save:
+            with open(args.save, "a") as fh:
+                fh.write(" ".join(f"{smid[i]}:{dur[i]:.3f}" for i in order) + "\n")
 
 
 if __name__ == "__main__":
