@@ -128,6 +128,11 @@ int wsvd_layer_set_oproj(wsvd_layer_t layer, const double* w_o_rows, int32_t e_o
 int wsvd_cache_create(wsvd_layer_t layer, int32_t batch, int32_t capacity, int32_t cache_dtype,
                       wsvd_cache_t* out);
 int wsvd_cache_destroy(wsvd_cache_t cache);
+/* Raises the capacity to at least `capacity` rows, keeping the committed rows
+ * (reallocates and copies; synchronises the device).  The reference's cache
+ * grows row by row (Matrix::append_row); the C++ drop-in grows by doubling. */
+int wsvd_cache_grow(wsvd_cache_t cache, int32_t capacity);
+int wsvd_cache_capacity(wsvd_cache_t cache, int32_t* capacity);
 /* empties the cache (length 0) */
 int wsvd_cache_reset(wsvd_cache_t cache);
 /* decode with another factor set of identical geometry (the reference passes
@@ -258,6 +263,34 @@ int wsvd_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_
                      wsvd_comm_t* out);
 int wsvd_comm_destroy(wsvd_comm_t comm);
 int wsvd_allreduce_sum_f32(wsvd_comm_t comm, float* buf, int64_t count, void* stream);
+
+/* ------------------------------------------- comparison baselines (dense.cu) --
+ * The reference's uncompressed and shared-latent baselines on the device
+ * (decode.hpp:114-170; decode.cpp:208-432), fp32: dense per-head K/V caches
+ * (FullKvCache) with the attention of eager_decode_step / flash_decode_step
+ * (one softmax over the cached rows; the two schedules differ only in their
+ * traffic tallies), and the GEMV / GEMM blocks of append_token_dense,
+ * append_token_shared and shared_decode_step(materialize).  Device pointers;
+ * row-major matrices. */
+typedef struct wsvd_dense_cache_s* wsvd_dense_cache_t;
+int wsvd_dense_cache_create(int32_t n_heads, int32_t head_dim, int32_t device, wsvd_dense_cache_t* out);
+int wsvd_dense_cache_destroy(wsvd_dense_cache_t cache);
+int wsvd_dense_cache_length(wsvd_dense_cache_t cache, int32_t* len);
+/* FullKvCache::push of every head + bump_length: k, v [n_heads][head_dim] */
+int wsvd_dense_cache_append(wsvd_dense_cache_t cache, const float* k, const float* v, void* stream);
+/* keys(head) / values(head) to the host as fp64 [len][head_dim] */
+int wsvd_dense_cache_read_host(wsvd_dense_cache_t cache, int32_t head, double* k, double* v);
+/* softmax(q . k_j / sqrt(H)) . V per head: q, out [n_heads][head_dim];
+ * tile_len as TileConfig (0 -> WSVD_ECONFIG) */
+int wsvd_dense_decode_step(wsvd_dense_cache_t cache, const float* q, int32_t tile_len, float* out, void* stream);
+/* the same over caller buffers keys / values [n_heads][ld][head_dim] (len rows
+ * valid), scores scratch [n_heads][ld] */
+int wsvd_dense_attend(const float* keys, const float* values, int32_t n_heads, int32_t len, int32_t ld,
+                      int32_t head_dim, const float* q, float* scores, float* out, void* stream);
+/* y[n] = sum_k x[k] w[k][n] (vec_mat, decode.cpp:97-110) */
+int wsvd_vecmat_f32(const float* x, const float* w, int32_t k, int32_t n, float* y, void* stream);
+/* c[m][n] = a[m][k] . b[k][n] (matmul, matrix.cpp) */
+int wsvd_matmul_f32(const float* a, const float* b, int32_t m, int32_t k, int32_t n, float* c, void* stream);
 
 #ifdef __cplusplus
 }

@@ -1002,6 +1002,57 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     return WSVD_OK;
 }
 
+int wsvd_cache_grow(wsvd_cache_t c, int32_t capacity) {
+    if (!c) return set_err(WSVD_ECONFIG, "null cache");
+    if (capacity <= c->cap) return WSVD_OK;
+    CUDA_TRY(cudaSetDevice(c->L->d.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    const int cap_alloc = round_up(capacity, 128);
+    const size_t regions = static_cast<size_t>(c->B) * c->L->d.n_heads;
+    const size_t old_pitch = static_cast<size_t>(c->cap_alloc) * c->row_bytes;
+    const size_t new_pitch = static_cast<size_t>(cap_alloc) * c->row_bytes;
+    DevBuf nd, ns;
+    CUDA_TRY(nd.alloc(regions * new_pitch + (128u << 10)));
+    if (c->len > 0) {
+        // whole 1 KB swizzle blocks of the used rows: the 16-byte XOR swizzle
+        // permutes units inside 128-byte lines, relative to the region start
+        const size_t used = std::min((static_cast<size_t>(c->len) * c->row_bytes + 1023) / 1024 * 1024, old_pitch);
+        CUDA_TRY(cudaMemcpy2D(nd.p, new_pitch, c->data.p, old_pitch, used, regions, cudaMemcpyDeviceToDevice));
+    }
+    if (c->cdtype == WSVD_I8) {
+        CUDA_TRY(ns.alloc(regions * cap_alloc * 4 + (16u << 10)));
+        if (c->len > 0)
+            CUDA_TRY(cudaMemcpy2D(ns.p, static_cast<size_t>(cap_alloc) * 4, c->scales.p, static_cast<size_t>(c->cap_alloc) * 4,
+                                  static_cast<size_t>(c->len) * 4, regions, cudaMemcpyDeviceToDevice));
+    }
+    std::swap(c->data.p, nd.p);
+    std::swap(c->data.n, nd.n);
+    if (c->cdtype == WSVD_I8) {
+        std::swap(c->scales.p, ns.p);
+        std::swap(c->scales.n, ns.n);
+    }
+    c->cap = capacity;
+    c->cap_alloc = cap_alloc;
+    // captured step graphs hold the old buffers
+    if (c->gexec) {
+        cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+    }
+    if (c->graph) {
+        cudaGraphDestroy(c->graph);
+        c->graph = nullptr;
+    }
+    c->gpending = false;
+    c->gkey = GraphKey{};
+    return WSVD_OK;
+}
+
+int wsvd_cache_capacity(wsvd_cache_t c, int32_t* capacity) {
+    if (!c || !capacity) return set_err(WSVD_ECONFIG, "null argument");
+    *capacity = c->cap;
+    return WSVD_OK;
+}
+
 int wsvd_cache_destroy(wsvd_cache_t c) {
     delete c;
     return WSVD_OK;

@@ -10,6 +10,7 @@
 
 #include "../../oracle/wsvd_oracle.h"
 #include "wsvd/decode.hpp"
+#include "wsvd/errors.hpp"
 
 using namespace wsvd;
 using namespace wsvd::decode;
