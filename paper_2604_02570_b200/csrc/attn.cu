@@ -69,30 +69,38 @@ struct Cfg {
     // hiding: 4 warps per SM sub-partition); CUDA-core consumers: one token per thread
     static constexpr int NW = ((MMA || IMMA) && (V & 2)) ? 16 : 8;
     static constexpr int THREADS = 32 * NW + 64;  // + one producer warp + one merge (helper) warp
-    // tokens per stage: int8 rows are half as wide, so the tensor-core int8
-    // consumer takes 512-token stages (the same 32 KB per stage as bf16)
-    // int8 tensor-core consumers take 1024-token stages (64 KB at r = 32: fewer
-    // per-stage reductions and conversions per token) when three of them fit,
-    // else 512 (the same 32 KB per stage as bf16); V bit 5 forces 512
-    static constexpr bool BIG = IMMA && !(V & 32) && 3 * (4 * kStageTok * 2 * R + 16 * kStageTok + 256) <= 218 * 1024;
-    static constexpr int ST = IMMA ? (BIG ? 4 : 2) * kStageTok : kStageTok;
+    static constexpr int QTB = 512;               // the unit's absorbed query (R <= 128 floats)
+    static constexpr int RSTRIDE = R + 4;         // floats per lane row of the reduction scratch
+    static constexpr int RED = (MMA || IMMA) ? 0 : NW * 32 * RSTRIDE * 4;
+    static constexpr int BUDGET = 222 * 1024;
+    // Tokens per stage.  The tensor-core consumers want >= 3 stages in flight,
+    // the CUDA-core one >= 2.  int8 tensor-core consumers take 1024-token
+    // stages (64 KB at r = 32: fewer per-stage reductions and conversions per
+    // token) when three fit, else 512 (the same 32 KB per stage as bf16), else
+    // 256 (large ranks); V bit 5 rules out 1024.  bf16 and the CUDA-core
+    // consumer take 256-token stages, 128 for large ranks (rows up to 512 B).
+    static constexpr int stage_bytes(int st) { return st * ROWB + ((CD == I8) ? 4 * st : 0) + QTB; }
+    static constexpr int NEED = (MMA || IMMA) ? 3 : 2;
+    static constexpr bool fits(int st) { return NEED * stage_bytes(st) + RED + 4096 <= BUDGET; }
+    static constexpr bool BIG = IMMA && !(V & 32) && fits(4 * kStageTok);
+    static constexpr int ST = IMMA ? (BIG ? 4 * kStageTok : (fits(2 * kStageTok) ? 2 * kStageTok : kStageTok))
+                                   : (fits(kStageTok) ? kStageTok : kStageTok / 2);
     static constexpr int GPW = ST / (16 * NW);  // 16-token groups per warp per stage
     static constexpr int ROWS = ST * ROWB;
     static constexpr int SC = (CD == I8) ? 4 * ST : 0;
     static constexpr int QT_OFF = ROWS + SC;   // absorbed query of the unit (first stage)
-    static constexpr int STAGE = QT_OFF + 256;
-    static constexpr int RSTRIDE = R + 4;      // floats per lane row of the reduction scratch
-    static constexpr int RED = (MMA || IMMA) ? 0 : NW * 32 * RSTRIDE * 4;
-    static constexpr int BUDGET = 222 * 1024;
+    static constexpr int STAGE = QT_OFF + QTB;
     static constexpr int ST_RAW = (BUDGET - RED - 4096) / STAGE;
     static constexpr int STAGES = ST_RAW > 8 ? 8 : ST_RAW;
     static constexpr int BAR_OFF = STAGES * STAGE;
     static constexpr int RED_OFF = BAR_OFF + 256;
     static constexpr int MISC_OFF = RED_OFF + RED;
-    static constexpr bool OK = ST_RAW >= 2;         // f32 rows of R > 32 do not fit two stages
+    // >= 2 stages; every tensor-core warp owns whole 16-token groups (pairs for
+    // the int8 P.V k-steps)
+    static constexpr bool OK = ST_RAW >= 2 && (!(MMA || IMMA) || (GPW >= 1 && (!IMMA || GPW % 2 == 0)));
     static constexpr int SMEM = OK ? MISC_OFF : 0;
     static_assert(PART % 16 == 0, "latent half must be a multiple of 16 bytes");
-    static_assert(R * 4 <= 256, "query row must fit the stage's query area");
+    static_assert(R * 4 <= QTB, "query row must fit the stage's query area");
 };
 
 WSVD_DEV float ex2(float x) {
@@ -1198,7 +1206,9 @@ int attn_variant() {
 
 template <int CD, int R>
 cudaError_t launch_t(const AttnArgs& a, cudaStream_t s) {
-    if constexpr (CD == I8) {
+    if constexpr (R > 64) {
+        return launch_v<CD, R, 0>(a, s);  // large ranks: the default consumers only
+    } else if constexpr (CD == I8) {
         // WSVD_ATTN_VARIANT bit 3: the CUDA-core int8 consumer; bit 1: 16 consumer warps (A/B)
         if (attn_variant() & 8) return launch_v<CD, R, 8>(a, s);
         if (attn_variant() & 4) return launch_v<CD, R, 4>(a, s);  // streaming probe (no compute)
@@ -1235,6 +1245,10 @@ int smem_for(int R) {
         case 32: return Cfg<CD, 32>::SMEM;
         case 48: return Cfg<CD, 48>::SMEM;
         case 64: return Cfg<CD, 64>::SMEM;
+        case 80: return Cfg<CD, 80>::SMEM;
+        case 96: return Cfg<CD, 96>::SMEM;
+        case 112: return Cfg<CD, 112>::SMEM;
+        case 128: return Cfg<CD, 128>::SMEM;
     }
     return 0;
 }
@@ -1246,6 +1260,10 @@ cudaError_t launch_cd(const AttnArgs& a, cudaStream_t s) {
         case 32: return launch_t<CD, 32>(a, s);
         case 48: return launch_t<CD, 48>(a, s);
         case 64: return launch_t<CD, 64>(a, s);
+        case 80: return launch_t<CD, 80>(a, s);
+        case 96: return launch_t<CD, 96>(a, s);
+        case 112: return launch_t<CD, 112>(a, s);
+        case 128: return launch_t<CD, 128>(a, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -1315,6 +1333,10 @@ bool cluster_ok_cd(int R, int Cn) {
         case 32: return cluster_ok_t<CD, 32>(Cn);
         case 48: return cluster_ok_t<CD, 48>(Cn);
         case 64: return cluster_ok_t<CD, 64>(Cn);
+        case 80: return cluster_ok_t<CD, 80>(Cn);
+        case 96: return cluster_ok_t<CD, 96>(Cn);
+        case 112: return cluster_ok_t<CD, 112>(Cn);
+        case 128: return cluster_ok_t<CD, 128>(Cn);
     }
     return false;
 }

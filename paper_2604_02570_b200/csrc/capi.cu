@@ -685,11 +685,12 @@ int wsvd_layer_create(const wsvd_layer_desc* desc, const int32_t* ranks, wsvd_la
             return set_err(WSVD_ESHAPE, "rank " + std::to_string(ranks[i]) + " outside [1, head_dim]");
         rmax = std::max(rmax, static_cast<int>(ranks[i]));
     }
-    int R = round_up(rmax, 16);
-    if (R == 16 || R == 32 || R == 48 || R == 64) {
-    } else {
-        return set_err(WSVD_ECONFIG, "padded rank " + std::to_string(R) + " unsupported (max 64)");
-    }
+    // every head is zero-padded to one common width, a multiple of 16 (the
+    // MMA k-step); the reference accepts any rank <= H (factorize.cpp:72-164),
+    // the kernels any padded width up to 128 (= the LLaVA head dim)
+    const int R = round_up(rmax, 16);
+    if (R > 128)
+        return set_err(WSVD_ECONFIG, "padded rank " + std::to_string(R) + " unsupported (max 128)");
     CUDA_TRY(cudaSetDevice(d.device));
     auto* L = new wsvd_layer_s();
     L->d = d;
