@@ -236,6 +236,12 @@ int wsvd_layer_step_graph(wsvd_cache_t cache, const float* x, float* y, void* st
  * summed over K splits, int32 (I8/I4) or fp32, [rows][n_heads*3*rpad];
  * 3 absorbed queries fp32 [batch][n_heads][rpad].  *bytes is in/out. */
 int wsvd_cache_debug_copy(wsvd_cache_t cache, int32_t what, void* host, int64_t* bytes);
+/* Test hook, INT8 caches: flags bit 0 makes the following attention launches
+ * record every cached row's int32 score accumulators -- the rows times the
+ * hi and lo int8 parts of the split absorbed query --
+ * read back with wsvd_cache_debug_copy(what = 5) as int32
+ * [batch][n_heads][capacity][2].  Off by default (no cost). */
+int wsvd_cache_set_debug(wsvd_cache_t cache, int32_t flags);
 
 /* ----------------------------------------------------- host utilities ---
  * The reference weight quantiser (quant::quantize_weight, quant.cpp:99-119):

@@ -109,6 +109,7 @@ def lib():
         L.orc_quant_cache_row.restype = C.c_uint16
         L.orc_quant_cache_row.argtypes = [_fp, _sz, _i8p]
         L.orc_unpack_int4.argtypes = [C.POINTER(C.c_uint8), _sz, _i8p]
+        L.orc_i8_scores.argtypes = [_fp, _sz, _i8p, _sz, _sz, _ip]
         _lib = L
     return _lib
 
@@ -404,3 +405,14 @@ def quant_cache_row(c32):
 
 def f16_to_f32(h):
     return np.float32(lib().orc_f16_to_f32(int(h)))
+
+
+def i8_scores(qt32, rows_i8, R):
+    """int32 score accumulators (hi, lo) of every int8 cache row against the
+    split absorbed query (orc_i8_scores; attn.cu's int8 consumers).
+    qt32 [R] fp32, rows_i8 [L][ld] int8 -> [L][2] int32."""
+    q = np.ascontiguousarray(qt32, dtype=np.float32)
+    rows = np.ascontiguousarray(rows_i8, dtype=np.int8)
+    acc = np.zeros((rows.shape[0], 2), dtype=np.int32)
+    lib().orc_i8_scores(_ptr(q, _fp), R, _ptr(rows, _i8p), rows.shape[0], rows.shape[1], _ptr(acc, _ip))
+    return acc

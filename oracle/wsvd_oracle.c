@@ -608,3 +608,44 @@ void orc_unpack_int4(const uint8_t* packed, size_t n, int8_t* out) {
         out[i] = (int8_t)(v >= 8 ? v - 16 : v);
     }
 }
+
+/* ======================= int8-cache attention: the integer score stage === */
+/* The absorbed query of an INT8 cache is split into two int8 vectors
+ * (paper_2604_02570_b200/csrc/attn.cu consume_mma_i8 / consume_imma_i8; SURVEY
+ * Appendix A.5 "if the absorbed form is used for INT8 configs, the oracle must
+ * implement the same absorbed form"): s1 = max|q| / 127 (1 when q == 0),
+ * s2 = s1 / 254, h = rint(q / s1), l = clamp(rint(fma(-h, s1, q) / s2), +-127)
+ * with rint = round half to even, all in fp32.  Each cached int8 row c_j then
+ * gives the exact int32 accumulators hi_j = sum_t c_j[t] h[t] and
+ * lo_j = sum_t c_j[t] l[t]; the score is (hi_j s1 + lo_j s2) * s_cK[j] in the
+ * log2 domain.  rows: L x ld int8 (the first R columns are C_K). */
+void orc_i8_query_split(const float* q, size_t R, int8_t* h, int8_t* l, float* s1_out, float* s2_out) {
+    float mx = 0.0f;
+    for (size_t k = 0; k < R; ++k) mx = fmaxf(mx, fabsf(q[k]));
+    const float s1 = (mx == 0.0f) ? 1.0f : mx / 127.0f;
+    const float s2 = s1 / 254.0f;
+    for (size_t k = 0; k < R; ++k) {
+        const float hv = rintf(q[k] / s1);
+        float lv = rintf(fmaf(-hv, s1, q[k]) / s2);
+        lv = fminf(fmaxf(lv, -127.0f), 127.0f);
+        h[k] = (int8_t)hv;
+        l[k] = (int8_t)lv;
+    }
+    *s1_out = s1;
+    *s2_out = s2;
+}
+
+void orc_i8_scores(const float* q, size_t R, const int8_t* rows, size_t L, size_t ld, int32_t* acc) {
+    int8_t h[256], l[256];
+    float s1, s2;
+    orc_i8_query_split(q, R, h, l, &s1, &s2);
+    for (size_t j = 0; j < L; ++j) {
+        int32_t a = 0, b = 0;
+        for (size_t t = 0; t < R; ++t) {
+            a += (int32_t)rows[j * ld + t] * (int32_t)h[t];
+            b += (int32_t)rows[j * ld + t] * (int32_t)l[t];
+        }
+        acc[2 * j] = a;
+        acc[2 * j + 1] = b;
+    }
+}

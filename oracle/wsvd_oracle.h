@@ -162,6 +162,13 @@ uint16_t orc_quant_cache_row(const float* c, size_t n, int8_t* q);
 /* Sign-extend the nibbles of a packed int4 row (lo nibble = even index). */
 void orc_unpack_int4(const uint8_t* packed, size_t n, int8_t* out);
 
+/* INT8-cache attention, the integer score stage of the absorbed form
+ * (attn.cu consume_mma_i8 / consume_imma_i8): the fp32
+ * absorbed query split into int8 hi / lo parts, and every cached row's int32
+ * accumulators against them, acc [L][2] = (hi, lo).  R <= 256. */
+void orc_i8_query_split(const float* q, size_t R, int8_t* h, int8_t* l, float* s1, float* s2);
+void orc_i8_scores(const float* q, size_t R, const int8_t* rows, size_t L, size_t ld, int32_t* acc);
+
 #ifdef __cplusplus
 }
 #endif

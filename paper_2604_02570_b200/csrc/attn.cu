@@ -409,7 +409,7 @@ WSVD_DEV void consume_mma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, ui
                         if (kk * 32 + 16 * j >= R) break;  // the padded half of a last k-step
                         const float v = q[kk * 32 + 16 * j + 4 * t4 + e];
                         const float h = rintf(v / s1);
-                        const float lo = rintf((v - h * s1) / s2);
+                        const float lo = rintf(fmaf(-h, s1, v) / s2);  // oracle: orc_i8_query_split
                         w1 |= (static_cast<uint32_t>(static_cast<int32_t>(h)) & 0xffu) << (8 * e);
                         w2 |= (static_cast<uint32_t>(static_cast<int32_t>(fminf(fmaxf(lo, -127.f), 127.f))) & 0xffu) << (8 * e);
                     }
@@ -438,6 +438,11 @@ WSVD_DEV void consume_mma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, ui
                 mma_s8_16832(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
             }
             const int t0 = tb + g8, t1 = tb + g8 + 8;
+            if (a.dbg_scores && t4 == 0) {  // test hook: the int32 score accumulators (hi, lo query parts)
+                int* dbg = a.dbg_scores + (static_cast<size_t>(g.bh) * a.cap + g.t0 + s * C::ST) * 2;
+                if (t0 < rows) { dbg[2 * t0] = d[0]; dbg[2 * t0 + 1] = d[1]; }
+                if (t1 < rows) { dbg[2 * t1] = d[2]; dbg[2 * t1 + 1] = d[3]; }
+            }
             const float k0 = __low2float(sc2[t0]), k1 = __low2float(sc2[t1]);
             sc[grp][0] = (t4 == 0 && t0 < rows)
                 ? fmaf(static_cast<float>(d[0]), s1, static_cast<float>(d[1]) * s2) * k0 : -INFINITY;
@@ -580,6 +585,11 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
                 mma_s8_16832(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
             }
             const int t0 = tb + g8, t1 = tb + g8 + 8;
+            if (a.dbg_scores && t4 == 0) {  // test hook: the int32 score accumulators (hi, lo query parts)
+                int* dbg = a.dbg_scores + (static_cast<size_t>(g.bh) * a.cap + g.t0 + s * C::ST) * 2;
+                if (t0 < rows) { dbg[2 * t0] = d[0]; dbg[2 * t0 + 1] = d[1]; }
+                if (t1 < rows) { dbg[2 * t1] = d[2]; dbg[2 * t1 + 1] = d[3]; }
+            }
             const float k0 = __low2float(sc2[t0]), k1 = __low2float(sc2[t1]);
             sc[grp][0] = (t4 == 0 && t0 < rows)
                 ? fmaf(static_cast<float>(d[0]), s1, static_cast<float>(d[1]) * s2) * k0 : -INFINITY;
@@ -605,7 +615,7 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
                     if (kk * 32 + 16 * j >= R) break;
                     const float v = q[kk * 32 + 16 * j + 4 * t4 + e];
                     const float h = rintf(v / s1);
-                    const float lo = rintf((v - h * s1) / s2);
+                    const float lo = rintf(fmaf(-h, s1, v) / s2);  // oracle: orc_i8_query_split
                     w1 |= (static_cast<uint32_t>(static_cast<int32_t>(h)) & 0xffu) << (8 * e);
                     w2 |= (static_cast<uint32_t>(static_cast<int32_t>(fminf(fmaxf(lo, -127.f), 127.f))) & 0xffu) << (8 * e);
                 }

@@ -242,6 +242,8 @@ struct wsvd_cache_s {
     DevBuf trace;                     // fused-step phase timeline (WSVD_STEP_TRACE)
     DevBuf xo;                        // fused step: bf16 X rows of the O-projection
     DevBuf fws;                       // fused step: per-CTA segment states
+    DevBuf dbg;                       // test hook: int8 score accumulators [B*nh][cap_alloc][2]
+    bool dbg_on = false;
     int attn_mode = 0;                // WSVD_ATTN_ABSORBED or WSVD_ATTN_EXPLICIT_TC
     DevBuf qfull;                     // [B][nh][H] query of the last append (explicit mode)
     int chunk = 512, max_chunks = 1, grid = 148;
@@ -449,6 +451,7 @@ int run_attention(wsvd_cache_s* c, float* out, float* vlat, int len_add, cudaStr
     a.cdtype = c->cdtype;
     a.row_bytes = c->row_bytes;
     a.grid = c->grid;
+    a.dbg_scores = c->dbg_on ? c->dbg.as<int>() : nullptr;
     static const bool no_fin = getenv("WSVD_ATTN_COMBINE") != nullptr;
     a.no_finalize = no_fin ? 1 : 0;
     // Few (sequence, head) pairs (e.g. one sequence): clusters of C CTAs, one
@@ -1507,6 +1510,15 @@ int wsvd_cache_debug_copy(wsvd_cache_t c, int32_t what, void* host, int64_t* byt
         *bytes = static_cast<int64_t>(n);
         return WSVD_OK;
     }
+    if (what == 5) {
+        if (!c->dbg_on) return set_err(WSVD_ECONFIG, "score capture is off (wsvd_cache_set_debug)");
+        const size_t per = static_cast<size_t>(c->cap_alloc) * 2 * 4;
+        const size_t n = static_cast<size_t>(c->B) * L->d.n_heads * per;
+        if (*bytes < static_cast<int64_t>(n)) return set_err(WSVD_ESHAPE, "host buffer too small");
+        CUDA_TRY(cudaMemcpy(host, c->dbg.p, n, cudaMemcpyDeviceToHost));
+        *bytes = static_cast<int64_t>(n);
+        return WSVD_OK;
+    }
     if (what == 4) {
         if (!c->trace.p) return set_err(WSVD_ECONFIG, "no step trace (set WSVD_STEP_TRACE)");
         if (*bytes < static_cast<int64_t>(c->trace.n)) return set_err(WSVD_ESHAPE, "host buffer too small");
@@ -1515,6 +1527,16 @@ int wsvd_cache_debug_copy(wsvd_cache_t c, int32_t what, void* host, int64_t* byt
         return WSVD_OK;
     }
     return set_err(WSVD_ECONFIG, "unknown debug buffer");
+}
+
+int wsvd_cache_set_debug(wsvd_cache_t c, int32_t flags) {
+    if (!c) return set_err(WSVD_ECONFIG, "null cache");
+    c->dbg_on = (flags & 1) != 0 && c->cdtype == WSVD_I8;
+    if (c->dbg_on) {
+        const size_t need = static_cast<size_t>(c->B) * c->L->d.n_heads * c->cap_alloc * 2 * 4;
+        if (c->dbg.n < need) CUDA_TRY(c->dbg.alloc(need));
+    }
+    return WSVD_OK;
 }
 
 int wsvd_quantize_weight(const double* w, int64_t rows, int64_t cols, int32_t bits, int8_t* q,

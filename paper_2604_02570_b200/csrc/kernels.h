@@ -107,6 +107,7 @@ struct AttnArgs {
     // explicit key reconstruction (attn_tc.cu): per-head B_K^T tiles and the query
     const uint8_t* bkt;     // [nh][attn_tc_btile_bytes()] bf16, MMA B-operand layout
     const float* q;         // [B][nh][H] query rows
+    int* dbg_scores;        // test hook (int8 cache): [B*nh][cap][2] int32 score accumulators, or null
 };
 int attn_smem_bytes(int cdtype, int R);
 int attn_occupancy(int cdtype, int R);  // resident CTAs per SM (0 if unsupported)

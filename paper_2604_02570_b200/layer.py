@@ -166,7 +166,7 @@ class DecodeLayer:
 
     def debug_copy(self, what: str) -> np.ndarray:
         """Internal buffers of the last append (see wsvd_cache_debug_copy)."""
-        code = {"xq": 0, "sx": 1, "acc": 2, "qt": 3, "trace": 4}[what]
+        code = {"xq": 0, "sx": 1, "acc": 2, "qt": 3, "trace": 4, "scores": 5}[what]
         nbytes = C.c_int64(1 << 30)
         buf = np.empty(1 << 28, dtype=np.uint8)
         N.call("wsvd_cache_debug_copy", self.h, code, C.c_void_p(buf.ctypes.data), C.byref(nbytes))
@@ -175,9 +175,16 @@ class DecodeLayer:
             return raw.view(np.int8)
         if what == "trace":
             return raw.view(np.uint64).reshape(-1, 24)
+        if what == "scores":
+            return raw.view(np.int32)
         if what == "acc":
             return raw.view(np.int32 if self.layer.weight_dtype in ("i8", "i4") else np.float32)
         return raw.view(np.float32)
+
+    def set_debug(self, flags: int):
+        """Test hook (int8 caches): bit 0 records the int32 score accumulators
+        of the following attention launches (debug_copy("scores"))."""
+        N.call("wsvd_cache_set_debug", self.h, int(flags))
 
     def read_raw(self, seq: int, head: int):
         L = self.length()

@@ -255,3 +255,34 @@ def test_layer_step_in_kernel_merge(cache, B, nh, L, r):
     torch.cuda.synchronize()
     y_ref = out.cpu().numpy().reshape(B, -1).astype(np.float64) @ w_o
     assert np.abs(y.cpu().numpy() - y_ref).max() <= 1e-2 * np.abs(y_ref).max()
+
+
+@pytest.mark.parametrize("r,L", [(32, 1500), (48, 300), (96, 260)])
+def test_int8_attention_score_accumulators_bit_exact(r, L):
+    """the int8 attention scores every cached row against
+    the absorbed query split into int8 hi / lo parts (attn.cu consume_imma_i8 at
+    r = 32, consume_mma_i8 above); the oracle restates the split
+    (orc_i8_query_split) and the int32 accumulators must agree exactly for
+    every row of every (sequence, head)."""
+    from paper_2604_02570_b200.layer import DecodeLayer
+    rng = O.Rng(7700 + r)
+    E, nh, H, B = 512, 4, 128, 2
+    lay = O.random_layer(rng, E, H, [[r, r, r]] * nh)
+    quant, _ = quant_layer(lay, 8)
+    layer = DecodeLayer(to_factors(lay), None, batch=B, capacity=L + 8, cache_dtype="i8", weight_dtype="i8",
+                        quantized=quant)
+    R = layer.rpad
+    dev = torch.device("cuda", 0)
+    layer.prefill(torch.from_numpy(rng.normal_matrix(L * B, E).reshape(L, B, E).astype(np.float32)).to(dev))
+    q = torch.from_numpy(rng.normal_matrix(B * nh, H).reshape(B, nh, H).astype(np.float32)).to(dev)
+    out = torch.empty((B, nh, H), device=dev)
+    layer.set_debug(1)
+    layer.attend(q, out)
+    torch.cuda.synchronize()
+    qt = layer.debug_copy("qt").reshape(B, nh, R)
+    acc = layer.debug_copy("scores").reshape(B, nh, -1, 2)
+    for b in range(B):
+        for h in range(nh):
+            rows, _ = layer.read_raw(b, h)
+            ref = O.i8_scores(qt[b, h], rows.view(np.int8), R)
+            assert np.array_equal(acc[b, h, :L], ref), f"int32 score accumulators differ (b={b} h={h})"
