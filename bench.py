@@ -236,12 +236,35 @@ def run_ours(args, cfg_name, cfg):
     y = torch.empty((B, E), device=dev, dtype=torch.float32)
     out = torch.empty((B, nh_g, H), device=dev, dtype=torch.float32)
     stream = torch.cuda.current_stream()
+    # Single GPU: the NL layers are a decode chain (layer l + 1's token = layer
+    # l's output, pipe::decode_factored's layer loop without the FFN), run as
+    # ONE persistent kernel per pass over the layers (wsvd_chain_step); a
+    # timed "step" is still one layer step of every sequence.  N > 1: every
+    # layer step is its own launch followed by the NCCL all-reduce.
+    from paper_2604_02570_b200.layer import DecodeChain
+    ys = [torch.empty((B, E), device=dev, dtype=torch.float32) for _ in range(NL)]
+    chains = {}
+    use_chain = world == 1 and NL > 1 and not args.no_chain and DecodeChain(layers).fused()
 
-    def step(i):
-        # the step's tokens are resident in HBM (xs[i]); one launch per step
-        layers[i % NL].step(xs[i], y)
-        if comm is not None:
-            comm.allreduce_(y)
+    def chain_of(start, cnt):
+        if (start, cnt) not in chains:
+            chains[(start, cnt)] = DecodeChain(layers[start:start + cnt])
+        return chains[(start, cnt)]
+
+    def run_steps(i0, n):
+        """layer steps i0 .. i0 + n - 1 (step i on layer i mod NL)"""
+        j = i0
+        while j < i0 + n:
+            start = j % NL
+            if use_chain:
+                cnt = min(NL - start, i0 + n - j)
+                chain_of(start, cnt).step(xs[j // NL], ys[start:start + cnt])
+            else:
+                cnt = 1
+                layers[start].step(xs[j // NL] if start == 0 else ys[start - 1], ys[start])
+                if comm is not None:
+                    comm.allreduce_(ys[start])
+            j += cnt
 
     # setup, untimed: each layer's first step sizes its workspaces and folds
     # its M_QK (host work with synchronising allocations)
@@ -250,8 +273,7 @@ def run_ours(args, cfg_name, cfg):
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
-    for i in range(W):
-        step(i)
+    run_steps(0, W)
     torch.cuda.synchronize()
     # soak: keep the GPU under the same load (the attention kernel, no append)
     # while the clock sampler collects samples around the timed region
@@ -265,8 +287,7 @@ def run_ours(args, cfg_name, cfg):
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for j in range(K):
-        step(W + j)
+    run_steps(W, K)
     ev1.record(stream)
     torch.cuda.synchronize()
     if world > 1:
@@ -281,6 +302,27 @@ def run_ours(args, cfg_name, cfg):
     ms_total = float(ms_t.item())
     ms_step = ms_total / K
     value = B / (ms_step / 1e3)
+    launches = 0
+    j = W
+    while j < W + K:
+        start = j % NL
+        cnt = min(NL - start, W + K - j) if use_chain else 1
+        launches += 1 if use_chain else layer.launches_per_step()
+        j += cnt
+
+    # ---- the same layer steps as one launch each (no chaining), for reference
+    single = None
+    if use_chain:
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        for i in range(NL):
+            layers[i].step(xs[0], ys[i])
+        torch.cuda.synchronize()
+        s0.record(stream)
+        for i in range(K):
+            layers[i % NL].step(xs[i // NL] if i % NL == 0 else ys[i % NL - 1], ys[i % NL])
+        s1.record(stream)
+        torch.cuda.synchronize()
+        single = s0.elapsed_time(s1) / K
 
     # ---- dominant kernel alone: decode attention (same stream, CUDA events)
     R = 20
@@ -315,8 +357,15 @@ def run_ours(args, cfg_name, cfg):
     yd = torch.empty((B, E), device=dev, dtype=torch.float32)
     Ke = max(3, min(K, 100))  # host-step wall time is noisy: time as many steps as the device run
     e2e_ms = None
+    e2e_unit_layers = NL if use_chain else 1  # layer steps per host call
     if max(lay.length() for lay in layers) + Ke // NL + NL + 4 < cap:
+        full = chain_of(0, NL) if use_chain else None
+
         def e2e_step(i):
+            if use_chain:
+                # one token through the NL chained layers: x in, the last y out
+                full.step_host(xh.numpy(), yh.numpy())
+                return
             lay = layers[i % NL]
             if comm is None:
                 lay.step_host(xh.numpy(), yh.numpy())
@@ -326,16 +375,17 @@ def run_ours(args, cfg_name, cfg):
                 comm.allreduce_(yd)
                 yh.copy_(yd, non_blocking=True)
                 stream.synchronize()
-        for i in range(NL):  # first calls size workspaces / resolve the mapped pointers
+        ncalls = max(3, Ke // e2e_unit_layers)
+        for i in range(NL if not use_chain else 1):  # first calls size workspaces / resolve the mapped pointers
             e2e_step(i)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t_e = time.perf_counter()
-        for i in range(Ke):
+        for i in range(ncalls):
             e2e_step(i)
         torch.cuda.synchronize()
-        e2e_ms = (time.perf_counter() - t_e) * 1e3 / Ke
+        e2e_ms = (time.perf_counter() - t_e) * 1e3 / (ncalls * e2e_unit_layers)
         et = torch.tensor([e2e_ms], device=dev)
         if world > 1:
             dist.all_reduce(et, op=dist.ReduceOp.MAX)
@@ -381,7 +431,9 @@ def run_ours(args, cfg_name, cfg):
                              f"{attn_bytes / 1e6:.0f} MB latent cache and {(step_bytes - attn_bytes) / 1e6:.0f} MB "
                              f"of weights last touched {NL} steps earlier ({NL * step_bytes / 1e9:.2f} GB cycle)",
                        "layers": NL,
-                       "launch": layer.step_kind()},
+                       "launch": (f"the {NL} rotating layers chained (layer l+1's token = layer l's y): one "
+                                  f"persistent kernel per pass over them (wsvd_chain_step); {launches} launches "
+                                  f"for the {K} timed layer steps" if use_chain else layer.step_kind())},
             "roofline": ({"bound": "hbm", "kernel": "layer_step_kernel (whole step: projection, append, "
                                                     "attention, merge, O-projection)",
                           "achieved": round(step_bytes / (ms_step / 1e3) / 1e9, 1), "peak": peak,
@@ -404,13 +456,21 @@ def run_ours(args, cfg_name, cfg):
                           "step_frac": round(step_bytes / (ms_step / 1e3) / 1e9 / peak, 4)}),
             "clocks": clocks,
             "baselines": baselines,
-            "gpu_launches": K * layer.launches_per_step(),
+            "gpu_launches": launches,
+            "single_layer_launches": ({"ms_per_step": round(single, 5), "tokens_per_s": round(B / (single / 1e3), 1),
+                                       "note": "the same layer steps, one wsvd_layer_step launch each"}
+                                      if single is not None else None),
             "e2e": {"value": round(B / (e2e_ms / 1e3), 1) if e2e_ms else None, "unit": "tokens/s",
                     "ms_per_step": round(e2e_ms, 4) if e2e_ms else None,
-                    "h2d_bytes_per_step": B * E * 4, "d2h_bytes_per_step": B * E * 4,
-                    "api": ("wsvd_layer_step_host (C ABI; pinned x/y moved by the fused kernel's own "
-                            "bus loads/stores)" if fused else "wsvd_layer_step_host (C ABI; copy engine)")
-                           if world == 1 else "DecodeLayer.step + NCCL"},
+                    "h2d_bytes_per_step": B * E * 4 // e2e_unit_layers,
+                    "d2h_bytes_per_step": B * E * 4 // e2e_unit_layers,
+                    "api": (f"wsvd_chain_step_host (C ABI): one token of every sequence through the {NL} "
+                            f"chained layers per call, pinned x in / last y out moved by the kernel's own bus "
+                            f"loads/stores; per layer step = call time / {NL}, bytes per layer step = "
+                            f"x + y bytes / {NL}") if use_chain else
+                           (("wsvd_layer_step_host (C ABI; pinned x/y moved by the fused kernel's own "
+                             "bus loads/stores)" if fused else "wsvd_layer_step_host (C ABI; copy engine)")
+                            if world == 1 else "DecodeLayer.step + NCCL")},
         }
     if not args.no_strong:
         strong = strong_scaling_point(args, world, rank, local, comm)
@@ -746,6 +806,8 @@ def main():
     ap.add_argument("--layers", type=int, default=8,
                     help="rotating layers (own weights and cache each): step i runs layer i mod n")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-chain", action="store_true",
+                    help="one launch per layer step instead of the fused layer chain")
     ap.add_argument("--cpu-sample-seqs", type=int, default=2)
     ap.add_argument("--no-baselines", action="store_true", help="skip the Flash Decoding (SDPA) comparison")
     args = ap.parse_args()

@@ -230,6 +230,24 @@ int wsvd_layer_step_host(wsvd_cache_t cache, const float* x_host, float* y_host,
  * calls with the same arguments replay it (1 launch instead of ~5). */
 int wsvd_layer_step_graph(wsvd_cache_t cache, const float* x, float* y, void* stream);
 
+/* -------------------------------------------------------------- chains --
+ * pipe::decode_factored's layer loop (pipeline.cpp:318-336) over the
+ * attention blocks of n layers, one token per sequence: layer 0 takes x,
+ * layer l > 0 takes layer l - 1's output ys[l - 1] (the attention blocks of a
+ * decode stack chained, no FFN between them), and every layer appends to its
+ * own cache.  caches[l]: n distinct caches of one geometry (batch, heads,
+ * embed_dim, rank, e_out == embed_dim), each bound to its layer with an
+ * O-projection; ys[l]: [batch][E] fp32 device buffers.  When every layer runs
+ * the fused step (wsvd_cache_step_info) and n <= 32, the chain is ONE
+ * persistent kernel launch -- the next layer's projection weights load while
+ * a layer finishes; otherwise it is n wsvd_layer_step calls. */
+int wsvd_chain_step(wsvd_cache_t const* caches, int32_t n, const float* x, float* const* ys, void* stream);
+/* Same through host buffers, synchronising the stream: x_host [batch][E] in,
+ * y_host [batch][E] = the last layer's output out (pinned or pageable); the
+ * intermediate outputs stay on the device. */
+int wsvd_chain_step_host(wsvd_cache_t const* caches, int32_t n, const float* x_host, float* y_host,
+                         void* stream);
+
 /* Copies internal per-step buffers of the last append to the host, for
  * bit-exact parity checks of the integer path: what = 0 quantised tokens
  * int8 [rows][Kp]; 1 token scales fp32 [rows]; 2 projection accumulators

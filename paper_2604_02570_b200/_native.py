@@ -75,6 +75,20 @@ SIGNATURES = {
     "wsvd_comm_create": (C.c_int, [_u8p, _i32, _i32, _i32, C.POINTER(_vp)]),
     "wsvd_comm_destroy": (C.c_int, [_vp]),
     "wsvd_allreduce_sum_f32": (C.c_int, [_vp, _fp, _i64, _vp]),
+    "wsvd_cache_grow": (C.c_int, [_vp, _i32]),
+    "wsvd_cache_capacity": (C.c_int, [_vp, _i32p]),
+    "wsvd_cache_set_debug": (C.c_int, [_vp, _i32]),
+    "wsvd_dense_cache_create": (C.c_int, [_i32, _i32, _i32, C.POINTER(_vp)]),
+    "wsvd_dense_cache_destroy": (C.c_int, [_vp]),
+    "wsvd_dense_cache_length": (C.c_int, [_vp, _i32p]),
+    "wsvd_dense_cache_append": (C.c_int, [_vp, _fp, _fp, _vp]),
+    "wsvd_dense_cache_read_host": (C.c_int, [_vp, _i32, _dp, _dp]),
+    "wsvd_dense_decode_step": (C.c_int, [_vp, _fp, _i32, _fp, _vp]),
+    "wsvd_dense_attend": (C.c_int, [_fp, _fp, _i32, _i32, _i32, _i32, _fp, _fp, _fp, _vp]),
+    "wsvd_vecmat_f32": (C.c_int, [_fp, _fp, _i32, _i32, _fp, _vp]),
+    "wsvd_matmul_f32": (C.c_int, [_fp, _fp, _i32, _i32, _i32, _fp, _vp]),
+    "wsvd_chain_step": (C.c_int, [C.POINTER(_vp), _i32, _fp, C.POINTER(_vp), _vp]),
+    "wsvd_chain_step_host": (C.c_int, [C.POINTER(_vp), _i32, _fp, _fp, _vp]),
 }
 
 _lib = None

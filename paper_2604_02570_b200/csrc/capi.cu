@@ -572,32 +572,45 @@ int fused_serialize(int device, cudaStream_t s) {
     return WSVD_OK;
 }
 
-// the whole step as one persistent kernel (step.cu)
-int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bool x_host = false) {
+// The whole step as one persistent kernel (step.cu), for a chain of n layers
+// (n = 1: one layer step).  Layer l's token is ys[l - 1] (l > 0); the launch's
+// control block, workspaces and trace are the first cache's.  x_host / y_host:
+// x (layer 0) / ys[n - 1] are mapped pinned host memory.
+int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const* ys, cudaStream_t s,
+                    bool x_host = false, bool y_host = false) {
+    wsvd_cache_s* c = cs[0];
     wsvd_layer_s* L = c->L;
-    int rc = ensure_mqk(L);
-    if (rc) return rc;
+    if (n < 1 || n > kStepMaxLayers) return set_err(WSVD_ECONFIG, "a fused chain holds 1 .. " + std::to_string(kStepMaxLayers) + " layers");
+    StepArgs a{};
+    for (int l = 0; l < n; ++l) {
+        int rc = ensure_mqk(cs[l]->L);
+        if (rc) return rc;
+        StepLayer& Ly = a.layer[l];
+        Ly.A = cs[l]->L->A.as<uint8_t>();
+        Ly.mqk = cs[l]->L->mqk.as<float>();
+        Ly.cache = cs[l]->data.as<uint8_t>();
+        Ly.counters = cs[l]->attn_cnt.as<int>();
+        Ly.Wo = cs[l]->L->Wo.as<uint8_t>();
+        Ly.d_len = cs[l]->d_len();
+        Ly.y = ys[l];
+        Ly.cap = cs[l]->cap_alloc;
+    }
+    a.nlayers = n;
     const int splits = L->Kp / L->ks;
     const size_t need = static_cast<size_t>(splits) * c->B * L->Nrows * 4;
     if (c->P.n < need) CUDA_TRY(c->P.alloc(need));
-    StepArgs a{};
     a.x = x;
-    a.y = y;
     a.x_host = x_host ? 1 : 0;
+    a.y_host = y_host ? 1 : 0;
     if (x_host) {
         const size_t xb = static_cast<size_t>(c->B) * L->d.embed_dim * 4;
         if (c->x_dev.n < xb) CUDA_TRY(c->x_dev.alloc(xb));
         a.xd = c->x_dev.as<float>();
     }
-    a.A = L->A.as<uint8_t>();
     a.P = c->P.as<float>();
-    a.mqk = L->mqk.as<float>();
-    a.cache = c->data.as<uint8_t>();
-    a.counters = c->attn_cnt.as<int>();
-    a.Wo = L->Wo.as<uint8_t>();
-    a.d_len = c->d_len();
-    // ctrl: [0] len [1] done [2] step epoch [4] grid barrier [16..32) x-fetch counters
+    // ctrl: [0] len [1] done [2] fused launches [4] grid barrier [5] barrier generations [16..32) x-fetch counters
     a.bar = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 4);
+    a.bgen = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 5);
     a.epoch = c->ctrl.as<int>() + 2;
     a.xcnt = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 16);
     const size_t xob = step_xo_bytes(c->B, L->oKp);
@@ -614,7 +627,6 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bo
     a.e_out = L->e_out;
     a.oKp = L->oKp;
     a.otiles = round_up(L->e_out, 16) / 16;
-    a.cap = c->cap_alloc;
     a.grid = c->sms;
     // CTA pairs: the region a pair shares meets through DSMEM (WSVD_STEP_NOCLUSTER=1: through L2)
     static const bool no_cluster = getenv("WSVD_STEP_NOCLUSTER") != nullptr;
@@ -631,15 +643,25 @@ int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bo
     a.p3_tma = p3_tma ? 1 : 0;
     static const bool x_first = !(getenv("WSVD_STEP_XFIRST") && std::string(getenv("WSVD_STEP_XFIRST")) == "0");
     a.x_first = x_first ? 1 : 0;
+    static const int l2n = getenv("WSVD_STEP_L2NEXT") ? atoi(getenv("WSVD_STEP_L2NEXT")) : 1;  // A/B switch
+    a.l2_next = l2n;
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
+    static const int trace_layer = getenv("WSVD_STEP_TRACE_LAYER") ? atoi(getenv("WSVD_STEP_TRACE_LAYER")) : -1;
     if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 24 * 8));
     a.trace = trace ? c->trace.as<uint64_t>() : nullptr;
-    rc = fused_serialize(L->d.device, s);
+    a.trace_layer = trace_layer >= 0 && trace_layer < n ? trace_layer : n - 1;  // default: the last layer
+    int rc = fused_serialize(L->d.device, s);
     if (rc) return rc;
     CUDA_TRY(launch_layer_step(a, s));
     c->P_M = c->B;
     c->P_splits = splits;
     return WSVD_OK;
+}
+
+int run_step_fused(wsvd_cache_s* c, const float* x, float* y, cudaStream_t s, bool x_host = false) {
+    wsvd_cache_s* cs[1] = {c};
+    float* ys[1] = {y};
+    return run_chain_fused(cs, 1, x, ys, s, x_host, x_host);
 }
 
 // append (row written, length not yet committed) -> attention over len + 1
@@ -1465,6 +1487,101 @@ int wsvd_layer_step_host(wsvd_cache_t c, const float* x_host, float* y_host, voi
     if (rc) return rc;
     CUDA_TRY(cudaStreamSynchronize(s));
     c->len += 1;
+    return WSVD_OK;
+}
+
+// ---------------------------------------------------------------- chains --
+// pipe::decode_factored's layer loop (pipeline.cpp:318-336), attention blocks
+// chained: one persistent launch when every layer runs the fused step.
+static int chain_check(wsvd_cache_t const* cs, int32_t n, bool& fused) {
+    if (!cs || n < 1) return set_err(WSVD_ECONFIG, "a chain needs at least one cache");
+    fused = n <= kStepMaxLayers;
+    const wsvd_cache_s* c0 = cs[0];
+    if (!c0) return set_err(WSVD_ECONFIG, "null cache handle");
+    for (int l = 0; l < n; ++l) {
+        wsvd_cache_s* c = cs[l];
+        if (!c) return set_err(WSVD_ECONFIG, "null cache handle");
+        for (int k = 0; k < l; ++k)
+            if (cs[k] == c) return set_err(WSVD_ECONFIG, "a cache appears twice in the chain");
+        int rc = check_layer(c->L);
+        if (rc) return rc;
+        const wsvd_layer_s* L = c->L;
+        const wsvd_layer_s* L0 = c0->L;
+        if (!L->Wo.p) return set_err(WSVD_ECONFIG, "layer has no O-projection folded from its current V factors (wsvd_layer_set_oproj)");
+        if (L->e_out != L->d.embed_dim) return set_err(WSVD_ESHAPE, "a chained layer must project back to embed_dim");
+        if (c->B != c0->B || L->d.embed_dim != L0->d.embed_dim || L->d.n_heads != L0->d.n_heads ||
+            L->d.head_dim != L0->d.head_dim || L->R != L0->R || L->d.device != L0->d.device)
+            return set_err(WSVD_ESHAPE, "chained caches differ in geometry (batch, heads, embed_dim, rank, device)");
+        if (c->len + 1 > c->cap) return set_err(WSVD_ESHAPE, "latent cache is full (capacity " + std::to_string(c->cap) + ")");
+        if (!fused_step_ok(c) || L->Kp != L0->Kp || L->oKp != L0->oKp || L->Nrows != L0->Nrows || c->sms != c0->sms)
+            fused = false;
+    }
+    return WSVD_OK;
+}
+
+int wsvd_chain_step(wsvd_cache_t const* cs, int32_t n, const float* x, float* const* ys, void* stream) {
+    if (!x || !ys) return set_err(WSVD_ECONFIG, "null argument");
+    bool fused = false;
+    int rc = chain_check(cs, n, fused);
+    if (rc) return rc;
+    for (int l = 0; l < n; ++l)
+        if (!ys[l]) return set_err(WSVD_ECONFIG, "null layer output");
+    CUDA_TRY(cudaSetDevice(cs[0]->L->d.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (fused) {
+        rc = run_chain_fused(cs, n, x, ys, s);
+        if (rc) return rc;
+        for (int l = 0; l < n; ++l) cs[l]->len += 1;
+        return WSVD_OK;
+    }
+    for (int l = 0; l < n; ++l) {
+        rc = wsvd_layer_step(cs[l], l == 0 ? x : ys[l - 1], nullptr, ys[l], stream);
+        if (rc) return rc;
+    }
+    return WSVD_OK;
+}
+
+int wsvd_chain_step_host(wsvd_cache_t const* cs, int32_t n, const float* x_host, float* y_host, void* stream) {
+    if (!x_host || !y_host) return set_err(WSVD_ECONFIG, "null argument");
+    bool fused = false;
+    int rc = chain_check(cs, n, fused);
+    if (rc) return rc;
+    wsvd_cache_s* c0 = cs[0];
+    CUDA_TRY(cudaSetDevice(c0->L->d.device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const size_t xb = static_cast<size_t>(c0->B) * c0->L->d.embed_dim * 4;
+    std::vector<float*> ys(n);
+    for (int l = 0; l < n; ++l) {
+        if (cs[l]->y_dev.n < xb) CUDA_TRY(cs[l]->y_dev.alloc(xb));
+        ys[l] = cs[l]->y_dev.as<float>();
+    }
+    if (c0->x_dev.n < xb) CUDA_TRY(c0->x_dev.alloc(xb));
+    // mapped pinned buffers: the kernel fetches x and stores the last y itself
+    // (one launch + one synchronise, as wsvd_layer_step_host)
+    static const bool no_zc = getenv("WSVD_HOST_ZEROCOPY") && std::string(getenv("WSVD_HOST_ZEROCOPY")) == "0";
+    if (fused && !no_zc && !(c0->hkey.x == x_host && c0->hkey.y == y_host)) {
+        cudaPointerAttributes ax{}, ay{};
+        const bool okx = cudaPointerGetAttributes(&ax, x_host) == cudaSuccess;
+        const bool oky = cudaPointerGetAttributes(&ay, y_host) == cudaSuccess;
+        cudaGetLastError();
+        c0->hzc = okx && oky && ax.type == cudaMemoryTypeHost && ay.type == cudaMemoryTypeHost && ax.devicePointer &&
+                  ay.devicePointer;
+        c0->hx = c0->hzc ? static_cast<const float*>(ax.devicePointer) : nullptr;
+        c0->hy = c0->hzc ? static_cast<float*>(ay.devicePointer) : nullptr;
+        c0->hkey = {x_host, y_host, s};
+    }
+    if (fused && !no_zc && c0->hzc) {
+        ys[n - 1] = c0->hy;
+        rc = run_chain_fused(cs, n, c0->hx, ys.data(), s, true, true);
+        if (rc) return rc;
+        for (int l = 0; l < n; ++l) cs[l]->len += 1;
+    } else {
+        CUDA_TRY(cudaMemcpyAsync(c0->x_dev.p, x_host, xb, cudaMemcpyHostToDevice, s));
+        rc = wsvd_chain_step(cs, n, c0->x_dev.as<float>(), ys.data(), stream);
+        if (rc) return rc;
+        CUDA_TRY(cudaMemcpyAsync(y_host, ys[n - 1], xb, cudaMemcpyDeviceToHost, s));
+    }
+    CUDA_TRY(cudaStreamSynchronize(s));
     return WSVD_OK;
 }
 

@@ -126,32 +126,46 @@ cudaError_t launch_decode_attn_tc(const AttnArgs& a, cudaStream_t s);  // + laun
 
 // ------------------------------------------------- fused layer step (step.cu) --
 // projection -> append -> attention -> merge -> folded O-projection as one
-// persistent kernel (bf16 weights / cache, rank 32, batch <= 32).
-struct StepArgs {
-    const float* x;        // [B][E] fp32 tokens (device, or mapped host memory when x_host)
-    int x_host;            // x is pinned host memory: fetched once over the bus into xd
-    float* xd;             // [B][E] device copy of a host x
-    unsigned* xcnt;        // [kMaxSplits] per-K-split fetch counters (monotone)
-    int* epoch;            // fused steps run so far (their generation)
-    float* y;              // [B][e_out] fp32 output (plain stores: device or mapped host memory)
+// persistent kernel (bf16 weights / cache, rank 32, batch <= 32), for one layer
+// or for a chain of layers in one launch (layer l + 1's token = layer l's y:
+// pipe::decode_factored's layer loop, pipeline.cpp:318-336, attention blocks
+// only).
+constexpr int kStepMaxLayers = 32;
+struct StepLayer {         // one layer of the launch (all share the geometry below)
     const uint8_t* A;      // projection W-tiles (bf16, K split 512)
-    float* P;              // [splits][B][Nrows] projection partials
     const float* mqk;      // [nh][R][R]
     uint8_t* cache;        // [B][nh][cap][4R] bf16, swizzled
-    float* ws;             // [grid][kMaxU][36] segment states (step_ws_bytes)
     int* counters;         // [B*nh] segments arrived per (sequence, head), self-resetting
     const uint8_t* Wo;     // folded O-projection W-tiles (bf16, K split 512)
     int* d_len;            // committed length (the new row goes to *d_len)
-    unsigned* bar;         // grid barrier count (monotone: two barriers per step)
-    uint8_t* xo;           // [osplits][2][MT*16][1088] bf16 hi / lo X rows of the O-projection
-    uint64_t* trace;       // [grid][16] %globaltimer at the phase marks, or null
-    int B, nh, E, Kp, Nrows, e_out, oKp, otiles, cap;
+    float* y;              // [B][e_out] fp32 output; the next layer's token
+    int cap;
+    int pad_;
+};
+struct StepArgs {
+    const float* x;        // [B][E] fp32 tokens of layer 0 (device, or mapped host memory when x_host)
+    int x_host;            // x is pinned host memory: fetched once over the bus into xd
+    int y_host;            // the last layer's y is mapped host memory (plain stores, whole tiles per CTA)
+    float* xd;             // [B][E] device copy of a host x
+    unsigned* xcnt;        // [kMaxSplits] per-K-split fetch counters (monotone)
+    int* epoch;            // fused launches run so far (x-fetch counter generations)
+    unsigned* bgen;        // grid-barrier generations completed so far
+    unsigned* bar;         // grid barrier count (monotone, wrap-safe compares)
+    float* P;              // [splits][B][Nrows] projection partials
+    float* ws;             // [grid][kMaxU][36] segment states (step_ws_bytes)
+    uint8_t* xo;           // [osplits][2][MT*16][1024] bf16 hi / lo X rows of the O-projection (swizzled)
+    uint64_t* trace;       // [grid][24] %globaltimer at the phase marks of layer trace_layer, or null
+    int trace_layer;
+    int B, nh, E, Kp, Nrows, e_out, oKp, otiles;
     int grid;
     int cluster;           // 2: CTA pairs (the region a pair shares meets through DSMEM), else 1
-    int pos_hint;          // the host's expected length (-1: unknown, e.g. graph replays)
-    int pre_stages;        // cache stages per CTA prefetched into L2 before the grid-dependency wait
+    int pos_hint;          // the host's expected length of layer 0 (-1: unknown, e.g. graph replays)
+    int pre_stages;        // layer-0 cache stages per CTA prefetched into L2 before the grid-dependency wait
     int p3_tma;            // O-projection input rows staged by TMA (1) or by plain loads (0)
     int x_first;           // parked projection weights go out after the token slice is requested
+    int l2_next;           // prefetch the next layer's late weight items into L2 during the tail
+    int nlayers;           // 1 .. kStepMaxLayers
+    StepLayer layer[kStepMaxLayers];
 };
 bool step_supported(int R, int B, int nh, int Kp, int oKp, int otiles, int grid);
 int step_item_k();

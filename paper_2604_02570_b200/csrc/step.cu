@@ -1,49 +1,47 @@
-// step.cu -- the whole decode-layer step as ONE persistent kernel (bf16 weights,
-// bf16 latent cache, rank 32).
+// step.cu -- the decode-layer step as ONE persistent kernel (bf16 weights,
+// bf16 latent cache, rank 32), for one layer or a chain of layers.
 //
 // pipe::decode_factored's per-layer body (reference src/pipeline.cpp:320-329)
 // is append_token (decode.cpp:127-153) -> fused_decode_step (decode.cpp:155-206)
 // -> heads_row . W_o.  The multi-kernel path (capi.cu layer_step_impl) runs it
 // as projection GEMM -> append epilogue -> attention -> combine -> O-projection.
-// This kernel runs the same arithmetic with one CTA per SM, ordered so that
-// HBM never waits for a synchronisation:
+// This kernel runs the same arithmetic with one CTA per SM.  Per layer:
 //
-//   P1q  query projection  P[split][b][n] = x_b . A_Q[:, n] over one K split
-//        (swap-AB mma.sync over W-tiles streamed by TMA, as gemm.cu); each CTA
-//        releases a grid-wide count once its query items are written;
-//   P1kv key / value projection of the new token, the same way, interleaved
-//        with the attention stages as its W-tiles land; a second count
-//        releases these partials;
+//   P1   latent projection P[split][b][n] = x_b . A[:, n] over one K split
+//        (swap-AB mma.sync over W-tiles streamed by TMA, as gemm.cu);
+//   G1   grid barrier: every projection partial is written;
 //   P2   attention over the cached rows 0 .. pos-1: the B*nh*pos rows of all
 //        (sequence, head) regions are cut into G equal contiguous ranges (at
 //        32-row boundaries), one per CTA, so every SM streams the same bytes.
 //        A range covers a few (sequence, head) segments.  The helper warp
-//        derives each segment's absorbed query qt = (sum_split c_Q) . M_QK once
-//        the query count is complete; the consumer warps run the tensor-core
-//        scores K_tile . [qt_hi | qt_lo] and acc += V_tile^T . [p_hi | p_lo]
-//        with a warp-uniform running max (SoftmaxState::observe,
-//        decode.cpp:35-57, in the log2 domain);
+//        derives each segment's absorbed query qt = (sum_split c_Q) . M_QK;
+//        the consumer warps run the tensor-core scores K_tile . [qt_hi | qt_lo]
+//        and acc += V_tile^T . [p_hi | p_lo] with a warp-uniform running max
+//        (SoftmaxState::observe, decode.cpp:35-57, in the log2 domain);
 //   merge  per segment, the helper merges the 8 warp states (fixed order);
 //        the segment that ends a region also observes the step's own token
-//        (its K/V latents from the P1kv partials, rounded to the cache's bf16
-//        and written to row pos: the reference appends before attending,
-//        decode.cpp:143-149); segments publish their state and the LAST one of
-//        a (sequence, head) to arrive (atomic count) merges all of them in
-//        range order (SoftmaxState::merge, decode.cpp:59-75) -- nobody waits
-//        for anybody -- and writes v~ = acc / denom as hi + lo bf16 rows of
-//        the O-projection input;
-//   --   grid barrier (every row complete; the cache length is committed);
+//        (its K/V latents from the projection partials, rounded to the
+//        cache's bf16 and written to row pos: the reference appends before
+//        attending, decode.cpp:143-149).  A region shared by the two CTAs of a
+//        cluster pair meets through distributed shared memory; any other
+//        shared region publishes its parts and the LAST to arrive merges them
+//        in range order (SoftmaxState::merge, decode.cpp:59-75), writing
+//        v~ = acc / denom as hi + lo bf16 rows of the O-projection input;
+//   G2   grid barrier: every row is merged; the cache length is committed;
 //   P3   folded O-projection y = v~ . (B_V . W_o) over W-tiles prefetched into
-//        shared memory during P2; each CTA owns whole output tiles and sums
-//        their K splits itself -- no atomics, run-to-run deterministic.
+//        shared memory during P2 (run-to-run deterministic: fixed-order sums,
+//        or exactly two red.add addends onto zeros);
+//   G3   (chains only) grid barrier: y is complete -- it is the next layer's
+//        token (pipeline.cpp:318-336 with the attention blocks chained).
 //
-// The producer warp drives two rings at once: lane 0 the weight ring (query
-// items, key / value items, then the O-projection items, the first four
-// issued before the grid-dependency wait), lane 1 the cache stream into the
-// attention ring from the moment the length is known.  The consumer warps
-// project their query items first and their key / value items whenever those
-// have landed (between attention stages), so neither stream waits for the
-// other.
+// The producer warps drive two rings: warp 8 the weight ring (P1 items, then
+// the O-projection items, continuing across layers), warp 9 the cache stream.
+// Projection items beyond the 4-slot weight ring are parked in the attention
+// ring's stages.  In a chain, the next layer's parked items are loaded while
+// this layer finishes: into the stages the O-projection does not use as soon
+// as this CTA's attention has consumed them, into the rest once P3 is done --
+// so the next layer's projection finds its weights in shared memory when its
+// token (this layer's y) is complete.
 #include "common.cuh"
 #include "kernels.h"
 
@@ -61,7 +59,7 @@ constexpr int kST = 256;             // tokens per attention stage
 constexpr int kKS = 512;             // K per weight work item
 constexpr int kItem = 16 * kKS * 2;  // one weight work item: 16 rows x 512 bf16 = 16 KB
 constexpr int kNA = 4;               // weight ring slots
-constexpr int kXS = kKS * 2 + 64;    // bytes per staged token row (stride == 64 mod 128)
+constexpr int kXS = kKS * 2;         // bytes per staged token row (16-byte units XOR 4 on odd rows)
 constexpr int kMaxU = 10;            // (sequence, head) segments per CTA (host-checked)
 constexpr int kMaxSplits = 16;       // projection K splits (host-checked)
 constexpr int kWS = 36;              // floats per segment state in ws: acc[32], m, l, pad (16 B rows)
@@ -78,17 +76,20 @@ struct SC {
     static constexpr int XB2 = 2 * XB;        // an O-projection X slice: hi rows, then lo rows
     // per segment: absorbed query, the 8 warp states, the own token's K|V row
     static constexpr int RED = kMaxU * (R * 4 + kNW * (R + 2) * 4 + 4 * R) + (R + 4) * 4;  // + the partner's state
-    static constexpr int CUTB = (kMaxG + 1) * 8 + kMaxU * 32;  // + the segment table
+    static constexpr int PARTB = 2 * kNA * 16 * MT * 16 * 4;  // P3 partial tiles [2][kNA][16][MT*16] fp32
+    static constexpr bool PART_IN_RED = PARTB <= RED;          // the merge area is free during P3
+    static constexpr int CUTB = (kMaxG + 1) * 8 + kMaxU * 32 + 16;  // + the segment table + (pos, nseg)
     static constexpr int FIXED = kNA * kItem + XB + RED + CUTB + 768;
     static constexpr int NB_RAW = (225 * 1024 - FIXED) / STAGE;
     static constexpr int NB = NB_RAW > 6 ? 6 : NB_RAW;
+    static constexpr int RING = NB * STAGE;
     static constexpr int B_OFF = kNA * kItem;
     static constexpr int X_OFF = B_OFF + NB * STAGE;
     static constexpr int RED_OFF = X_OFF + XB;
     static constexpr int CUT_OFF = RED_OFF + RED;
     static constexpr int BAR_OFF = CUT_OFF + CUTB;
     static constexpr int SMEM = BAR_OFF + 512;
-    static constexpr bool OK = NB_RAW >= 2;
+    static constexpr bool OK = NB_RAW >= 2 && XB2 + (PART_IN_RED ? 0 : PARTB) <= NB * STAGE;
 };
 
 WSVD_DEV float ex2(float x) {
@@ -109,8 +110,9 @@ WSVD_DEV uint64_t gtimer() {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     return t;
 }
+// phase marks of layer a.trace_layer (variable l in scope)
 #define STEP_MARK(k) \
-    do { if (a.trace && (tid & 31) == 0) a.trace[cta * kTr + (k)] = gtimer(); } while (0)
+    do { if (a.trace && l == a.trace_layer && (tid & 31) == 0) a.trace[cta * kTr + (k)] = gtimer(); } while (0)
 
 WSVD_DEV unsigned ld_acquire(const unsigned* p) {
     unsigned v;
@@ -125,10 +127,17 @@ WSVD_DEV unsigned atom_add_acq_rel(unsigned* p) {
     asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
     return old;
 }
+// wait until the monotone count reaches target (modulo 2^32: the counts wrap
+// after ~10^7 steps; the signed difference stays meaningful)
 WSVD_DEV void wait_count(const unsigned* p, unsigned target) {
-    while (ld_acquire(p) < target) {
+    while (static_cast<int>(ld_acquire(p) - target) < 0) {
     }
 }
+WSVD_DEV void mbar_arrive_n(uint64_t* bar, uint32_t n) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(n) : "memory");
+}
+// generic-proxy shared-memory writes before async-proxy (TMA) writes to the same bytes
+WSVD_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Grid-wide barrier among the consumer and helper warps of every CTA (all
 // CTAs are resident: one per SM).  bar is a monotone arrival count; arrival is
@@ -161,7 +170,7 @@ WSVD_DEV long long cut_row(int c, int G, long long T, int pos) {
 struct Seg {
     int bh, t0, t1;
 };
-// this CTA's segments, resolved once per step: region, rows, and the CTAs
+// this CTA's segments, resolved once per layer: region, rows, and the CTAs
 // [c0, c1) whose ranges reach into the region (owners of them hold a part)
 struct SegInfo {
     int bh, t0, t1, owners, c0, c1, pad0, pad1;
@@ -208,10 +217,13 @@ WSVD_DEV void seg_owners(const long long* cut, int G, int pos, int bh, int& c0, 
     c1 = c;
 }
 
+// byte offset of 16-byte unit u of staged token row m (odd rows XOR 4: the
+// fragment loads of rows g and g + 1 hit disjoint bank quads)
+WSVD_DEV uint32_t xrow_off(int m, int u) { return static_cast<uint32_t>(m * kXS + ((u ^ ((m & 1) << 2)) * 16)); }
+
 // fp32 X[rows][ldx] columns [k0, k0 + kKS) -> bf16 smem [MT*16][kXS], zero
 // padded.  Every load of the thread is issued before the first is consumed:
-// the slice costs one memory latency, not one per item (x is usually not in
-// L2 when the step starts; this is on the critical path to the query).
+// the slice costs one memory latency, not one per item.
 template <int MT>
 WSVD_DEV void stage_rows(const float* X, int rows, int ldx, int kvalid, int k0, uint8_t* xs, int ctid,
                          uint64_t* issued = nullptr) {
@@ -251,7 +263,7 @@ WSVD_DEV void stage_rows(const float* X, int rows, int ldx, int kvalid, int k0, 
         uint4 o;
         o.x = pack_bf16x2(v[u][0].x, v[u][0].y); o.y = pack_bf16x2(v[u][0].z, v[u][0].w);
         o.z = pack_bf16x2(v[u][1].x, v[u][1].y); o.w = pack_bf16x2(v[u][1].z, v[u][1].w);
-        *reinterpret_cast<uint4*>(xs + m * kXS + kk * 2) = o;
+        *reinterpret_cast<uint4*>(xs + xrow_off(m, kk / 8)) = o;
     }
 }
 
@@ -264,7 +276,7 @@ WSVD_DEV void item_mma(uint32_t slot_addr, uint32_t xs_addr, int lane, float (&f
     const uint32_t swz = static_cast<uint32_t>((g & 1) << 2);
     const uint32_t row_lo = slot_addr + static_cast<uint32_t>(g * kKS * 2);
     const uint32_t row_hi = row_lo + static_cast<uint32_t>(8 * kKS * 2);
-    const uint32_t xbase = xs_addr + static_cast<uint32_t>(g * kXS + t * 16);
+    const uint32_t xbase = xs_addr + static_cast<uint32_t>(g * kXS);  // token rows g (+ 8, 16, ...): same swizzle
 #pragma unroll
     for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -280,7 +292,7 @@ WSVD_DEV void item_mma(uint32_t slot_addr, uint32_t xs_addr, int lane, float (&f
         for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
-                const uint4 xv = lds128(xbase + static_cast<uint32_t>((mt * 16 + hh * 8) * kXS + b * 64));
+                const uint4 xv = lds128(xbase + static_cast<uint32_t>((mt * 16 + hh * 8) * kXS) + uoff);
                 mma_bf16_16816(facc[mt][hh], wl.x, wh.x, wl.y, wh.y, xv.x, xv.y);
                 mma_bf16_16816(facc[mt][hh], wl.z, wh.z, wl.w, wh.w, xv.z, xv.w);
             }
@@ -288,7 +300,7 @@ WSVD_DEV void item_mma(uint32_t slot_addr, uint32_t xs_addr, int lane, float (&f
 }
 
 template <int R, int MT>
-__global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
+__global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_constant__ StepArgs a) {
     static_assert(R == 32, "the fused step is specialised for rank 32 (one latent dim per lane)");
     using C = SC<R, MT>;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -301,6 +313,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     float* pst = reinterpret_cast<float*>(nrow + kMaxU * 2 * R);  // [R+2] the pair partner's state (DSMEM)
     long long* cut = reinterpret_cast<long long*>(smem + C::CUT_OFF);  // [G+1]
     SegInfo* sinf = reinterpret_cast<SegInfo*>(cut + kMaxG + 1);          // [kMaxU]
+    volatile int* meta = reinterpret_cast<volatile int*>(sinf + kMaxU);   // [0] pos [1] nseg of the current layer
     uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     uint64_t* emptyA = fullA + kNA;
     uint64_t* fullB = emptyA + kNA;
@@ -313,11 +326,15 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     uint64_t* b1bar = wdone + C::NB;      // grid barrier 1 passed (gates the parked stages' refill)
     uint64_t* pbar = b1bar + 1;           // the pair partner's state landed (DSMEM)
     uint64_t* xin = pbar + 1;             // every consumer warp has requested its token-slice loads
-    static_assert((2 * kNA + 2 * C::NB + 2 * kMaxU + 1 + 2 * C::NB + C::NB + 3) * 8 <= C::SMEM - C::BAR_OFF,
+    uint64_t* tready = xin + 1;           // the layer's range / segment table is built (helper)
+    uint64_t* p3done = tready + 1;        // the layer's O-projection no longer uses the attention ring
+    static_assert((2 * kNA + 2 * C::NB + 2 * kMaxU + 1 + 2 * C::NB + C::NB + 5) * 8 <= C::SMEM - C::BAR_OFF,
                   "mbarriers overflow their shared-memory region");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x, cta = blockIdx.x;
+    const int nL = a.nlayers;
+    int l = 0;  // the layer (trace marks)
 
     STEP_MARK(0);
     if (a.trace && tid == 0) {
@@ -325,8 +342,9 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
         a.trace[cta * kTr + 10] = smid;
     }
-    // ---- projection geometry: K split ps, a contiguous run [plo, phi) of the
-    // split's 16-row W-tiles (rows n = (head*3 + role)*R + i, capi.cu packing)
+    // ---- projection geometry (the same for every layer): K split ps, a
+    // contiguous run [plo, phi) of the split's 16-row W-tiles (rows n =
+    // (head*3 + role)*R + i, capi.cu packing)
     const int splits = a.Kp / kKS;
     const int cps = G / splits;  // CTAs per projection split
     const int ps = cta % splits, pj = cta / splits;
@@ -335,40 +353,53 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     const int phi = pj < cps ? static_cast<int>(static_cast<long>(pj + 1) * ptiles / cps) : 0;
     const int np1 = phi - plo;
     const int osplits = a.oKp / kKS;
-    // P3 items (tile, K split).  Device y with two K splits: CTA c takes split
-    // c % 2 of a run of tiles, so it stages only that split's X rows; the two
-    // partial sums meet in y through fp32 red.add onto zeros -- with exactly
-    // two addends the result does not depend on their order (0 + a + b ==
-    // 0 + b + a), so y stays run-to-run deterministic.  Otherwise (host y --
-    // mapped pinned memory, no atomics over the bus -- or one K split) the
-    // CTA owns whole tiles with all their splits and sums them itself; host y
-    // is a contiguous run of tiles, written as 16-byte stores over 64-128-byte
-    // row segments (bus writes drain faster).
-    const bool ycontig = a.x_host != 0;
-    const bool ysplit = !ycontig && osplits == 2;
-    const int cps3 = G / 2;
-    int t3lo, nt3, t3step, p3s0, p3ns;
-    if (ysplit) {
-        const int pj3 = cta / 2;
-        t3lo = pj3 < cps3 ? static_cast<int>(static_cast<long>(pj3) * a.otiles / cps3) : 0;
-        nt3 = pj3 < cps3 ? static_cast<int>(static_cast<long>(pj3 + 1) * a.otiles / cps3) - t3lo : 0;
-        t3step = 1;
-        p3s0 = cta % 2;
-        p3ns = 1;
-    } else {
-        t3lo = ycontig ? static_cast<int>(static_cast<long>(cta) * a.otiles / G) : cta;
-        nt3 = ycontig ? static_cast<int>(static_cast<long>(cta + 1) * a.otiles / G) - t3lo
-                      : (cta < a.otiles ? (a.otiles - 1 - cta) / G + 1 : 0);
-        t3step = ycontig ? 1 : G;  // tile i of this CTA: t3lo + i * t3step
-        p3s0 = 0;
-        p3ns = osplits;
-    }
-    const int np3 = nt3 * p3ns;  // <= kNA (host-checked)
+    // P3 items (tile, K split) of layer l.  Device y with two K splits: CTA c
+    // takes split c % 2 of a run of tiles, so it stages only that split's X
+    // rows; the two partial sums meet in y through fp32 red.add onto zeros --
+    // with exactly two addends the result does not depend on their order
+    // (0 + a + b == 0 + b + a), so y stays run-to-run deterministic.
+    // Otherwise (host y -- mapped pinned memory, no atomics over the bus -- or
+    // one K split) the CTA owns whole tiles with all their splits and sums them
+    // itself; host y is a contiguous run of tiles, written as 16-byte stores
+    // over 64-128-byte row segments (bus writes drain faster).  The X slices
+    // sit at the end of the attention ring, the partial tiles in the merge area.
+    struct P3G {
+        int t3lo, nt3, t3step, p3s0, p3ns, np3, per, xoff, p3lo;
+        bool ycontig, ysplit;
+    };
+    auto p3geom = [&](int li) {
+        P3G g;
+        g.ycontig = a.y_host != 0 && li == nL - 1;
+        g.ysplit = !g.ycontig && osplits == 2;
+        const int cps3 = G / 2;
+        if (g.ysplit) {
+            const int pj3 = cta / 2;
+            g.t3lo = pj3 < cps3 ? static_cast<int>(static_cast<long>(pj3) * a.otiles / cps3) : 0;
+            g.nt3 = pj3 < cps3 ? static_cast<int>(static_cast<long>(pj3 + 1) * a.otiles / cps3) - g.t3lo : 0;
+            g.t3step = 1;
+            g.p3s0 = cta % 2;
+            g.p3ns = 1;
+        } else {
+            g.t3lo = g.ycontig ? static_cast<int>(static_cast<long>(cta) * a.otiles / G) : cta;
+            g.nt3 = g.ycontig ? static_cast<int>(static_cast<long>(cta + 1) * a.otiles / G) - g.t3lo
+                              : (cta < a.otiles ? (a.otiles - 1 - cta) / G + 1 : 0);
+            g.t3step = g.ycontig ? 1 : G;  // tile i of this CTA: t3lo + i * t3step
+            g.p3s0 = 0;
+            g.p3ns = osplits;
+        }
+        g.np3 = g.nt3 * g.p3ns;  // <= kNA (host-checked)
+        const int pb = C::PART_IN_RED ? 0 : C::PARTB;
+        g.per = (g.p3ns * C::XB2 + pb <= C::RING) ? g.p3ns : 1;  // K splits staged together
+        g.xoff = C::RING - g.per * C::XB2;
+        g.p3lo = g.xoff - pb;  // first attention-ring byte P3 uses
+        return g;
+    };
     // Projection items beyond the 4-slot weight ring are parked in the
     // attention ring (2 per stage, in consumption order): the attention cannot
     // start before grid barrier 1 anyway, and with every item in flight at
     // once the projection costs one memory round trip instead of one per ring
-    // turn.  Ring-A sequence: P1 items k < 4 or k >= 4 + nBH, then the P3 items.
+    // turn.  Ring-A sequence of a layer: P1 items k < 4 or k >= 4 + nBH, then
+    // its P3 items; the sequence continues across the layers of a chain.
     const int nBH = min(max(np1 - kNA, 0), 2 * C::NB);
     const int nA1 = np1 - nBH;
     const int nWS = (nBH + 1) / 2;  // attention stages holding parked items (the first nWS)
@@ -394,57 +425,60 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
             mbar_init(b1bar, 1);
             mbar_init(pbar, 1);
             mbar_init(xin, kNW);
+            mbar_init(tready, 1);
+            mbar_init(p3done, 1);
         }
         fence_mbar_init();  // every lane: the fence covers the executing thread's inits
     }
     __syncthreads();
     if (a.cluster > 1) cluster_sync_all();  // the partner's barriers are initialised before any remote arrive
-    // The weights are constant across steps: the producer streams them before
-    // the predecessor has drained (programmatic dependent launch); the token,
-    // the length and the cache rows wait for it.
-    auto a_src = [&](int ia) -> const uint8_t* {  // ring-A item ia -> source
+    // ring-A item ia (in-layer sequence) of layer li -> source
+    auto a_src = [&](int li, int ia) -> const uint8_t* {
+        const StepLayer& Ly = a.layer[li];
         if (ia < nA1) {
             const int k = ia < kNA ? ia : ia + nBH;
-            return a.A + (static_cast<size_t>(plo + k) * splits + ps) * kItem;
+            return Ly.A + (static_cast<size_t>(plo + k) * splits + ps) * kItem;
         }
+        const P3G g = p3geom(li);
         const int j = ia - nA1;
-        return a.Wo + (static_cast<size_t>(t3lo + (j / p3ns) * t3step) * osplits + p3s0 + j % p3ns) * kItem;
+        return Ly.Wo + (static_cast<size_t>(g.t3lo + (j / g.p3ns) * g.t3step) * osplits + g.p3s0 + j % g.p3ns) * kItem;
     };
-    // the projection items parked in the attention ring: before the
-    // grid-dependency wait, or (a.x_first) once the token slice has been
-    // requested -- its loads then do not queue behind 100+ KB of weights
-    auto issue_parked = [&]() {
-        for (int b = 0; b < nBH; ++b) {
+    auto parked_src = [&](int li, int b) -> const uint8_t* {
+        return a.layer[li].A + (static_cast<size_t>(plo + kNA + b) * splits + ps) * kItem;
+    };
+    auto issue_parked = [&](int li, int b0, int b1) {
+        for (int b = b0; b < b1 && b < nBH; ++b) {
             mbar_arrive_expect_tx(&wfull[b], kItem);
-            tma_bulk_g2s(parked(b), a.A + (static_cast<size_t>(plo + kNA + b) * splits + ps) * kItem, kItem,
-                         &wfull[b]);
+            tma_bulk_g2s(parked(b), parked_src(li, b), kItem, &wfull[b]);
         }
     };
+    // The weights are constant across steps: the producer streams layer 0's
+    // before the predecessor has drained (programmatic dependent launch); the
+    // token, the length and the cache rows wait for it.
     int ia_pre = 0;
+    const int na0 = nA1 + p3geom(0).np3;
     if (warp == kNW && lane == 0) {
-        for (; ia_pre < kNA && ia_pre < nA1 + np3; ++ia_pre) {
+        for (; ia_pre < kNA && ia_pre < na0; ++ia_pre) {
             mbar_arrive_expect_tx(&fullA[ia_pre], kItem);
-            tma_bulk_g2s(ringA + ia_pre * kItem, a_src(ia_pre), kItem, &fullA[ia_pre]);
+            tma_bulk_g2s(ringA + ia_pre * kItem, a_src(0, ia_pre), kItem, &fullA[ia_pre]);
         }
-        if (!a.x_first) issue_parked();
+        if (!a.x_first) issue_parked(0, 0, nBH);
     }
+    const int nbh = a.B * a.nh;
     if (warp == kNW + 1 && lane == 0 && a.pos_hint > 0 && a.pre_stages > 0) {
         // Before the predecessor has drained: request the first stages of this
-        // CTA's cache range into L2 (a prefetch is only a hint -- L2 is the
-        // point of coherence, so a row the predecessor still writes stays
-        // correct), at the length the host expects; HBM is otherwise idle
-        // until the projection weights and the token arrive
-        const long long Th = static_cast<long long>(a.B * a.nh) * a.pos_hint;
+        // CTA's layer-0 cache range into L2 (a prefetch is only a hint -- L2 is
+        // the point of coherence), at the length the host expects
+        const long long Th = static_cast<long long>(nbh) * a.pos_hint;
         long long cc[2] = {cut_row(cta, G, Th, a.pos_hint), cut_row(cta + 1, G, Th, a.pos_hint)};
-        // a two-entry table seen from this CTA: seg_at(cut - cta, ...)
-        const long long* ct = cc - cta;
-        const int ns = seg_count(ct, cta, G, a.pos_hint, a.B * a.nh);
+        const long long* ct = cc - cta;  // a two-entry table seen from this CTA
+        const int ns = seg_count(ct, cta, G, a.pos_hint, nbh);
         int left = a.pre_stages;
         for (int p = 0; p < ns && left > 0; ++p) {
             const Seg sg = seg_at(ct, cta, G, a.pos_hint, (cta & 1) ? ns - 1 - p : p);
             for (int t = sg.t0; t < sg.t1 && left > 0; t += kST, --left) {
                 const int rows = min(kST, sg.t1 - t);
-                prefetch_l2_bulk(a.cache + (static_cast<size_t>(sg.bh) * a.cap + t) * C::ROWB,
+                prefetch_l2_bulk(a.layer[0].cache + (static_cast<size_t>(sg.bh) * a.layer[0].cap + t) * C::ROWB,
                                  static_cast<uint32_t>(((rows * C::ROWB + 1023) / 1024) * 1024));
             }
         }
@@ -453,568 +487,664 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const StepArgs a) {
     griddep_launch_dependents();
     STEP_MARK(1);
 
-    const int pos = *a.d_len;  // the new token's row; attention covers rows 0..pos-1 + the new one
-    const unsigned epoch = static_cast<unsigned>(*a.epoch);  // fused steps so far (barrier generations)
-    const int len = pos + 1;
-    const int nbh = a.B * a.nh;
-    const long long T = static_cast<long long>(nbh) * pos;
-    for (int c = tid; c <= G; c += kThr) cut[c] = cut_row(c, G, T, pos);
-    __syncthreads();
-    const int nseg = seg_count(cut, cta, G, pos, nbh);  // <= kMaxU (host-checked)
-    if (a.trace && tid == 0) a.trace[cta * kTr + 11] = static_cast<uint64_t>(nseg);
-    if (tid < nseg) {  // the segment table (64-bit index arithmetic, once)
-        const Seg sg = seg_at(cut, cta, G, pos, tid);
-        SegInfo& si = sinf[tid];
-        si.bh = sg.bh;
-        si.t0 = sg.t0;
-        si.t1 = sg.t1;
-        seg_owners(cut, G, pos, sg.bh, si.c0, si.c1);
-        int owners = 0;
-        for (int c = si.c0; c < si.c1; ++c) owners += (cut[c] < cut[c + 1] || pos == 0) ? 1 : 0;
-        si.owners = owners;
-    }
-    __syncthreads();
+    const unsigned epoch = static_cast<unsigned>(*a.epoch);  // fused launches so far (x-fetch generations)
+    const unsigned bgen0 = *a.bgen;                          // grid barriers completed so far
+    unsigned gen = bgen0;
     // Odd CTAs walk their segments backwards: the region a pair (2k, 2k+1)
     // shares is then the LAST one both attend (its two parts finish together
     // and meet through distributed shared memory), the region shared with
     // the next pair the FIRST one (its merge through L2 happens early, off
     // the critical path).  Processing order p -> segment (range order) j.
     const bool rev = (cta & 1) != 0;
-    auto seg_of = [&](int p) { return rev ? nseg - 1 - p : p; };
-    const size_t cap = static_cast<size_t>(a.cap);
     const size_t pstride = static_cast<size_t>(a.B) * a.Nrows;
 
-    // ================================================================ producer
+    // ================================================================ producers
     if (warp == kNW || warp == kNW + 1) {
         if (warp == kNW && lane == 0) {
+            // the weight ring: every layer's P1 ring items, then its P3 items
             if (a.x_first && nBH > 0) {
                 mbar_wait(xin, 0u);
-                issue_parked();
+                issue_parked(0, 0, nBH);
             }
-            int ia = ia_pre;  // the first weight items went out before griddep_wait
-            const int na = nA1 + np3;
-            auto issue_a = [&]() {
-                const int slot = ia % kNA;
-                const uint32_t ph = static_cast<uint32_t>(ia / kNA) & 1u;
-                mbar_wait(&emptyA[slot], ph ^ 1u);
-                mbar_arrive_expect_tx(&fullA[slot], kItem);
-                tma_bulk_g2s(ringA + slot * kItem, a_src(ia), kItem, &fullA[slot]);
-                ++ia;
-            };
-            while (ia < na) issue_a();  // projection rest, O-proj weights (as the weight ring frees)
+            unsigned ia_g = static_cast<unsigned>(ia_pre);  // items issued this launch
+            for (int li = 0; li < nL; ++li) {
+                const int na = nA1 + p3geom(li).np3;
+                for (int i = (li == 0 ? ia_pre : 0); i < na; ++i) {
+                    const int slot = static_cast<int>(ia_g % kNA);
+                    mbar_wait(&emptyA[slot], ((ia_g / kNA) & 1u) ^ 1u);
+                    mbar_arrive_expect_tx(&fullA[slot], kItem);
+                    tma_bulk_g2s(ringA + slot * kItem, a_src(li, i), kItem, &fullA[slot]);
+                    ++ia_g;
+                }
+            }
         } else if (warp == kNW + 1 && lane == 0) {
             // the cache stream, from its own warp: waiting for a ring-A slot
             // never holds it up (divergent lanes of one warp are scheduled as one)
             const uint64_t pol = policy_evict_first();
-            int ib = 0;
-            auto issue_stage = [&](const SegInfo& sg, int t) {
-                const int rows = min(kST, sg.t1 - t);
-                // every slot's first fill is a whole stage (finite rows past the
-                // end, which the consumers read times p = 0; the allocation is padded)
-                const uint32_t rbytes = ib < C::NB ? static_cast<uint32_t>(C::STAGE)
-                                                   : static_cast<uint32_t>(min(C::STAGE, ((rows * C::ROWB + 1023) / 1024) * 1024));
-                const int slot = ib % C::NB;
-                if (ib < nWS) {
-                    mbar_wait(&wdone[slot], 0u);  // its parked projection items are consumed
-                    mbar_wait(b1bar, 0u);         // and grid barrier 1 has passed
+            uint32_t par = 0;  // per attention-ring slot: parity of its fills so far
+            for (int li = 0; li < nL; ++li) {
+                const uint32_t lp = static_cast<uint32_t>(li) & 1u;
+                if (li > 0) {
+                    // this layer's parked projection items: each stage as soon as
+                    // the previous layer's attention has consumed it and, where
+                    // the previous O-projection stages its rows, once P3 is done
+                    const P3G gp = p3geom(li - 1);
+                    bool p3w = false;
+                    for (int st = 0; st < nWS; ++st) {
+                        mbar_wait(&emptyB[st], ((par >> st) & 1u) ^ 1u);
+                        if (!p3w && (st + 1) * C::STAGE > gp.p3lo) {
+                            mbar_wait(p3done, lp ^ 1u);
+                            p3w = true;
+                        }
+                        issue_parked(li, 2 * st, 2 * st + 2);
+                    }
+                    // every other stage of the ring may hold P3 data until P3 is done
+                    if (!p3w) mbar_wait(p3done, lp ^ 1u);
                 }
-                mbar_wait(&emptyB[slot], (static_cast<uint32_t>(ib / C::NB) & 1u) ^ 1u);
-                mbar_arrive_expect_tx(&fullB[slot], rbytes);
-                const uint8_t* src = a.cache + (static_cast<size_t>(sg.bh) * cap + t) * C::ROWB;
-                tma_bulk_g2s_stream(ringB + slot * C::STAGE, src, rbytes, &fullB[slot], pol);
-                ++ib;
-            };
-            for (int p = 0; p < nseg; ++p) {
-                const SegInfo& sg = sinf[seg_of(p)];
-                for (int t = sg.t0; t < sg.t1; t += kST) issue_stage(sg, t);
+                mbar_wait(tready, lp);
+                const int pos = meta[0], nseg = meta[1];
+                const StepLayer& Ly = a.layer[li];
+                const size_t cap = static_cast<size_t>(Ly.cap);
+                int ib = 0;  // stage fills of this layer: slot ib % NB
+                for (int p = 0; p < nseg; ++p) {
+                    const SegInfo& sg = sinf[rev ? nseg - 1 - p : p];
+                    for (int t = sg.t0; t < sg.t1; t += kST) {
+                        const int rows = min(kST, sg.t1 - t);
+                        // every slot's first fill of a layer is a whole stage (finite
+                        // rows past the end, which the consumers read times p = 0;
+                        // the allocation is padded): stale bytes of parked items or
+                        // P3 partials never meet the tensor cores
+                        const uint32_t rbytes = ib < C::NB ? static_cast<uint32_t>(C::STAGE)
+                                                           : static_cast<uint32_t>(min(C::STAGE, ((rows * C::ROWB + 1023) / 1024) * 1024));
+                        const int slot = ib % C::NB;
+                        if (ib < nWS) {
+                            mbar_wait(&wdone[slot], lp);  // its parked projection items are consumed
+                            mbar_wait(b1bar, lp);         // and grid barrier 1 has passed
+                        }
+                        mbar_wait(&emptyB[slot], ((par >> slot) & 1u) ^ 1u);
+                        par ^= 1u << slot;
+                        mbar_arrive_expect_tx(&fullB[slot], rbytes);
+                        const uint8_t* src = Ly.cache + (static_cast<size_t>(sg.bh) * cap + t) * C::ROWB;
+                        tma_bulk_g2s_stream(ringB + slot * C::STAGE, src, rbytes, &fullB[slot], pol);
+                        ++ib;
+                    }
+                }
+                if (a.l2_next && li + 1 < nL) {
+                    // the next layer's items that are loaded last (after this
+                    // layer's P3): into L2 now, while this CTA's last stages stream
+                    const P3G g = p3geom(li);
+                    for (int b = 0; b < nBH; ++b)
+                        if ((b / 2 + 1) * C::STAGE > g.p3lo) prefetch_l2_bulk(parked_src(li + 1, b), kItem);
+                    for (int i = 0; i < nA1; ++i) prefetch_l2_bulk(a_src(li + 1, i), kItem);
+                }
             }
         }
         return;
     }
+
+    // ---- the range / segment table of layer li (helper warp; off the
+    // consumers' path: P1 does not need it)
+    auto build_table = [&](int li) {
+        const int pos = *static_cast<volatile const int*>(a.layer[li].d_len);
+        const long long T = static_cast<long long>(nbh) * pos;
+        for (int c = lane; c <= G; c += 32) cut[c] = cut_row(c, G, T, pos);
+        __syncwarp();
+        const int nseg = seg_count(cut, cta, G, pos, nbh);  // <= kMaxU (host-checked)
+        if (lane < nseg) {  // the segment table (64-bit index arithmetic, once)
+            const Seg sg = seg_at(cut, cta, G, pos, lane);
+            SegInfo& si = sinf[lane];
+            si.bh = sg.bh;
+            si.t0 = sg.t0;
+            si.t1 = sg.t1;
+            seg_owners(cut, G, pos, sg.bh, si.c0, si.c1);
+            int owners = 0;
+            for (int c = si.c0; c < si.c1; ++c) owners += (cut[c] < cut[c + 1] || pos == 0) ? 1 : 0;
+            si.owners = owners;
+        }
+        if (lane == 0) {
+            meta[0] = pos;
+            meta[1] = nseg;
+            if (a.trace && li == a.trace_layer) a.trace[cta * kTr + 11] = static_cast<uint64_t>(nseg);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(tready);
+    };
+    if (warp == kHelp) build_table(0);
 
     const int g8 = lane >> 2, t4 = lane & 3;
-    // ---- P1 (consumer warps): latent projection of this CTA's K split
-    if (warp < kNW) {
-        const float* xsrc = a.x;
-        if (a.x_host && pj < cps) {
-            // x lives in mapped (pinned) host memory: the cps CTAs of this K
-            // split each fetch 1/cps of its [B][kKS] slice over the bus into
-            // the device copy xd and publish a count; all stage from xd once
-            // the count is complete (the host bytes cross the bus once)
-            const int per = (a.B * kKS / 4 + cps - 1) / cps;  // float4 items per CTA
-            for (int i = pj * per + tid; i < min((pj + 1) * per, a.B * kKS / 4); i += 32 * kNW) {
-                const int m = i / (kKS / 4), k4 = i - m * (kKS / 4);
-                const size_t off = static_cast<size_t>(m) * a.E + ps * kKS + 4 * k4;
-                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-                if (ps * kKS + 4 * k4 + 4 <= a.E) v = __ldcv(reinterpret_cast<const float4*>(a.x + off));
-                *reinterpret_cast<float4*>(a.xd + off) = v;
+    uint32_t parc = 0;  // consumers: per attention-ring slot, parity of the fills consumed
+    unsigned abase = 0; // ring-A sequence index of the layer's first item
+    unsigned pcnt = 0;  // helper: pair-partner states received (pbar phases)
+    unsigned p3cnt = 0; // consumers: TMA-staged P3 rounds (p3bar phases)
+    for (l = 0; l < nL; ++l) {
+        const StepLayer& Ly = a.layer[l];
+        const uint32_t lp = static_cast<uint32_t>(l) & 1u;
+        const P3G g3 = p3geom(l);
+        if (l > 0) {
+            STEP_MARK(0);
+            STEP_MARK(1);
+        }
+        // ---- P1 (consumer warps): latent projection of this CTA's K split
+        if (warp < kNW) {
+            const float* xsrc = l == 0 ? a.x : a.layer[l - 1].y;
+            if (l == 0 && a.x_host && pj < cps) {
+                // x lives in mapped (pinned) host memory: the cps CTAs of this K
+                // split each fetch 1/cps of its [B][kKS] slice over the bus into
+                // the device copy xd and publish a count; all stage from xd once
+                // the count is complete (the host bytes cross the bus once)
+                const int per = (a.B * kKS / 4 + cps - 1) / cps;  // float4 items per CTA
+                for (int i = pj * per + tid; i < min((pj + 1) * per, a.B * kKS / 4); i += 32 * kNW) {
+                    const int m = i / (kKS / 4), k4 = i - m * (kKS / 4);
+                    const size_t off = static_cast<size_t>(m) * a.E + ps * kKS + 4 * k4;
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (ps * kKS + 4 * k4 + 4 <= a.E) v = __ldcv(reinterpret_cast<const float4*>(a.x + off));
+                    *reinterpret_cast<float4*>(a.xd + off) = v;
+                }
+                named_bar_sync(2, 32 * kNW);
+                if (tid == 0) {
+                    red_release(a.xcnt + ps);
+                    wait_count(a.xcnt + ps, static_cast<unsigned>(cps) * (epoch + 1u));
+                }
+                named_bar_sync(2, 32 * kNW);
+                xsrc = a.xd;
+            } else if (l == 0 && pj < cps && tid == 0) {
+                // keep the counters' invariant (cps arrivals per fused launch) in device mode
+                asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.xcnt + ps) : "memory");
             }
+            if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid, (l == 0) ? xin : nullptr);
             named_bar_sync(2, 32 * kNW);
-            if (tid == 0) {
-                red_release(a.xcnt + ps);
-                wait_count(a.xcnt + ps, static_cast<unsigned>(cps) * (epoch + 1u));
-            }
-            named_bar_sync(2, 32 * kNW);
-            xsrc = a.xd;
-        } else if (pj < cps && tid == 0) {
-            // keep the counters' invariant (cps arrivals per fused step) in device mode
-            asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.xcnt + ps) : "memory");
-        }
-        if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid, xin);
-        named_bar_sync(2, 32 * kNW);
-        // all kNW consumer warps take items k = warp mod kNW in item order:
-        // the weight ring's four (in flight first) and then the parked ones
-        for (int k = warp; k < np1; k += kNW) {
-            float facc[MT][2][4];
-            if (k >= kNA && k < kNA + nBH) {
-                const int b = k - kNA;
-                mbar_wait(&wfull[b], 0u);
-                item_mma<MT>(smem_u32(parked(b)), smem_u32(xbuf), lane, facc);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&wdone[b / 2]);
-            } else {
-                const int ia = k < kNA ? k : k - nBH, slot = ia % kNA;
-                mbar_wait(&fullA[slot], static_cast<uint32_t>(ia / kNA) & 1u);
-                item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(xbuf), lane, facc);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyA[slot]);
-            }
-            const int tile = plo + k;
-            float* P = a.P + static_cast<size_t>(ps) * pstride;
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int n = tile * 16 + g8 + ((i & 2) ? 8 : 0);
-                        const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
-                        if (m < a.B) P[static_cast<size_t>(m) * a.Nrows + n] = facc[mt][hh][i];
-                    }
-        }
-    }
-    // helper: the first segment's M_QK column does not depend on the projection;
-    // load it while the barrier drains (one L2 round trip off the critical path)
-    float mq0[R];
-    if (warp == kHelp && nseg > 0) {
-        const int h0 = sinf[seg_of(0)].bh % a.nh;
-        const float* mq = a.mqk + static_cast<size_t>(h0) * R * R + lane;
-#pragma unroll
-        for (int jj = 0; jj < R; ++jj) mq0[jj] = __ldg(mq + jj * R);
-    }
-    named_bar_sync(1, kSync);
-    STEP_MARK(2);  // every projection warp of this CTA is done
-    grid_sync(a.bar, (2u * epoch + 1u) * G);  // consumers + helper: every projection partial is written
-    if (tid == 0) mbar_arrive(b1bar);
-    STEP_MARK(3);
-
-    if (warp == kHelp) {
-        // ============================================================ helper warp
-        // (a) per segment, in processing order, ahead of the consumers:
-        //     qt = (sum_split c_Q) . M_QK (the append epilogue's order: fixed
-        //     split order, sequential fma); the segment that ends a region also
-        //     gets the step's own K / V latents (summed the same way, rounded to
-        //     the cache's bf16 -- the row the reference appends before
-        //     attending, decode.cpp:143-149), written to cache row pos
-        auto prep = [&](int p, const float (&mqv)[R]) {
-            const int j = seg_of(p);
-            const SegInfo& s = sinf[j];
-            const int b = s.bh / a.nh, h = s.bh - b * a.nh;
-            const bool own = s.t1 == pos;
-            const float* pb = a.P + static_cast<size_t>(b) * a.Nrows + static_cast<size_t>(h) * 3 * R + lane;
-            float pv[3][kMaxSplits];
-#pragma unroll
-            for (int sp = 0; sp < kMaxSplits; ++sp) {
-                pv[0][sp] = sp < splits ? __ldcg(pb + sp * pstride) : 0.f;
-                pv[1][sp] = (own && sp < splits) ? __ldcg(pb + sp * pstride + R) : 0.f;
-                pv[2][sp] = (own && sp < splits) ? __ldcg(pb + sp * pstride + 2 * R) : 0.f;
-            }
-            float v[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-            for (int sp = 0; sp < kMaxSplits; ++sp)
-#pragma unroll
-                for (int r = 0; r < 3; ++r) v[r] += pv[r][sp];  // zeros past `splits` leave the sum exact
-            float qt = 0.f;
-#pragma unroll
-            for (int jj = 0; jj < R; ++jj) qt = fmaf(__shfl_sync(0xffffffffu, v[0], jj), mqv[jj], qt);
-            qts[j * R + lane] = qt;
-            if (own) {
-                uint8_t* region = a.cache + static_cast<size_t>(s.bh) * cap * C::ROWB;
-                const uint32_t grow = static_cast<uint32_t>(pos) * C::ROWB;
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    const __nv_bfloat16 bv = __float2bfloat16_rn(v[1 + half]);
-                    nrow[j * 2 * R + half * R + lane] = bv;
-                    *reinterpret_cast<__nv_bfloat16*>(region + cache_swz(grow + half * C::PART + 2 * lane)) = bv;
+            // the kNW consumer warps take items in turn: layer 0 the weight
+            // ring's four first (in flight first), later layers the parked ones
+            // first (loaded during the previous layer's tail)
+            for (int o = warp; o < np1; o += kNW) {
+                const int k = (l == 0) ? o : (o < nBH ? kNA + o : o - nBH);
+                float facc[MT][2][4];
+                if (k >= kNA && k < kNA + nBH) {
+                    const int b = k - kNA;
+                    mbar_wait(&wfull[b], lp);
+                    item_mma<MT>(smem_u32(parked(b)), smem_u32(xbuf), lane, facc);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&wdone[b / 2]);
+                } else {
+                    const unsigned ia = abase + static_cast<unsigned>(k < kNA ? k : k - nBH);
+                    const int slot = static_cast<int>(ia % kNA);
+                    mbar_wait(&fullA[slot], (ia / kNA) & 1u);
+                    item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(xbuf), lane, facc);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&emptyA[slot]);
                 }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&uready[j]);
-        };
-        if (nseg > 0) prep(0, mq0);
-        if (a.trace && lane == 0) a.trace[cta * kTr + 16] = gtimer();
-        for (int p = 1; p < nseg; ++p) {
-            const int h = sinf[seg_of(p)].bh % a.nh;
-            float mqv[R];
-            const float* mq = a.mqk + static_cast<size_t>(h) * R * R + lane;
+                const int tile = plo + k;
+                float* P = a.P + static_cast<size_t>(ps) * pstride;
 #pragma unroll
-            for (int jj = 0; jj < R; ++jj) mqv[jj] = __ldg(mq + jj * R);
-            prep(p, mqv);
-        }
-        if (nseg > 0) STEP_MARK(4);
-        // (b) per segment as the consumers finish it: merge the kNW warp states
-        //     in warp order (+ the own token for a region's last segment).  A
-        //     region held by one CTA is complete.  A region shared by the two
-        //     CTAs of a cluster pair: the odd CTA's (later) part crosses into the
-        //     even CTA through distributed shared memory and the even CTA
-        //     merges.  Any other shared region: every part publishes its state
-        //     to L2 and the last to arrive merges them all in range order
-        //     (SoftmaxState::merge, decode.cpp:59-75) -- nobody waits.
-        for (int p = 0; p < nseg; ++p) {
-            const int j = seg_of(p);
-            mbar_wait(&sfull[j], 0u);
-            if (p == 0) STEP_MARK(15);
-            const SegInfo& s = sinf[j];
-            const float* rb = wst + j * kNW * (R + 2);
-            float M = -INFINITY;
+                for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-            for (int w = 0; w < kNW; ++w) M = fmaxf(M, rb[w * (R + 2) + R]);
-            float L = 0.f, av = 0.f;
+                    for (int hh = 0; hh < 2; ++hh)
 #pragma unroll
-            for (int w = 0; w < kNW; ++w) {
-                const float mw = rb[w * (R + 2) + R];
-                if (mw == -INFINITY) continue;
-                const float f = ex2(mw - M);
-                L = fmaf(rb[w * (R + 2) + R + 1], f, L);
-                av = fmaf(rb[w * (R + 2) + lane], f, av);
-            }
-            if (s.t1 == pos) {
-                // SoftmaxState::observe of the own token (decode.cpp:35-57)
-                const float kf = __bfloat162float(nrow[j * 2 * R + lane]);
-                const float vf = __bfloat162float(nrow[j * 2 * R + R + lane]);
-                const float sn = warp_sum(qts[j * R + lane] * kf);
-                const float Mn = fmaxf(M, sn);
-                const float fo = ex2(M - Mn), fn = ex2(sn - Mn);  // fo = 0 when M = -inf
-                L = fmaf(L, fo, fn);
-                av = fmaf(av, fo, vf * fn);
-                M = Mn;
-            }
-            const int c0 = s.c0, c1 = s.c1, owners = s.owners;
-            const bool pair = a.cluster == 2 && owners == 2 && c1 - c0 == 2 && (c0 & 1) == 0;
-            float L2 = L, a2 = av;
-            if (pair && cta == c0 + 1) {
-                // the later part of the pair's shared region -> the even CTA
-                const uint32_t dst = cluster_map(smem_u32(pst), 0u);
-                st_cluster_f32(dst + 4u * lane, av);
-                if (lane == 0) {
-                    st_cluster_f32(dst + 4u * R, M);
-                    st_cluster_f32(dst + 4u * (R + 1), L);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive_remote(cluster_map(smem_u32(pbar), 0u));
-                continue;
-            }
-            if (pair) {
-                // this CTA holds the earlier part: it first, the partner's next
-                mbar_wait_cluster(pbar, 0u);
-                const float mc = pst[R], lc = pst[R + 1], ac = pst[lane];
-                if (mc != -INFINITY) {
-                    const float Mn = fmaxf(M, mc);
-                    const float fo = ex2(M - Mn), fc = ex2(mc - Mn);
-                    L2 = fmaf(lc, fc, L * fo);
-                    a2 = fmaf(ac, fc, av * fo);
-                }
-            } else if (owners > 1) {
-                float* wsp = a.ws + (static_cast<size_t>(cta) * kMaxU + j) * kWS;
-                wsp[lane] = av;
-                if (lane == 0) {
-                    wsp[R] = M;
-                    wsp[R + 1] = L;
-                }
-                __syncwarp();
-                unsigned old = 0;
-                if (lane == 0) old = atom_add_acq_rel(reinterpret_cast<unsigned*>(a.counters) + s.bh);
-                old = __shfl_sync(0xffffffffu, old, 0);
-                if (old != static_cast<unsigned>(owners - 1)) continue;  // another part merges
-                // ---- last arriver: every part of region bh in range order
-                float M2 = -INFINITY;
-                L2 = 0.f;
-                a2 = 0.f;
-                for (int c = c0; c < c1; ++c) {
-                    if (!(cut[c] < cut[c + 1])) continue;
-                    const int jc = static_cast<int>(static_cast<long long>(s.bh) - cut[c] / pos);
-                    const float* wb = a.ws + (static_cast<size_t>(c) * kMaxU + jc) * kWS;
-                    const float mc = __ldcg(wb + R), lc = __ldcg(wb + R + 1), ac = __ldcg(wb + lane);
-                    if (mc == -INFINITY) continue;
-                    const float Mn = fmaxf(M2, mc);
-                    const float fo = ex2(M2 - Mn), fc = ex2(mc - Mn);  // fo = 0 while M2 = -inf
-                    L2 = fmaf(lc, fc, L2 * fo);
-                    a2 = fmaf(ac, fc, a2 * fo);
-                    M2 = Mn;
-                }
-                if (lane == 0) a.counters[s.bh] = 0;  // self-resetting for the next step
-            }
-            // latent output -> X rows of the O-projection, K index h*R + lane:
-            // hi = bf16(v) in row b, lo = bf16(v - hi) in row MT*16 + b (~16
-            // mantissa bits of the fp32 latent reach the tensor cores)
-            const int b = s.bh / a.nh, h = s.bh - b * a.nh;
-            const int k = h * R + lane, sx = k / kKS;
-            const float vo = a2 / L2;
-            const __nv_bfloat16 vh = __float2bfloat16_rn(vo);
-            const __nv_bfloat16 vl = __float2bfloat16_rn(vo - __bfloat162float(vh));
-            uint8_t* xs = a.xo + static_cast<size_t>(sx) * C::XB2;
-            reinterpret_cast<__nv_bfloat16*>(xs + static_cast<size_t>(b) * kXS)[k - sx * kKS] = vh;
-            reinterpret_cast<__nv_bfloat16*>(xs + static_cast<size_t>(MT * 16 + b) * kXS)[k - sx * kKS] = vl;
-        }
-        STEP_MARK(6);
-    } else {
-        // ========================================================= consumer warps
-        if (ysplit) {
-            // y collects the two K splits' partial sums (P3): zero this CTA's
-            // share now -- after barrier 1, so a y that aliases x is not
-            // touched before x is consumed
-            const size_t ny = static_cast<size_t>(a.B) * a.e_out;
-            const size_t y0 = ny * cta / G, y1 = ny * (cta + 1) / G;
-            for (size_t i = y0 + tid; i < y1; i += 32 * kNW) a.y[i] = 0.f;
-        }
-        // ---- P2: attention over this CTA's segments, in processing order
-        int slot = 0;
-        uint32_t phase = 0;
-        constexpr int KR = R / 16;
-        for (int p = 0; p < nseg; ++p) {
-            const int j = seg_of(p);
-            const SegInfo& s = sinf[j];
-            const int ntok = s.t1 - s.t0;
-            const int ns = (ntok + kST - 1) / kST;
-            mbar_wait(&uready[j], 0u);
-            if (p == 0) {
-                STEP_MARK(13);
-                if (a.trace && lane == 0 && (warp == 0 || warp == kNW - 1)) a.trace[cta * kTr + (warp == 0 ? 17 : 18)] = gtimer();
-            }
-            uint32_t qf[KR][2];
-#pragma unroll
-            for (int kk = 0; kk < KR; ++kk)
-#pragma unroll
-                for (int jj = 0; jj < 2; ++jj) {
-                    const int k0 = kk * 16 + 2 * t4 + 8 * jj;
-                    uint32_t h0, l0, h1, l1;
-                    split_bf16(qts[j * R + k0], h0, l0);
-                    split_bf16(qts[j * R + k0 + 1], h1, l1);
-                    qf[kk][jj] = (g8 == 0) ? (h0 | (h1 << 16)) : (g8 == 1 ? (l0 | (l1 << 16)) : 0u);
-                }
-            float m_w = -INFINITY, l = 0.f;
-            float acc[KR][4];
-#pragma unroll
-            for (int kk = 0; kk < KR; ++kk)
-#pragma unroll
-                for (int i = 0; i < 4; ++i) acc[kk][i] = 0.f;
-
-            for (int st = 0; st < ns; ++st) {
-                mbar_wait(&fullB[slot], phase);
-                if (a.trace && p == 0 && st == 0 && warp == 0 && lane == 0) a.trace[cta * kTr + 19] = gtimer();
-                const uint32_t sbase = smem_u32(ringB + slot * C::STAGE);
-                const int rows = min(kST, ntok - st * kST);
-                if (warp * 32 < rows) {
-                    // scores D(16 tok x 8) = K(16 x R) . [qt_hi | qt_lo]: lane (g8, t4 = 0)
-                    // holds the hi / lo partials of tokens g8 and g8 + 8
-                    float sc[2][2];
-#pragma unroll
-                    for (int grp = 0; grp < 2; ++grp) {
-                        const int tb = warp * 32 + grp * 16;
-                        float d[4] = {0.f, 0.f, 0.f, 0.f};
-                        const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
-#pragma unroll
-                        for (int kk = 0; kk < KR; ++kk) {
-                            uint32_t a0, a1, a2, a3;
-                            const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
-                            ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
-                            mma_bf16_16816(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+                        for (int i = 0; i < 4; ++i) {
+                            const int n = tile * 16 + g8 + ((i & 2) ? 8 : 0);
+                            const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
+                            if (m < a.B) P[static_cast<size_t>(m) * a.Nrows + n] = facc[mt][hh][i];
                         }
-                        sc[grp][0] = (t4 == 0 && tb + g8 < rows) ? d[0] + d[1] : -INFINITY;
-                        sc[grp][1] = (t4 == 0 && tb + g8 + 8 < rows) ? d[2] + d[3] : -INFINITY;
+            }
+        }
+        // helper: the first segment's M_QK column does not depend on the
+        // projection; load it while the barrier drains
+        float mq0[R];
+        int nseg = 0, pos = 0;
+        if (warp == kHelp) {
+            nseg = meta[1];
+            pos = meta[0];
+            if (nseg > 0) {
+                const int h0 = sinf[rev ? nseg - 1 : 0].bh % a.nh;
+                const float* mq = Ly.mqk + static_cast<size_t>(h0) * R * R + lane;
+#pragma unroll
+                for (int jj = 0; jj < R; ++jj) mq0[jj] = __ldg(mq + jj * R);
+            }
+        }
+        named_bar_sync(1, kSync);
+        STEP_MARK(2);  // every projection warp of this CTA is done
+        grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // G1: every projection partial is written
+        if (tid == 0) mbar_arrive(b1bar);
+        STEP_MARK(3);
+        if (warp < kNW) {
+            mbar_wait(tready, lp);  // (built before G1: returns at once)
+            nseg = meta[1];
+            pos = meta[0];
+        }
+        auto seg_of = [&](int p) { return rev ? nseg - 1 - p : p; };
+        const size_t cap = static_cast<size_t>(Ly.cap);
+
+        if (warp == kHelp) {
+            // ============================================================ helper warp
+            // segment slots this layer does not use complete their phases anyway
+            // (every segment barrier turns over exactly once per layer)
+            if (lane == 0)
+                for (int j = nseg; j < kMaxU; ++j) {
+                    mbar_arrive(&uready[j]);
+                    mbar_arrive_n(&sfull[j], kNW);
+                }
+            // (a) per segment, in processing order, ahead of the consumers:
+            //     qt = (sum_split c_Q) . M_QK (the append epilogue's order: fixed
+            //     split order, sequential fma); the segment that ends a region also
+            //     gets the step's own K / V latents (summed the same way, rounded to
+            //     the cache's bf16 -- the row the reference appends before
+            //     attending, decode.cpp:143-149), written to cache row pos
+            auto prep = [&](int p, const float (&mqv)[R]) {
+                const int j = seg_of(p);
+                const SegInfo& s = sinf[j];
+                const int b = s.bh / a.nh, h = s.bh - b * a.nh;
+                const bool own = s.t1 == pos;
+                const float* pb = a.P + static_cast<size_t>(b) * a.Nrows + static_cast<size_t>(h) * 3 * R + lane;
+                float pv[3][kMaxSplits];
+#pragma unroll
+                for (int sp = 0; sp < kMaxSplits; ++sp) {
+                    pv[0][sp] = sp < splits ? __ldcg(pb + sp * pstride) : 0.f;
+                    pv[1][sp] = (own && sp < splits) ? __ldcg(pb + sp * pstride + R) : 0.f;
+                    pv[2][sp] = (own && sp < splits) ? __ldcg(pb + sp * pstride + 2 * R) : 0.f;
+                }
+                float v[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+                for (int sp = 0; sp < kMaxSplits; ++sp)
+#pragma unroll
+                    for (int r = 0; r < 3; ++r) v[r] += pv[r][sp];  // zeros past `splits` leave the sum exact
+                float qt = 0.f;
+#pragma unroll
+                for (int jj = 0; jj < R; ++jj) qt = fmaf(__shfl_sync(0xffffffffu, v[0], jj), mqv[jj], qt);
+                qts[j * R + lane] = qt;
+                if (own) {
+                    uint8_t* region = Ly.cache + static_cast<size_t>(s.bh) * cap * C::ROWB;
+                    const uint32_t grow = static_cast<uint32_t>(pos) * C::ROWB;
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        const __nv_bfloat16 bv = __float2bfloat16_rn(v[1 + half]);
+                        nrow[j * 2 * R + half * R + lane] = bv;
+                        *reinterpret_cast<__nv_bfloat16*>(region + cache_swz(grow + half * C::PART + 2 * lane)) = bv;
                     }
-                    const float wm = warp_max(fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])));
-                    if (wm > m_w) {
-                        const float f = ex2(m_w - wm);
-                        l *= f;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&uready[j]);
+            };
+            if (nseg > 0) prep(0, mq0);
+            if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 16] = gtimer();
+            for (int p = 1; p < nseg; ++p) {
+                const int h = sinf[seg_of(p)].bh % a.nh;
+                float mqv[R];
+                const float* mq = Ly.mqk + static_cast<size_t>(h) * R * R + lane;
 #pragma unroll
-                        for (int kk = 0; kk < KR; ++kk)
+                for (int jj = 0; jj < R; ++jj) mqv[jj] = __ldg(mq + jj * R);
+                prep(p, mqv);
+            }
+            if (nseg > 0) STEP_MARK(4);
+            // (b) per segment as the consumers finish it: merge the kNW warp states
+            //     in warp order (+ the own token for a region's last segment).  A
+            //     region held by one CTA is complete.  A region shared by the two
+            //     CTAs of a cluster pair: the odd CTA's (later) part crosses into the
+            //     even CTA through distributed shared memory and the even CTA
+            //     merges.  Any other shared region: every part publishes its state
+            //     to L2 and the last to arrive merges them all in range order
+            //     (SoftmaxState::merge, decode.cpp:59-75) -- nobody waits.
+            for (int p = 0; p < nseg; ++p) {
+                const int j = seg_of(p);
+                mbar_wait(&sfull[j], lp);
+                if (p == 0) STEP_MARK(15);
+                const SegInfo& s = sinf[j];
+                const float* rb = wst + j * kNW * (R + 2);
+                float M = -INFINITY;
 #pragma unroll
-                            for (int i = 0; i < 4; ++i) acc[kk][i] *= f;
-                        m_w = wm;
+                for (int w = 0; w < kNW; ++w) M = fmaxf(M, rb[w * (R + 2) + R]);
+                float Ls = 0.f, av = 0.f;
+#pragma unroll
+                for (int w = 0; w < kNW; ++w) {
+                    const float mw = rb[w * (R + 2) + R];
+                    if (mw == -INFINITY) continue;
+                    const float f = ex2(mw - M);
+                    Ls = fmaf(rb[w * (R + 2) + R + 1], f, Ls);
+                    av = fmaf(rb[w * (R + 2) + lane], f, av);
+                }
+                if (s.t1 == pos) {
+                    // SoftmaxState::observe of the own token (decode.cpp:35-57)
+                    const float kf = __bfloat162float(nrow[j * 2 * R + lane]);
+                    const float vf = __bfloat162float(nrow[j * 2 * R + R + lane]);
+                    const float sn = warp_sum(qts[j * R + lane] * kf);
+                    const float Mn = fmaxf(M, sn);
+                    const float fo = ex2(M - Mn), fn = ex2(sn - Mn);  // fo = 0 when M = -inf
+                    Ls = fmaf(Ls, fo, fn);
+                    av = fmaf(av, fo, vf * fn);
+                    M = Mn;
+                }
+                const int c0 = s.c0, c1 = s.c1, owners = s.owners;
+                const bool pair = a.cluster == 2 && owners == 2 && c1 - c0 == 2 && (c0 & 1) == 0;
+                float L2 = Ls, a2 = av;
+                if (pair && cta == c0 + 1) {
+                    // the later part of the pair's shared region -> the even CTA
+                    const uint32_t dst = cluster_map(smem_u32(pst), 0u);
+                    st_cluster_f32(dst + 4u * lane, av);
+                    if (lane == 0) {
+                        st_cluster_f32(dst + 4u * R, M);
+                        st_cluster_f32(dst + 4u * (R + 1), Ls);
                     }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_remote(cluster_map(smem_u32(pbar), 0u));
+                    continue;
+                }
+                if (pair) {
+                    // this CTA holds the earlier part: it first, the partner's next
+                    mbar_wait_cluster(pbar, pcnt & 1u);
+                    ++pcnt;
+                    const float mc = pst[R], lc = pst[R + 1], ac = pst[lane];
+                    if (mc != -INFINITY) {
+                        const float Mn = fmaxf(M, mc);
+                        const float fo = ex2(M - Mn), fc = ex2(mc - Mn);
+                        L2 = fmaf(lc, fc, Ls * fo);
+                        a2 = fmaf(ac, fc, av * fo);
+                    }
+                } else if (owners > 1) {
+                    float* wsp = a.ws + (static_cast<size_t>(cta) * kMaxU + j) * kWS;
+                    wsp[lane] = av;
+                    if (lane == 0) {
+                        wsp[R] = M;
+                        wsp[R + 1] = Ls;
+                    }
+                    __syncwarp();
+                    unsigned old = 0;
+                    if (lane == 0) old = atom_add_acq_rel(reinterpret_cast<unsigned*>(Ly.counters) + s.bh);
+                    old = __shfl_sync(0xffffffffu, old, 0);
+                    if (old != static_cast<unsigned>(owners - 1)) continue;  // another part merges
+                    // ---- last arriver: every part of region bh in range order
+                    float M2 = -INFINITY;
+                    L2 = 0.f;
+                    a2 = 0.f;
+                    for (int c = c0; c < c1; ++c) {
+                        if (!(cut[c] < cut[c + 1])) continue;
+                        const int jc = static_cast<int>(static_cast<long long>(s.bh) - cut[c] / pos);
+                        const float* wb = a.ws + (static_cast<size_t>(c) * kMaxU + jc) * kWS;
+                        const float mc = __ldcg(wb + R), lc = __ldcg(wb + R + 1), ac = __ldcg(wb + lane);
+                        if (mc == -INFINITY) continue;
+                        const float Mn = fmaxf(M2, mc);
+                        const float fo = ex2(M2 - Mn), fc = ex2(mc - Mn);  // fo = 0 while M2 = -inf
+                        L2 = fmaf(lc, fc, L2 * fo);
+                        a2 = fmaf(ac, fc, a2 * fo);
+                        M2 = Mn;
+                    }
+                    if (lane == 0) Ly.counters[s.bh] = 0;  // self-resetting for the next step
+                }
+                // latent output -> X rows of the O-projection, K index h*R + lane:
+                // hi = bf16(v) in row b, lo = bf16(v - hi) in row MT*16 + b (~16
+                // mantissa bits of the fp32 latent reach the tensor cores)
+                const int b = s.bh / a.nh, h = s.bh - b * a.nh;
+                const int k = h * R + lane, sx = k / kKS, kk = k - sx * kKS;
+                const float vo = a2 / L2;
+                const __nv_bfloat16 vh = __float2bfloat16_rn(vo);
+                const __nv_bfloat16 vl = __float2bfloat16_rn(vo - __bfloat162float(vh));
+                uint8_t* xs = a.xo + static_cast<size_t>(sx) * C::XB2;
+                const uint32_t eb = static_cast<uint32_t>((kk & 7) * 2);
+                *reinterpret_cast<__nv_bfloat16*>(xs + xrow_off(b, kk >> 3) + eb) = vh;
+                *reinterpret_cast<__nv_bfloat16*>(xs + xrow_off(MT * 16 + b, kk >> 3) + eb) = vl;
+            }
+            STEP_MARK(6);
+        } else {
+            // ========================================================= consumer warps
+            if (g3.ysplit) {
+                // y collects the two K splits' partial sums (P3): zero this CTA's
+                // share now -- after barrier 1, so a y that aliases x is not
+                // touched before x is consumed
+                const size_t ny = static_cast<size_t>(a.B) * a.e_out;
+                const size_t y0 = ny * cta / G, y1 = ny * (cta + 1) / G;
+                for (size_t i = y0 + tid; i < y1; i += 32 * kNW) Ly.y[i] = 0.f;
+            }
+            // ---- P2: attention over this CTA's segments, in processing order
+            int slot = 0;
+            constexpr int KR = R / 16;
+            for (int p = 0; p < nseg; ++p) {
+                const int j = seg_of(p);
+                const SegInfo& s = sinf[j];
+                const int ntok = s.t1 - s.t0;
+                const int ns = (ntok + kST - 1) / kST;
+                mbar_wait(&uready[j], lp);
+                if (p == 0) {
+                    STEP_MARK(13);
+                    if (a.trace && l == a.trace_layer && lane == 0 && (warp == 0 || warp == kNW - 1))
+                        a.trace[cta * kTr + (warp == 0 ? 17 : 18)] = gtimer();
+                }
+                uint32_t qf[KR][2];
 #pragma unroll
-                    for (int grp = 0; grp < 2; ++grp) {
-                        const int tb = warp * 32 + grp * 16;
-                        const float p0 = (sc[grp][0] == -INFINITY) ? 0.f : ex2(sc[grp][0] - m_w);
-                        const float p1 = (sc[grp][1] == -INFINITY) ? 0.f : ex2(sc[grp][1] - m_w);
-                        l += p0 + p1;
+                for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                    for (int jj = 0; jj < 2; ++jj) {
+                        const int k0 = kk * 16 + 2 * t4 + 8 * jj;
                         uint32_t h0, l0, h1, l1;
-                        split_bf16(p0, h0, l0);
-                        split_bf16(p1, h1, l1);
-                        const uint32_t hi2 = h0 | (h1 << 16), lo2 = l0 | (l1 << 16);
-                        const int s0 = 8 * t4, s1 = 8 * t4 + 4;
-                        const uint32_t xh = __shfl_sync(0xffffffffu, hi2, s0), yh = __shfl_sync(0xffffffffu, hi2, s1);
-                        const uint32_t xl = __shfl_sync(0xffffffffu, lo2, s0), yl = __shfl_sync(0xffffffffu, lo2, s1);
-                        const uint32_t xx = (g8 == 0) ? xh : xl, yy = (g8 == 0) ? yh : yl;
-                        const uint32_t b0 = (g8 < 2) ? __byte_perm(xx, yy, 0x5410) : 0u;
-                        const uint32_t b1 = (g8 < 2) ? __byte_perm(xx, yy, 0x7632) : 0u;
-                        const int stok = tb + (lane & 7) + ((lane >> 4) & 1) * 8;
+                        split_bf16(qts[j * R + k0], h0, l0);
+                        split_bf16(qts[j * R + k0 + 1], h1, l1);
+                        qf[kk][jj] = (g8 == 0) ? (h0 | (h1 << 16)) : (g8 == 1 ? (l0 | (l1 << 16)) : 0u);
+                    }
+                float m_w = -INFINITY, lsm = 0.f;
+                float acc[KR][4];
 #pragma unroll
-                        for (int mm = 0; mm < KR; ++mm) {
-                            uint32_t a0, a1, a2, a3;
-                            const uint32_t off = static_cast<uint32_t>(stok * C::ROWB + C::PART + (mm * 2 + ((lane >> 3) & 1)) * 16);
-                            ldsm_x4_trans(sbase + cache_swz(off), a0, a1, a2, a3);
-                            mma_bf16_16816(acc[mm], a0, a1, a2, a3, b0, b1);
+                for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) acc[kk][i] = 0.f;
+
+                for (int st = 0; st < ns; ++st) {
+                    mbar_wait(&fullB[slot], (parc >> slot) & 1u);
+                    parc ^= 1u << slot;
+                    if (a.trace && l == a.trace_layer && p == 0 && st == 0 && warp == 0 && lane == 0)
+                        a.trace[cta * kTr + 19] = gtimer();
+                    const uint32_t sbase = smem_u32(ringB + slot * C::STAGE);
+                    const int rows = min(kST, ntok - st * kST);
+                    if (warp * 32 < rows) {
+                        // scores D(16 tok x 8) = K(16 x R) . [qt_hi | qt_lo]: lane (g8, t4 = 0)
+                        // holds the hi / lo partials of tokens g8 and g8 + 8
+                        float sc[2][2];
+#pragma unroll
+                        for (int grp = 0; grp < 2; ++grp) {
+                            const int tb = warp * 32 + grp * 16;
+                            float d[4] = {0.f, 0.f, 0.f, 0.f};
+                            const int ltok = tb + (lane & 7) + ((lane >> 3) & 1) * 8;
+#pragma unroll
+                            for (int kk = 0; kk < KR; ++kk) {
+                                uint32_t a0, a1, a2, a3;
+                                const uint32_t off = static_cast<uint32_t>(ltok * C::ROWB + (kk * 2 + (lane >> 4)) * 16);
+                                ldsm_x4(sbase + cache_swz(off), a0, a1, a2, a3);
+                                mma_bf16_16816(d, a0, a1, a2, a3, qf[kk][0], qf[kk][1]);
+                            }
+                            sc[grp][0] = (t4 == 0 && tb + g8 < rows) ? d[0] + d[1] : -INFINITY;
+                            sc[grp][1] = (t4 == 0 && tb + g8 + 8 < rows) ? d[2] + d[3] : -INFINITY;
+                        }
+                        const float wm = warp_max(fmaxf(fmaxf(sc[0][0], sc[0][1]), fmaxf(sc[1][0], sc[1][1])));
+                        if (wm > m_w) {
+                            const float f = ex2(m_w - wm);
+                            lsm *= f;
+#pragma unroll
+                            for (int kk = 0; kk < KR; ++kk)
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) acc[kk][i] *= f;
+                            m_w = wm;
+                        }
+#pragma unroll
+                        for (int grp = 0; grp < 2; ++grp) {
+                            const int tb = warp * 32 + grp * 16;
+                            const float p0 = (sc[grp][0] == -INFINITY) ? 0.f : ex2(sc[grp][0] - m_w);
+                            const float p1 = (sc[grp][1] == -INFINITY) ? 0.f : ex2(sc[grp][1] - m_w);
+                            lsm += p0 + p1;
+                            uint32_t h0, l0, h1, l1;
+                            split_bf16(p0, h0, l0);
+                            split_bf16(p1, h1, l1);
+                            const uint32_t hi2 = h0 | (h1 << 16), lo2 = l0 | (l1 << 16);
+                            const int s0 = 8 * t4, s1 = 8 * t4 + 4;
+                            const uint32_t xh = __shfl_sync(0xffffffffu, hi2, s0), yh = __shfl_sync(0xffffffffu, hi2, s1);
+                            const uint32_t xl = __shfl_sync(0xffffffffu, lo2, s0), yl = __shfl_sync(0xffffffffu, lo2, s1);
+                            const uint32_t xx = (g8 == 0) ? xh : xl, yy = (g8 == 0) ? yh : yl;
+                            const uint32_t b0 = (g8 < 2) ? __byte_perm(xx, yy, 0x5410) : 0u;
+                            const uint32_t b1 = (g8 < 2) ? __byte_perm(xx, yy, 0x7632) : 0u;
+                            const int stok = tb + (lane & 7) + ((lane >> 4) & 1) * 8;
+#pragma unroll
+                            for (int mm = 0; mm < KR; ++mm) {
+                                uint32_t a0, a1, a2, a3;
+                                const uint32_t off = static_cast<uint32_t>(stok * C::ROWB + C::PART + (mm * 2 + ((lane >> 3) & 1)) * 16);
+                                ldsm_x4_trans(sbase + cache_swz(off), a0, a1, a2, a3);
+                                mma_bf16_16816(acc[mm], a0, a1, a2, a3, b0, b1);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&emptyB[slot]);
+                    if (++slot == C::NB) slot = 0;
+                }
+                // this warp's state of segment j -> the helper
+                float* wr = wst + (j * kNW + warp) * (R + 2);
+                const float lsum = warp_sum(lsm);
+                if (t4 == 0) {
+#pragma unroll
+                    for (int mm = 0; mm < KR; ++mm) {
+                        wr[mm * 16 + g8] = acc[mm][0] + acc[mm][1];
+                        wr[mm * 16 + g8 + 8] = acc[mm][2] + acc[mm][3];
+                    }
+                }
+                if (lane == 0) {
+                    wr[R] = m_w;
+                    wr[R + 1] = lsum;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sfull[j]);
+            }
+            STEP_MARK(5);
+        }
+        // G2: every (sequence, head) row is merged; every CTA has read the length
+        grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));
+        STEP_MARK(7);
+        if (cta == 0 && tid == 0) *Ly.d_len = pos + 1;
+
+        if (warp == kHelp) {
+            // the next layer's table while P3 runs (this layer's readers are done)
+            if (l + 1 < nL) build_table(l + 1);
+        } else {
+            // ---- P3: folded O-projection over the prefetched W'_o items.  The X
+            // slices this CTA's items use (hi / lo bf16 rows built by the mergers)
+            // land at the end of the attention ring -- all at once, or one K
+            // split at a time when they do not fit together.  Item j = (tile j /
+            // p3ns, split p3s0 + j % p3ns) runs on warps slot and slot + 4, one
+            // half of its K range each, into part[half][j]; the halves and the
+            // splits are summed in a fixed order.
+            const P3G& g = g3;
+            float* part = C::PART_IN_RED ? reinterpret_cast<float*>(smem + C::RED_OFF)
+                                         : reinterpret_cast<float*>(ringB + g.p3lo);  // [2][kNA][16 rows][MT*16 tokens]
+            uint8_t* xsl = ringB + g.xoff;
+            const int half = warp / kNA, hslot = warp % kNA;
+            const unsigned a3 = abase + static_cast<unsigned>(nA1);  // ring-A index of P3 item 0
+            if (g.np3 > 0) {
+                for (int s0 = 0; s0 < g.p3ns; s0 += g.per) {
+                    if (a.p3_tma) {
+                        if (tid == 0) {
+                            // xo was written by other CTAs' generic stores (ordered by the
+                            // barrier); order them before this thread's async-proxy reads
+                            asm volatile("fence.proxy.async.global;" ::: "memory");
+                            mbar_arrive_expect_tx(p3bar, static_cast<uint32_t>(g.per * C::XB2));
+                            for (int s = s0; s < s0 + g.per; ++s)
+                                tma_bulk_g2s(xsl + (s - s0) * C::XB2, a.xo + static_cast<size_t>(g.p3s0 + s) * C::XB2,
+                                             C::XB2, p3bar);
+                        }
+                        mbar_wait(p3bar, p3cnt & 1u);
+                        ++p3cnt;
+                    } else {
+                        // plain 16-byte loads by every consumer thread, all in flight at once
+                        constexpr int V = C::XB2 / 16;  // uint4 per split
+                        constexpr int NV = (V + 32 * kNW - 1) / (32 * kNW);
+                        for (int s = s0; s < s0 + g.per; ++s) {
+                            const uint4* src = reinterpret_cast<const uint4*>(a.xo + static_cast<size_t>(g.p3s0 + s) * C::XB2);
+                            uint4* dst = reinterpret_cast<uint4*>(xsl + (s - s0) * C::XB2);
+                            uint4 v[NV];
+#pragma unroll
+                            for (int u = 0; u < NV; ++u) {
+                                const int i = tid + u * 32 * kNW;
+                                if (i < V) v[u] = __ldcg(src + i);
+                            }
+#pragma unroll
+                            for (int u = 0; u < NV; ++u) {
+                                const int i = tid + u * 32 * kNW;
+                                if (i < V) dst[i] = v[u];
+                            }
+                        }
+                        named_bar_sync(2, 32 * kNW);
+                    }
+                    if (s0 == 0) STEP_MARK(8);
+                    for (int j = 0; j < g.np3; ++j) {
+                        const unsigned ia = a3 + static_cast<unsigned>(j);
+                        const int slot = static_cast<int>(ia % kNA), s = j % g.p3ns;
+                        if (slot != hslot || s < s0 || s >= s0 + g.per) continue;
+                        mbar_wait(&fullA[slot], (ia / kNA) & 1u);
+                        // token columns 0..MT*16-1 are the hi rows, MT*16.. the lo rows
+                        float facc[2 * MT][2][4];
+                        item_mma<2 * MT>(smem_u32(ringA + slot * kItem), smem_u32(xsl + (s - s0) * C::XB2), lane, facc,
+                                         half * kKS / 64, (half + 1) * kKS / 64);
+                        float* pj3 = part + (half * kNA + j) * 16 * MT * 16;
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                            for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const int n = g8 + ((i & 2) ? 8 : 0);
+                                    const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
+                                    pj3[n * MT * 16 + m] = facc[mt][hh][i] + facc[mt + MT][hh][i];
+                                }
+                    }
+                    named_bar_sync(2, 32 * kNW);  // the X buffer is free again / every partial is written
+                }
+                // the weight ring's P3 slots are free (both halves have run)
+                if (tid < g.np3) mbar_arrive(&emptyA[(a3 + static_cast<unsigned>(tid)) % kNA]);
+                STEP_MARK(12);
+                // part[(half * kNA + j)] -> sum over halves, then splits
+                auto psum = [&](int ti, int n, int m) {
+                    float v = 0.f;
+                    for (int s = 0; s < g.p3ns; ++s) {
+                        const int j = ti * g.p3ns + s;
+                        v += part[(j * 16 + n) * MT * 16 + m] + part[((kNA + j) * 16 + n) * MT * 16 + m];
+                    }
+                    return v;
+                };
+                if (!g.ycontig) {
+                    for (int i = tid; i < g.nt3 * 16 * a.B; i += 32 * kNW) {
+                        const int ti = i / (16 * a.B), r = i - ti * 16 * a.B;
+                        const int m = r / 16, n = r - m * 16;  // n fastest: 64-byte row segments of y
+                        const int col = (g.t3lo + ti * g.t3step) * 16 + n;
+                        if (col >= a.e_out) continue;
+                        float* yp = Ly.y + static_cast<size_t>(m) * a.e_out + col;
+                        if (g.ysplit) atomicAdd(yp, psum(ti, n, m));  // red.add: one of exactly two addends onto 0
+                        else *yp = psum(ti, n, m);
+                    }
+                } else {
+                    const int q4 = g.nt3 * 4;  // 4-column groups of this CTA's row segment
+                    for (int i = tid; i < a.B * q4; i += 32 * kNW) {
+                        const int m = i / q4, q = i - m * q4;
+                        const int ti = q >> 2, n0 = (q & 3) * 4;
+                        const int col = (g.t3lo + ti) * 16 + n0;
+                        float v[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) v[e] = psum(ti, n0 + e, m);
+                        float* yr = Ly.y + static_cast<size_t>(m) * a.e_out;
+                        if (col + 4 <= a.e_out && (a.e_out & 3) == 0) {
+                            *reinterpret_cast<float4*>(yr + col) = make_float4(v[0], v[1], v[2], v[3]);
+                        } else {
+                            for (int e = 0; e < 4; ++e)
+                                if (col + e < a.e_out) yr[col + e] = v[e];
                         }
                     }
                 }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&emptyB[slot]);
-                if (++slot == C::NB) {
-                    slot = 0;
-                    phase ^= 1u;
-                }
             }
-            // this warp's state of segment j -> the helper
-            float* wr = wst + (j * kNW + warp) * (R + 2);
-            const float lsum = warp_sum(l);
-            if (t4 == 0) {
-#pragma unroll
-                for (int mm = 0; mm < KR; ++mm) {
-                    wr[mm * 16 + g8] = acc[mm][0] + acc[mm][1];
-                    wr[mm * 16 + g8 + 8] = acc[mm][2] + acc[mm][3];
-                }
-            }
-            if (lane == 0) {
-                wr[R] = m_w;
-                wr[R + 1] = lsum;
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sfull[j]);
-        }
-        STEP_MARK(5);
-    }
-    grid_sync(a.bar, (2u * epoch + 2u) * G);  // every (sequence, head) row is merged; every CTA read the length
-    STEP_MARK(7);
-    if (cta == 0 && tid == 0) {
-        *a.d_len = len;
-        *a.epoch += 1;  // fused steps run (the barrier generations)
-    }
-
-    // ---- P3: folded O-projection over the prefetched W'_o items
-    if (np3 == 0 || warp >= kNW) {
-        STEP_MARK(8);
-        STEP_MARK(9);
-        return;
-    }
-    // The X slices this CTA's items use (hi / lo bf16 rows built by the
-    // mergers) arrive by TMA -- all at once, or one K split at a time when
-    // they do not fit the attention ring together (two token tiles).  Item j
-    // = (tile j / p3ns, split p3s0 + j % p3ns) runs on warps slot and slot + 4,
-    // one half of its K range each, into part[half][j]; the halves and the
-    // splits are summed in a fixed order.
-    const int ring_bytes = C::NB * C::STAGE;
-    const int partb = 2 * kNA * 16 * MT * 16 * 4;
-    const int per = (p3ns * C::XB2 + partb <= ring_bytes) ? p3ns : 1;  // splits staged together
-    float* part = reinterpret_cast<float*>(ringB + per * C::XB2);  // [2][np3][16 rows][MT*16 tokens]
-    const int half = warp / kNA, hslot = warp % kNA;
-    for (int s0 = 0; s0 < p3ns; s0 += per) {
-        if (a.p3_tma) {
-            if (tid == 0) {
-                // xo was written by other CTAs' generic stores (ordered by the
-                // barrier); order them before this thread's async-proxy reads
-                asm volatile("fence.proxy.async.global;" ::: "memory");
-                mbar_arrive_expect_tx(p3bar, static_cast<uint32_t>(per * C::XB2));
-                for (int s = s0; s < s0 + per; ++s)
-                    tma_bulk_g2s(ringB + (s - s0) * C::XB2, a.xo + static_cast<size_t>(p3s0 + s) * C::XB2, C::XB2,
-                                 p3bar);
-            }
-            mbar_wait(p3bar, static_cast<uint32_t>(s0 / per) & 1u);
-        } else {
-            // plain 16-byte loads by every consumer thread, all in flight at once
-            constexpr int V = C::XB2 / 16;  // uint4 per split
-            constexpr int NV = (V + 32 * kNW - 1) / (32 * kNW);
-            for (int s = s0; s < s0 + per; ++s) {
-                const uint4* src = reinterpret_cast<const uint4*>(a.xo + static_cast<size_t>(p3s0 + s) * C::XB2);
-                uint4* dst = reinterpret_cast<uint4*>(ringB + (s - s0) * C::XB2);
-                uint4 v[NV];
-#pragma unroll
-                for (int u = 0; u < NV; ++u) {
-                    const int i = tid + u * 32 * kNW;
-                    if (i < V) v[u] = __ldcg(src + i);
-                }
-#pragma unroll
-                for (int u = 0; u < NV; ++u) {
-                    const int i = tid + u * 32 * kNW;
-                    if (i < V) dst[i] = v[u];
-                }
-            }
+            STEP_MARK(9);
+            // the attention ring and the merge area are free for the next layer's
+            // parked items (their generic writes ordered before those TMA writes)
+            fence_proxy_async_smem();
             named_bar_sync(2, 32 * kNW);
+            if (tid == 0) mbar_arrive(p3done);
         }
-        if (s0 == 0) STEP_MARK(8);
-        for (int j = 0; j < np3; ++j) {
-            const int k = nA1 + j, slot = k % kNA, s = j % p3ns;
-            if (slot != hslot || s < s0 || s >= s0 + per) continue;
-            mbar_wait(&fullA[slot], static_cast<uint32_t>(k / kNA) & 1u);
-            // token columns 0..MT*16-1 are the hi rows, MT*16.. the lo rows
-            float facc[2 * MT][2][4];
-            item_mma<2 * MT>(smem_u32(ringA + slot * kItem), smem_u32(ringB + (s - s0) * C::XB2), lane, facc,
-                             half * kKS / 64, (half + 1) * kKS / 64);
-            float* pj3 = part + (half * kNA + j) * 16 * MT * 16;
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                for (int hh = 0; hh < 2; ++hh)
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const int n = g8 + ((i & 2) ? 8 : 0);
-                        const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
-                        pj3[n * MT * 16 + m] = facc[mt][hh][i] + facc[mt + MT][hh][i];
-                    }
-        }
-        named_bar_sync(2, 32 * kNW);  // the X buffer is free again / every partial is written
+        abase += static_cast<unsigned>(nA1 + g3.np3);
+        if (l + 1 < nL) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // G3: y is the next layer's token
     }
-    STEP_MARK(12);
-    // part[(half * kNA + j)] -> sum over halves, then splits
-    auto psum = [&](int ti, int n, int m) {
-        float v = 0.f;
-        for (int s = 0; s < p3ns; ++s) {
-            const int j = ti * p3ns + s;
-            v += part[(j * 16 + n) * MT * 16 + m] + part[((kNA + j) * 16 + n) * MT * 16 + m];
-        }
-        return v;
-    };
-    if (!ycontig) {
-        for (int i = tid; i < nt3 * 16 * a.B; i += 32 * kNW) {
-            const int ti = i / (16 * a.B), r = i - ti * 16 * a.B;
-            const int m = r / 16, n = r - m * 16;  // n fastest: 64-byte row segments of y
-            const int col = (t3lo + ti * t3step) * 16 + n;
-            if (col >= a.e_out) continue;
-            float* yp = a.y + static_cast<size_t>(m) * a.e_out + col;
-            if (ysplit) atomicAdd(yp, psum(ti, n, m));  // red.add: one of exactly two addends onto 0
-            else *yp = psum(ti, n, m);
-        }
-        STEP_MARK(9);
-        return;
+    if (cta == 0 && tid == 0) {
+        *a.epoch += 1;  // fused launches run (the x-fetch generations)
+        *a.bgen = gen;  // this launch's barriers are all passed (every CTA read bgen before its first)
     }
-    const int q4 = nt3 * 4;  // 4-column groups of this CTA's row segment
-    for (int i = tid; i < a.B * q4; i += 32 * kNW) {
-        const int m = i / q4, q = i - m * q4;
-        const int ti = q >> 2, n0 = (q & 3) * 4;
-        const int col = (t3lo + ti) * 16 + n0;
-        float v[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) v[e] = psum(ti, n0 + e, m);
-        float* yr = a.y + static_cast<size_t>(m) * a.e_out;
-        if (col + 4 <= a.e_out && (a.e_out & 3) == 0) {
-            *reinterpret_cast<float4*>(yr + col) = make_float4(v[0], v[1], v[2], v[3]);
-        } else {
-            for (int e = 0; e < 4; ++e)
-                if (col + e < a.e_out) yr[col + e] = v[e];
-        }
-    }
-    STEP_MARK(9);
 }
 
 template <int MT>

@@ -193,3 +193,46 @@ class DecodeLayer:
         N.call("wsvd_cache_read_raw", self.h, seq, head, C.c_void_p(rows.ctypes.data),
                C.c_void_p(scales.ctypes.data))
         return rows, scales
+
+
+class DecodeChain:
+    """The attention blocks of a decode stack chained on one GPU:
+    pipe::decode_factored's layer loop (pipeline.cpp:318-336) with layer
+    l + 1's token = layer l's output (no FFN between them).  ``step`` runs the
+    whole chain as ONE persistent kernel when every layer takes the fused step
+    (wsvd_chain_step); every layer appends to its own cache."""
+
+    def __init__(self, layers):
+        self.layers = list(layers)
+        if not self.layers:
+            raise ConfigError("a chain needs at least one layer")
+        self._hs = (C.c_void_p * len(self.layers))(*[lay.h.value for lay in self.layers])
+        l0 = self.layers[0]
+        self.batch, self.embed_dim = l0.batch, l0.embed_dim
+
+    def __len__(self):
+        return len(self.layers)
+
+    def fused(self) -> bool:
+        return len(self.layers) <= 32 and all(lay._step_info()[0] for lay in self.layers)
+
+    def launches_per_step(self) -> int:
+        return 1 if self.fused() else sum(lay.launches_per_step() for lay in self.layers)
+
+    def step(self, x, ys, stream=None):
+        """x [batch][E] fp32 device tensor; ys: one [batch][E] fp32 device
+        tensor per layer (layer l's output; the last is the chain's)."""
+        if len(ys) != len(self.layers):
+            raise ShapeError(f"{len(self.layers)} layers need {len(self.layers)} outputs, got {len(ys)}")
+        yp = (C.c_void_p * len(ys))(*[t.data_ptr() for t in ys])
+        N.call("wsvd_chain_step", self._hs, len(self.layers), DecodeLayer._ptr(x), yp,
+               DecodeLayer._stream(stream))
+
+    def step_host(self, x_host, y_host, stream=None):
+        """Same through host buffers: x_host in, the last layer's y out."""
+        def hp(t):
+            if isinstance(t, np.ndarray):
+                return C.c_void_p(t.ctypes.data)
+            return C.c_void_p(t.data_ptr())
+        N.call("wsvd_chain_step_host", self._hs, len(self.layers), hp(x_host), hp(y_host),
+               DecodeLayer._stream(stream))

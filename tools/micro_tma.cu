@@ -106,7 +106,7 @@ int main() {
                 if (smem > 220 * 1024) continue;
                 auto k = stream_kernel<8>;
                 cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                for (int g : {sms, 2 * sms}) {
+                for (int g : {sms / 2, sms, 2 * sms}) {
                     if (g == 2 * sms && smem > 110 * 1024) continue;
                     double gbs = timeit([&] { k<<<g, 288, smem>>>(buf, total, sb, st, mode, sink); });
                     cudaError_t err = cudaGetLastError();

@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--attn-only", action="store_true")
     ap.add_argument("--proj-only", action="store_true")
     ap.add_argument("--host", action="store_true", help="steps through wsvd_layer_step_host (pinned x / y)")
+    ap.add_argument("--chain", type=int, default=0,
+                    help="run N chained layers as one launch (wsvd_chain_step); the marks are those of the layer "
+                         "WSVD_STEP_TRACE_LAYER (default the last); 'entry' = that layer's start")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     E, B, L = cfg["E"], cfg["B"], cfg["L"]
@@ -46,8 +49,25 @@ def main():
     x = torch.randn((B, E), generator=g, device=dev)
     y = torch.empty((B, E), device=dev)
     xh, yh = x.cpu().pin_memory(), torch.empty((B, E)).pin_memory()
+    chain = None
+    if args.chain > 1:
+        from paper_2604_02570_b200.layer import DecodeChain
+        more = []
+        for li in range(1, args.chain):
+            f2, w2 = bench.synthetic_layer(cfg, seed=li)
+            lay2 = DecodeLayer(f2, w2, batch=B, capacity=L + 64, cache_dtype=cfg["cache"],
+                               weight_dtype=cfg["weights"])
+            lay2.fill_synthetic(L - 1 - args.steps, seed=li)
+            more.append(lay2)
+        chain = DecodeChain([layer] + more)
+        ys = [torch.empty((B, E), device=dev) for _ in range(args.chain)]
     for _ in range(args.steps):
-        if args.host:
+        if chain is not None:
+            if args.host:
+                chain.step_host(xh.numpy(), yh.numpy())
+            else:
+                chain.step(x, ys)
+        elif args.host:
             layer.step_host(xh.numpy(), yh.numpy())
         else:
             layer.step(x, y, graph=False)
