@@ -12,7 +12,7 @@ import os
 
 from .errors import ConfigError, CudaError, IoError, NumericError, ShapeError, WsvdError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwsvd_b200.so")
+LIB_PATH = os.environ.get("WSVD_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libwsvd_b200.so")
 
 F32, BF16, I8, I4 = 0, 1, 2, 3
 DTYPES = {"f32": F32, "bf16": BF16, "i8": I8, "i4": I4}

@@ -19,8 +19,11 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libwsvd_b200.so")
+# WSVD_BUILD_TAG=x builds a variant (e.g. with WSVD_EXTRA_NVCC=-DWSVD_PIPE_DEBUG)
+# into _build_x / libwsvd_b200_x.so; load it with WSVD_LIB=<that path>
+_TAG = os.environ.get("WSVD_BUILD_TAG", "")
+OBJ = os.path.join(PKG, "_build" + (f"_{_TAG}" if _TAG else ""))
+LIB = os.path.join(PKG, "libwsvd_b200" + (f"_{_TAG}" if _TAG else "") + ".so")
 
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -30,7 +33,7 @@ CUDA_FLAGS += os.environ.get("WSVD_EXTRA_NVCC", "").split()  # experiment switch
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall", "-Wextra", f"-I{os.path.join(ROOT, 'include')}",
              "-I/usr/local/cuda/include"]
 
-CU_SOURCES = ["attn.cu", "attn_tc.cu", "gemm.cu", "append.cu", "step.cu", "dense.cu", "capi.cu"]
+CU_SOURCES = ["attn.cu", "attn_tc.cu", "gemm.cu", "append.cu", "step.cu", "step2.cu", "dense.cu", "capi.cu"]
 # host_decode.cpp (the C++ wsvd::decode drop-in) is NOT part of the library: it
 # is compiled inside the reference build against the reference's own
 # matrix / errors / factorize headers (oracle/Makefile target dropin)

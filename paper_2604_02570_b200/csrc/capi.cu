@@ -242,6 +242,7 @@ struct wsvd_cache_s {
     DevBuf trace;                     // fused-step phase timeline (WSVD_STEP_TRACE)
     DevBuf xo;                        // fused step: bf16 X rows of the O-projection
     DevBuf fws;                       // fused step: per-CTA segment states
+    DevBuf pP, pxo, pws;              // two-group chain (step2.cu): partials, O-proj rows, segment states
     DevBuf dbg;                       // test hook: int8 score accumulators [B*nh][cap_alloc][2]
     bool dbg_on = false;
     int attn_mode = 0;                // WSVD_ATTN_ABSORBED or WSVD_ATTN_EXPLICIT_TC
@@ -645,6 +646,8 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     a.x_first = x_first ? 1 : 0;
     static const int l2n = getenv("WSVD_STEP_L2NEXT") ? atoi(getenv("WSVD_STEP_L2NEXT")) : 1;  // A/B switch
     a.l2_next = l2n;
+    static const int cpre = getenv("WSVD_CHAIN_PRE") ? atoi(getenv("WSVD_CHAIN_PRE")) : 0;  // A/B switch
+    a.chain_pre = cpre;
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
     static const int trace_layer = getenv("WSVD_STEP_TRACE_LAYER") ? atoi(getenv("WSVD_STEP_TRACE_LAYER")) : -1;
     if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 24 * 8));
@@ -655,6 +658,95 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     CUDA_TRY(launch_layer_step(a, s));
     c->P_M = c->B;
     c->P_splits = splits;
+    return WSVD_OK;
+}
+
+// The chain as two batch groups half a layer apart (step2.cu); workspaces and
+// control words (ctrl[6..9]: per group barrier count and generations) are the
+// first cache's.
+bool chain_pipe_ok(wsvd_cache_s* const* cs, int n) {
+    // opt-in (WSVD_CHAIN_PIPE=1): measured slower than the one-group chain on
+    // B200 -- the hidden phases run at loaded latencies
+    static const bool on = getenv("WSVD_CHAIN_PIPE") && std::string(getenv("WSVD_CHAIN_PIPE")) == "1";
+    if (!on || n < 1 || n > kStepMaxLayers) return false;
+    const wsvd_cache_s* c = cs[0];
+    const wsvd_layer_s* L = c->L;
+    if (!pipe_supported(L->R, c->B, L->d.n_heads, L->Kp, L->oKp, round_up(L->e_out, 16) / 16, c->sms)) return false;
+    static int occ = -1;
+    if (occ < 0) occ = pipe_resident_ctas_per_sm();
+    return occ >= 1;
+}
+
+int run_chain_pipe(wsvd_cache_s* const* cs, int n, const float* x, float* const* ys, cudaStream_t s) {
+    wsvd_cache_s* c = cs[0];
+    wsvd_layer_s* L = c->L;
+    PipeArgs a{};
+    for (int l = 0; l < n; ++l) {
+        int rc = ensure_mqk(cs[l]->L);
+        if (rc) return rc;
+        StepLayer& Ly = a.layer[l];
+        Ly.A = cs[l]->L->A.as<uint8_t>();
+        Ly.mqk = cs[l]->L->mqk.as<float>();
+        Ly.cache = cs[l]->data.as<uint8_t>();
+        Ly.counters = cs[l]->attn_cnt.as<int>();
+        Ly.Wo = cs[l]->L->Wo.as<uint8_t>();
+        Ly.d_len = cs[l]->d_len();
+        Ly.y = ys[l];
+        Ly.cap = cs[l]->cap_alloc;
+    }
+    a.nlayers = n;
+    a.x = x;
+    const size_t pb = pipe_p_bytes(L->Kp, L->Nrows), xb = pipe_xo_bytes(L->oKp), wb = pipe_ws_bytes(c->sms);
+    if (c->pP.n < 2 * pb) CUDA_TRY(c->pP.alloc(2 * pb));
+    if (c->pxo.n < 2 * xb) CUDA_TRY(c->pxo.alloc(2 * xb));  // zeroed: rows past a group's batch stay 0
+    if (c->pws.n < 2 * wb) CUDA_TRY(c->pws.alloc(2 * wb));
+    for (int g = 0; g < 2; ++g) {
+        a.bar[g] = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 6 + 2 * g);
+        a.bgen[g] = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 7 + 2 * g);
+        a.P[g] = reinterpret_cast<float*>(c->pP.as<uint8_t>() + g * pb);
+        a.xo[g] = c->pxo.as<uint8_t>() + g * xb;
+        a.ws[g] = reinterpret_cast<float*>(c->pws.as<uint8_t>() + g * wb);
+    }
+    a.B = c->B;
+    a.nh = L->d.n_heads;
+    a.E = L->d.embed_dim;
+    a.Kp = L->Kp;
+    a.Nrows = L->Nrows;
+    a.e_out = L->e_out;
+    a.oKp = L->oKp;
+    a.otiles = round_up(L->e_out, 16) / 16;
+    a.grid = c->sms;
+    static const bool no_cluster = getenv("WSVD_STEP_NOCLUSTER") != nullptr;
+    static int pair = -1;
+    if (pair < 0) pair = pipe_pair_clusters_ok(c->sms);
+    a.cluster = (!no_cluster && pair == 1) ? 2 : 1;
+    static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;
+    static const int trace_layer = getenv("WSVD_STEP_TRACE_LAYER") ? atoi(getenv("WSVD_STEP_TRACE_LAYER")) : -1;
+    static const int trace_group = getenv("WSVD_STEP_TRACE_GROUP") ? atoi(getenv("WSVD_STEP_TRACE_GROUP")) : 0;
+    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 24 * 8));
+    a.trace = trace ? c->trace.as<uint64_t>() : nullptr;
+    a.trace_layer = trace_layer >= 0 && trace_layer < n ? trace_layer : n - 1;
+    a.trace_group = trace_group & 1;
+    int rc = fused_serialize(L->d.device, s);
+    if (rc) return rc;
+    static int* dbg_host = nullptr;
+    static int* dbg_dev = nullptr;
+    if (!dbg_host && getenv("WSVD_PIPE_DEBUG")) {
+        CUDA_TRY(cudaHostAlloc(reinterpret_cast<void**>(&dbg_host), 4 * 4096, cudaHostAllocMapped));
+        std::memset(dbg_host, 0, 4 * 4096);
+        CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dbg_dev), dbg_host, 0));
+        pipe_set_debug(dbg_dev);
+    }
+    CUDA_TRY(launch_chain_pipe(a, s));
+    if (dbg_host) {
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess || dbg_host[0] > 0) {
+            fprintf(stderr, "[pipe debug] %s, %d stuck waits (cta thread tag parity):\n", cudaGetErrorString(e), dbg_host[0]);
+            for (int k = 0; k < std::min(dbg_host[0], 1000); ++k)
+                fprintf(stderr, "  %d %d %d %d\n", dbg_host[1 + 4 * k], dbg_host[2 + 4 * k], dbg_host[3 + 4 * k], dbg_host[4 + 4 * k]);
+            fflush(stderr);
+        }
+    }
     return WSVD_OK;
 }
 
@@ -1529,7 +1621,7 @@ int wsvd_chain_step(wsvd_cache_t const* cs, int32_t n, const float* x, float* co
     CUDA_TRY(cudaSetDevice(cs[0]->L->d.device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     if (fused) {
-        rc = run_chain_fused(cs, n, x, ys, s);
+        rc = chain_pipe_ok(cs, n) ? run_chain_pipe(cs, n, x, ys, s) : run_chain_fused(cs, n, x, ys, s);
         if (rc) return rc;
         for (int l = 0; l < n; ++l) cs[l]->len += 1;
         return WSVD_OK;
@@ -1559,7 +1651,7 @@ int wsvd_chain_step_host(wsvd_cache_t const* cs, int32_t n, const float* x_host,
     // mapped pinned buffers: the kernel fetches x and stores the last y itself
     // (one launch + one synchronise, as wsvd_layer_step_host)
     static const bool no_zc = getenv("WSVD_HOST_ZEROCOPY") && std::string(getenv("WSVD_HOST_ZEROCOPY")) == "0";
-    if (fused && !no_zc && !(c0->hkey.x == x_host && c0->hkey.y == y_host)) {
+    if (fused && !no_zc && !chain_pipe_ok(cs, n) && !(c0->hkey.x == x_host && c0->hkey.y == y_host)) {
         cudaPointerAttributes ax{}, ay{};
         const bool okx = cudaPointerGetAttributes(&ax, x_host) == cudaSuccess;
         const bool oky = cudaPointerGetAttributes(&ay, y_host) == cudaSuccess;
@@ -1570,7 +1662,7 @@ int wsvd_chain_step_host(wsvd_cache_t const* cs, int32_t n, const float* x_host,
         c0->hy = c0->hzc ? static_cast<float*>(ay.devicePointer) : nullptr;
         c0->hkey = {x_host, y_host, s};
     }
-    if (fused && !no_zc && c0->hzc) {
+    if (fused && !no_zc && c0->hzc && !chain_pipe_ok(cs, n)) {
         ys[n - 1] = c0->hy;
         rc = run_chain_fused(cs, n, c0->hx, ys.data(), s, true, true);
         if (rc) return rc;

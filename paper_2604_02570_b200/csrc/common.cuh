@@ -206,6 +206,10 @@ WSVD_DEV void cluster_sync_all() {
 WSVD_DEV void st_cluster_f32(uint32_t addr, float v) {
     asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
+WSVD_DEV void st_cluster_v4(uint32_t addr, float x, float y, float z, float w) {
+    asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(x), "f"(y), "f"(z), "f"(w)
+                 : "memory");
+}
 WSVD_DEV void mbar_arrive_remote(uint32_t bar_cluster_addr) {  // release at cluster scope
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }

@@ -164,10 +164,36 @@ struct StepArgs {
     int p3_tma;            // O-projection input rows staged by TMA (1) or by plain loads (0)
     int x_first;           // parked projection weights go out after the token slice is requested
     int l2_next;           // prefetch the next layer's late weight items into L2 during the tail
+    int chain_pre;         // the next layer's first cache stages per CTA prefetched into L2 during the tail
     int nlayers;           // 1 .. kStepMaxLayers
     StepLayer layer[kStepMaxLayers];
 };
 bool step_supported(int R, int B, int nh, int Kp, int oKp, int otiles, int grid);
+
+// The layer chain with the batch as two groups half a layer apart (step2.cu):
+// one group's latency-bound phases run under the other's attention stream.
+struct PipeArgs {
+    const float* x;        // [B][E] layer-0 tokens (device)
+    unsigned* bar[2];      // per group: grid barrier count (monotone, wrap-safe compares)
+    unsigned* bgen[2];     // per group: barrier generations completed
+    float* P[2];           // per group: [splits][8][Nrows] projection partials
+    uint8_t* xo[2];        // per group: [osplits][16][1024] bf16 hi / lo O-projection rows (swizzled)
+    float* ws[2];          // per group: [grid][6][36] segment states
+    uint64_t* trace;       // [grid][24] phase marks of (trace_group, trace_layer), or null
+    int trace_layer, trace_group;
+    int B, nh, E, Kp, Nrows, e_out, oKp, otiles;
+    int grid, cluster;
+    int nlayers;
+    StepLayer layer[kStepMaxLayers];
+};
+bool pipe_supported(int R, int B, int nh, int Kp, int oKp, int otiles, int grid);
+size_t pipe_xo_bytes(int oKp);            // per group
+size_t pipe_ws_bytes(int grid);           // per group
+size_t pipe_p_bytes(int Kp, int Nrows);   // per group
+int pipe_resident_ctas_per_sm();
+int pipe_pair_clusters_ok(int grid);
+cudaError_t launch_chain_pipe(const PipeArgs& a, cudaStream_t s);
+int pipe_set_debug(int* mapped);  // debug builds (-DWSVD_PIPE_DEBUG): where stuck waits are recorded
 int step_item_k();
 size_t step_xo_bytes(int B, int oKp);  // bytes of StepArgs::xo
 size_t step_ws_bytes(int grid);        // bytes of StepArgs::ws

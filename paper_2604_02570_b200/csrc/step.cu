@@ -79,15 +79,16 @@ struct SC {
     static constexpr int PARTB = 2 * kNA * 16 * MT * 16 * 4;  // P3 partial tiles [2][kNA][16][MT*16] fp32
     static constexpr bool PART_IN_RED = PARTB <= RED;          // the merge area is free during P3
     static constexpr int CUTB = (kMaxG + 1) * 8 + kMaxU * 32 + 16;  // + the segment table + (pos, nseg)
-    static constexpr int FIXED = kNA * kItem + XB + RED + CUTB + 768;
-    static constexpr int NB_RAW = (225 * 1024 - FIXED) / STAGE;
+    // two range tables (layer parity: the next layer's is built during this layer's attention)
+    static constexpr int FIXED = kNA * kItem + XB + RED + 2 * CUTB + 768;
+    static constexpr int NB_RAW = (227 * 1024 - FIXED) / STAGE;
     static constexpr int NB = NB_RAW > 6 ? 6 : NB_RAW;
     static constexpr int RING = NB * STAGE;
     static constexpr int B_OFF = kNA * kItem;
     static constexpr int X_OFF = B_OFF + NB * STAGE;
     static constexpr int RED_OFF = X_OFF + XB;
     static constexpr int CUT_OFF = RED_OFF + RED;
-    static constexpr int BAR_OFF = CUT_OFF + CUTB;
+    static constexpr int BAR_OFF = CUT_OFF + 2 * CUTB;
     static constexpr int SMEM = BAR_OFF + 512;
     static constexpr bool OK = NB_RAW >= 2 && XB2 + (PART_IN_RED ? 0 : PARTB) <= NB * STAGE;
 };
@@ -311,9 +312,13 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     float* wst = qts + kMaxU * R;                              // [kMaxU][kNW][R+2]
     __nv_bfloat16* nrow = reinterpret_cast<__nv_bfloat16*>(wst + kMaxU * kNW * (R + 2));  // [kMaxU][2R]
     float* pst = reinterpret_cast<float*>(nrow + kMaxU * 2 * R);  // [R+2] the pair partner's state (DSMEM)
-    long long* cut = reinterpret_cast<long long*>(smem + C::CUT_OFF);  // [G+1]
-    SegInfo* sinf = reinterpret_cast<SegInfo*>(cut + kMaxG + 1);          // [kMaxU]
-    volatile int* meta = reinterpret_cast<volatile int*>(sinf + kMaxU);   // [0] pos [1] nseg of the current layer
+    // range table of layer li (buffer li & 1): cut [G+1], segments [kMaxU], meta [0] pos [1] nseg
+    auto cut_of = [&](int li) { return reinterpret_cast<long long*>(smem + C::CUT_OFF + (li & 1) * C::CUTB); };
+    auto sinf_of = [&](int li) { return reinterpret_cast<SegInfo*>(cut_of(li) + kMaxG + 1); };
+    auto meta_of = [&](int li) { return reinterpret_cast<volatile int*>(sinf_of(li) + kMaxU); };
+    // tables built so far (helper; readers spin on it -- a count never aliases
+    // the way an mbarrier parity can when the builder runs a layer ahead)
+    volatile int* tbuilt = reinterpret_cast<volatile int*>(smem + C::BAR_OFF + 504);
     uint64_t* fullA = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
     uint64_t* emptyA = fullA + kNA;
     uint64_t* fullB = emptyA + kNA;
@@ -326,9 +331,9 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     uint64_t* b1bar = wdone + C::NB;      // grid barrier 1 passed (gates the parked stages' refill)
     uint64_t* pbar = b1bar + 1;           // the pair partner's state landed (DSMEM)
     uint64_t* xin = pbar + 1;             // every consumer warp has requested its token-slice loads
-    uint64_t* tready = xin + 1;           // the layer's range / segment table is built (helper)
-    uint64_t* p3done = tready + 1;        // the layer's O-projection no longer uses the attention ring
-    static_assert((2 * kNA + 2 * C::NB + 2 * kMaxU + 1 + 2 * C::NB + C::NB + 5) * 8 <= C::SMEM - C::BAR_OFF,
+    uint64_t* p3done = xin + 1;           // the layer's O-projection no longer uses the attention ring
+    uint64_t* ybar = p3done + 1;          // pair P3: the odd CTA's split-1 sums landed (DSMEM, kNW arrivals)
+    static_assert((2 * kNA + 2 * C::NB + 2 * kMaxU + 1 + 2 * C::NB + C::NB + 6) * 8 <= 504,
                   "mbarriers overflow their shared-memory region");
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -365,12 +370,16 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     // sit at the end of the attention ring, the partial tiles in the merge area.
     struct P3G {
         int t3lo, nt3, t3step, p3s0, p3ns, np3, per, xoff, p3lo;
-        bool ycontig, ysplit;
+        bool ycontig, ysplit, pairy;
     };
     auto p3geom = [&](int li) {
         P3G g;
         g.ycontig = a.y_host != 0 && li == nL - 1;
         g.ysplit = !g.ycontig && osplits == 2;
+        // CTA pairs: the odd CTA's split-1 sums cross into the even CTA through
+        // distributed shared memory, which writes y = split 0 + split 1 with
+        // plain stores (no zeroing pass, no atomics; the same fixed order)
+        g.pairy = g.ysplit && a.cluster == 2;
         const int cps3 = G / 2;
         if (g.ysplit) {
             const int pj3 = cta / 2;
@@ -425,8 +434,9 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             mbar_init(b1bar, 1);
             mbar_init(pbar, 1);
             mbar_init(xin, kNW);
-            mbar_init(tready, 1);
+            *tbuilt = 0;
             mbar_init(p3done, 1);
+            mbar_init(ybar, kNW);
         }
         fence_mbar_init();  // every lane: the fence covers the executing thread's inits
     }
@@ -522,6 +532,30 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             // never holds it up (divergent lanes of one warp are scheduled as one)
             const uint64_t pol = policy_evict_first();
             uint32_t par = 0;  // per attention-ring slot: parity of its fills so far
+            // The first a.chain_pre stages of this CTA's range of layer li into
+            // L2, issued in the previous layer's tail once its projection items
+            // are out: HBM is otherwise idle until layer li's attention starts
+            // (O-projection, barriers, projection, query preparation), and those
+            // stages then stream from L2
+            auto prefetch_cache = [&](int li) {
+                if (a.chain_pre <= 0) return;
+                const StepLayer& Ly = a.layer[li];
+                const int pos = *static_cast<volatile const int*>(Ly.d_len);
+                if (pos <= 0) return;
+                const long long T = static_cast<long long>(nbh) * pos;
+                long long cc[2] = {cut_row(cta, G, T, pos), cut_row(cta + 1, G, T, pos)};
+                const long long* ct = cc - cta;  // a two-entry table seen from this CTA
+                const int ns = seg_count(ct, cta, G, pos, nbh);
+                int left = a.chain_pre;
+                for (int p = 0; p < ns && left > 0; ++p) {
+                    const Seg sg = seg_at(ct, cta, G, pos, rev ? ns - 1 - p : p);
+                    for (int t = sg.t0; t < sg.t1 && left > 0; t += kST, --left) {
+                        const int rows = min(kST, sg.t1 - t);
+                        prefetch_l2_bulk(Ly.cache + (static_cast<size_t>(sg.bh) * Ly.cap + t) * C::ROWB,
+                                         static_cast<uint32_t>(((rows * C::ROWB + 1023) / 1024) * 1024));
+                    }
+                }
+            };
             for (int li = 0; li < nL; ++li) {
                 const uint32_t lp = static_cast<uint32_t>(li) & 1u;
                 if (li > 0) {
@@ -533,16 +567,23 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     for (int st = 0; st < nWS; ++st) {
                         mbar_wait(&emptyB[st], ((par >> st) & 1u) ^ 1u);
                         if (!p3w && (st + 1) * C::STAGE > gp.p3lo) {
+                            prefetch_cache(li);
                             mbar_wait(p3done, lp ^ 1u);
                             p3w = true;
                         }
                         issue_parked(li, 2 * st, 2 * st + 2);
                     }
                     // every other stage of the ring may hold P3 data until P3 is done
-                    if (!p3w) mbar_wait(p3done, lp ^ 1u);
+                    if (!p3w) {
+                        prefetch_cache(li);
+                        mbar_wait(p3done, lp ^ 1u);
+                    }
                 }
-                mbar_wait(tready, lp);
-                const int pos = meta[0], nseg = meta[1];
+                while (*tbuilt < li + 1) {
+                }
+                __threadfence_block();
+                const SegInfo* sinf = sinf_of(li);
+                const int nseg = meta_of(li)[1];
                 const StepLayer& Ly = a.layer[li];
                 const size_t cap = static_cast<size_t>(Ly.cap);
                 int ib = 0;  // stage fills of this layer: slot ib % NB
@@ -585,6 +626,9 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     // ---- the range / segment table of layer li (helper warp; off the
     // consumers' path: P1 does not need it)
     auto build_table = [&](int li) {
+        long long* cut = cut_of(li);
+        SegInfo* sinf = sinf_of(li);
+        volatile int* meta = meta_of(li);
         const int pos = *static_cast<volatile const int*>(a.layer[li].d_len);
         const long long T = static_cast<long long>(nbh) * pos;
         for (int c = lane; c <= G; c += 32) cut[c] = cut_row(c, G, T, pos);
@@ -607,7 +651,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             if (a.trace && li == a.trace_layer) a.trace[cta * kTr + 11] = static_cast<uint64_t>(nseg);
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(tready);
+        if (lane == 0) {
+            __threadfence_block();
+            *tbuilt = li + 1;
+        }
     };
     if (warp == kHelp) build_table(0);
 
@@ -616,6 +663,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     unsigned abase = 0; // ring-A sequence index of the layer's first item
     unsigned pcnt = 0;  // helper: pair-partner states received (pbar phases)
     unsigned p3cnt = 0; // consumers: TMA-staged P3 rounds (p3bar phases)
+    unsigned ycnt = 0;  // consumers: pair P3 rounds (ybar phases)
     for (l = 0; l < nL; ++l) {
         const StepLayer& Ly = a.layer[l];
         const uint32_t lp = static_cast<uint32_t>(l) & 1u;
@@ -653,26 +701,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             }
             if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid, (l == 0) ? xin : nullptr);
             named_bar_sync(2, 32 * kNW);
-            // the kNW consumer warps take items in turn: layer 0 the weight
-            // ring's four first (in flight first), later layers the parked ones
-            // first (loaded during the previous layer's tail)
-            for (int o = warp; o < np1; o += kNW) {
-                const int k = (l == 0) ? o : (o < nBH ? kNA + o : o - nBH);
-                float facc[MT][2][4];
-                if (k >= kNA && k < kNA + nBH) {
-                    const int b = k - kNA;
-                    mbar_wait(&wfull[b], lp);
-                    item_mma<MT>(smem_u32(parked(b)), smem_u32(xbuf), lane, facc);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&wdone[b / 2]);
-                } else {
-                    const unsigned ia = abase + static_cast<unsigned>(k < kNA ? k : k - nBH);
-                    const int slot = static_cast<int>(ia % kNA);
-                    mbar_wait(&fullA[slot], (ia / kNA) & 1u);
-                    item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(xbuf), lane, facc);
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&emptyA[slot]);
-                }
+            // warps 0-3 take the weight-ring items (ring item i on warp i % 4:
+            // every fill of a slot is consumed by one warp, in order, so a
+            // parity wait never sees an older phase), warps 4-7 the parked ones
+            auto emit = [&](int k, const float (&facc)[MT][2][4]) {
                 const int tile = plo + k;
                 float* P = a.P + static_cast<size_t>(ps) * pstride;
 #pragma unroll
@@ -685,15 +717,39 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                             const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
                             if (m < a.B) P[static_cast<size_t>(m) * a.Nrows + n] = facc[mt][hh][i];
                         }
+            };
+            if (warp < kNA) {
+                for (int i = warp; i < nA1; i += kNA) {
+                    const int k = i < kNA ? i : i + nBH;
+                    const unsigned ia = abase + static_cast<unsigned>(i);
+                    const int slot = static_cast<int>(ia % kNA);
+                    float facc[MT][2][4];
+                    mbar_wait(&fullA[slot], (ia / kNA) & 1u);
+                    item_mma<MT>(smem_u32(ringA + slot * kItem), smem_u32(xbuf), lane, facc);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&emptyA[slot]);
+                    emit(k, facc);
+                }
+            } else {
+                for (int b = warp - kNA; b < nBH; b += kNW - kNA) {
+                    float facc[MT][2][4];
+                    mbar_wait(&wfull[b], lp);
+                    item_mma<MT>(smem_u32(parked(b)), smem_u32(xbuf), lane, facc);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&wdone[b / 2]);
+                    emit(kNA + b, facc);
+                }
             }
         }
         // helper: the first segment's M_QK column does not depend on the
         // projection; load it while the barrier drains
         float mq0[R];
         int nseg = 0, pos = 0;
+        long long* cut = cut_of(l);
+        const SegInfo* sinf = sinf_of(l);
         if (warp == kHelp) {
-            nseg = meta[1];
-            pos = meta[0];
+            nseg = meta_of(l)[1];
+            pos = meta_of(l)[0];
             if (nseg > 0) {
                 const int h0 = sinf[rev ? nseg - 1 : 0].bh % a.nh;
                 const float* mq = Ly.mqk + static_cast<size_t>(h0) * R * R + lane;
@@ -707,9 +763,11 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         if (tid == 0) mbar_arrive(b1bar);
         STEP_MARK(3);
         if (warp < kNW) {
-            mbar_wait(tready, lp);  // (built before G1: returns at once)
-            nseg = meta[1];
-            pos = meta[0];
+            while (*tbuilt < l + 1) {  // (built before G1: passes at once)
+            }
+            __threadfence_block();
+            nseg = meta_of(l)[1];
+            pos = meta_of(l)[0];
         }
         auto seg_of = [&](int p) { return rev ? nseg - 1 - p : p; };
         const size_t cap = static_cast<size_t>(Ly.cap);
@@ -775,6 +833,9 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 prep(p, mqv);
             }
             if (nseg > 0) STEP_MARK(4);
+            // the next layer's table into the other buffer, while this layer's
+            // attention streams (its readers use this layer's buffer)
+            if (l + 1 < nL) build_table(l + 1);
             // (b) per segment as the consumers finish it: merge the kNW warp states
             //     in warp order (+ the own token for a region's last segment).  A
             //     region held by one CTA is complete.  A region shared by the two
@@ -884,7 +945,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             STEP_MARK(6);
         } else {
             // ========================================================= consumer warps
-            if (g3.ysplit) {
+            if (g3.ysplit && !g3.pairy) {
                 // y collects the two K splits' partial sums (P3): zero this CTA's
                 // share now -- after barrier 1, so a y that aliases x is not
                 // touched before x is consumed
@@ -1014,10 +1075,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         STEP_MARK(7);
         if (cta == 0 && tid == 0) *Ly.d_len = pos + 1;
 
-        if (warp == kHelp) {
-            // the next layer's table while P3 runs (this layer's readers are done)
-            if (l + 1 < nL) build_table(l + 1);
-        } else {
+        if (warp != kHelp) {
             // ---- P3: folded O-projection over the prefetched W'_o items.  The X
             // slices this CTA's items use (hi / lo bf16 rows built by the mergers)
             // land at the end of the attention ring -- all at once, or one K
@@ -1102,7 +1160,48 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     }
                     return v;
                 };
-                if (!g.ycontig) {
+                if (g.pairy) {
+                    // [tile][row m][16 columns] fp32 split-1 sums, in the even CTA's merge area
+                    float* recv = reinterpret_cast<float*>(smem + C::RED_OFF + (C::PART_IN_RED ? C::PARTB : 0));
+                    const int q4 = g.nt3 * a.B * 4;  // 4-column groups
+                    if (cta & 1) {
+                        const uint32_t dst = cluster_map(smem_u32(recv), 0u);
+                        for (int i = tid; i < q4; i += 32 * kNW) {
+                            const int ti = i / (a.B * 4), r = i - ti * a.B * 4;
+                            const int m = r >> 2, n0 = (r & 3) * 4;
+                            st_cluster_v4(dst + 4u * static_cast<uint32_t>((ti * a.B + m) * 16 + n0), psum(ti, n0, m),
+                                          psum(ti, n0 + 1, m), psum(ti, n0 + 2, m), psum(ti, n0 + 3, m));
+                        }
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_remote(cluster_map(smem_u32(ybar), 0u));
+                    } else {
+                        float own[4][4];  // this CTA's split-0 sums (<= 4 groups per thread at B <= 32, nt3 <= 4)
+                        for (int u = 0, i = tid; i < q4; ++u, i += 32 * kNW) {
+                            const int ti = i / (a.B * 4), r = i - ti * a.B * 4;
+                            const int m = r >> 2, n0 = (r & 3) * 4;
+#pragma unroll
+                            for (int e = 0; e < 4; ++e) own[u & 3][e] = psum(ti, n0 + e, m);
+                        }
+                        mbar_wait_cluster(ybar, ycnt & 1u);
+                        for (int u = 0, i = tid; i < q4; ++u, i += 32 * kNW) {
+                            const int ti = i / (a.B * 4), r = i - ti * a.B * 4;
+                            const int m = r >> 2, n0 = (r & 3) * 4;
+                            const int col = (g.t3lo + ti) * 16 + n0;
+                            const float4 o = *reinterpret_cast<const float4*>(recv + (ti * a.B + m) * 16 + n0);
+                            float* yr = Ly.y + static_cast<size_t>(m) * a.e_out;
+                            const float v0 = own[u & 3][0] + o.x, v1 = own[u & 3][1] + o.y;
+                            const float v2 = own[u & 3][2] + o.z, v3 = own[u & 3][3] + o.w;
+                            if (col + 4 <= a.e_out && (a.e_out & 3) == 0) {
+                                *reinterpret_cast<float4*>(yr + col) = make_float4(v0, v1, v2, v3);
+                            } else {
+                                const float v[4] = {v0, v1, v2, v3};
+                                for (int e = 0; e < 4; ++e)
+                                    if (col + e < a.e_out) yr[col + e] = v[e];
+                            }
+                        }
+                    }
+                    ++ycnt;
+                } else if (!g.ycontig) {
                     for (int i = tid; i < g.nt3 * 16 * a.B; i += 32 * kNW) {
                         const int ti = i / (16 * a.B), r = i - ti * 16 * a.B;
                         const int m = r / 16, n = r - m * 16;  // n fastest: 64-byte row segments of y

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--config", default=bench.DEFAULT_CONFIG)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--layers", type=int, default=8)
+    ap.add_argument("--only", type=int, default=0, help="time only the chain of this many layers")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
     E, B, L = cfg["E"], cfg["B"], cfg["L"]
@@ -40,7 +41,7 @@ def main():
         layers[li].step(x, ys[li], graph=False)
     torch.cuda.synchronize()
     s = torch.cuda.current_stream()
-    for m in [1, 2, 4, 8]:
+    for m in ([args.only] if args.only else [1, 2, 4, 8]):
         if m > n:
             break
         ch = DecodeChain(layers[:m])
@@ -54,6 +55,8 @@ def main():
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / args.reps
         print(f"chain {m}: {us:8.2f} us per launch, {us / m:7.2f} us per layer", flush=True)
+    if args.only:
+        return
     # one launch per layer, same layers
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
