@@ -703,7 +703,8 @@ def run_stack(args, cfg_name, cfg):
             "data": "synthetic (random-init factors and FFN; synthetic N(0,1) latent caches)",
             "config": {"workload": cfg_name, "layers": nl, "embed_dim": E, "heads": cfg["nh"],
                        "heads_per_gpu": nh_g, "head_dim": H, "rank": cfg["r"], "global_batch": B,
-                       "ctx": L_end - K // 2, "ffn": f"toy tanh FFN 2E, bf16 cuBLAS, replicated",
+                       "ctx": L_end - K // 2, "ffn": "toy tanh FFN 2E (pipeline.cpp:330-334): wsvd_ffn_forward, two tcgen05 GEMMs "
+                              "(gemm_tc.cu), bf16 weights, replicated",
                        "parallelism": f"heads/{shard_of} (each GPU one {shard_of}-way head shard; {world} of "
                                       f"the {shard_of} shards run)",
                        "l2": f"inputs larger than L2: {nl * lbytes / 1e9:.1f} GB of latent caches per GPU",

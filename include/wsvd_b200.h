@@ -230,6 +230,19 @@ int wsvd_layer_step_host(wsvd_cache_t cache, const float* x_host, float* y_host,
  * calls with the same arguments replay it (1 launch instead of ~5). */
 int wsvd_layer_step_graph(wsvd_cache_t cache, const float* x, float* y, void* stream);
 
+/* ------------------------------------------------------ feed-forward --
+ * The reference model's per-layer feed-forward after the O-projection
+ * (pipe::decode_factored, pipeline.cpp:330-334): out = tanh(o . ff1) . ff2,
+ * ff1 [embed_dim][hidden], ff2 [hidden][embed_dim] (row-major fp32, stored on
+ * the device as bf16 W-tiles); two skinny tensor-core GEMMs (the projection
+ * kernel), the split sums with the tanh fused.  o, out: [rows][embed_dim]
+ * fp32 device buffers (rows <= 128; out may alias o). */
+typedef struct wsvd_ffn_s* wsvd_ffn_t;
+int wsvd_ffn_create(int32_t embed_dim, int32_t hidden, const float* ff1, const float* ff2, int32_t device,
+                    wsvd_ffn_t* out);
+int wsvd_ffn_destroy(wsvd_ffn_t ffn);
+int wsvd_ffn_forward(wsvd_ffn_t ffn, const float* o, int32_t rows, float* out, void* stream);
+
 /* -------------------------------------------------------------- chains --
  * pipe::decode_factored's layer loop (pipeline.cpp:318-336) over the
  * attention blocks of n layers, one token per sequence: layer 0 takes x,

@@ -323,6 +323,59 @@ def fold_oproj(layer: Layer, w_o, rpad: int, storage=None):
     return storage(fold) if storage is not None else fold
 
 
+def decode_factored(layers, w_os, ffn, xs, tile: int = 32, device_storage: bool = False, rpad: int | None = None,
+                    device_rows=None):
+    """pipe::decode_factored (reference src/pipeline.cpp:304-339) for one
+    sequence: xs [T][E] tokens through len(layers) layers from empty caches.
+    Per token and layer: append_token (:320), fused_decode_step (:321-322),
+    heads_row . W_o (:323-329), cur = tanh(o . ff1) . ff2 (:330-334); the
+    output row of token t is the last layer's cur (:336).  layers: Layer
+    factors, w_os: W_o [nh*H][E] per layer, ffn: (ff1 [E][F], ff2 [F][E]) per
+    layer.  Returns [T][E].
+
+    device_storage=True keeps the arithmetic in fp64 but rounds the operands
+    the device stores to bf16 where it stores them: the tokens entering each
+    layer, the appended cache rows, the folded O-projection W'_o = B_V . W_o
+    (heads_row . W_o = v~ . W'_o, fold_oproj) and the FFN GEMM inputs o and
+    tanh(o . ff1).  The factors and FFN weights are taken as given (pass the
+    bf16 values the device was given).  device_rows: per layer (K rows, V
+    rows) [nh][T][>= rmax] read back from the device -- the appended rows the
+    attention then runs over (a single bf16 rounding flip of a cache row is a
+    2^-8 perturbation the softmax over a short context carries straight to
+    the output; the layer tests compare on the device's rows the same way)."""
+    xs = np.asarray(xs, dtype=np.float64)
+    T, E = xs.shape
+    caches = [(np.zeros((lay.nh, T, lay.rmax)), np.zeros((lay.nh, T, lay.rmax))) for lay in layers]
+    folds = None
+    if device_storage:
+        rpad = rpad or max(lay.rmax for lay in layers)
+        folds = [fold_oproj(lay, w, rpad, bf16_round) for lay, w in zip(layers, w_os)]
+    out = np.zeros((T, E))
+    for t in range(T):
+        cur = xs[t]
+        for li, lay in enumerate(layers):
+            ck, cv = caches[li]
+            q = append_token(lay, ck, cv, t, bf16_round(cur) if device_storage else cur)
+            if device_storage:
+                ck[:, t] = bf16_round(ck[:, t])
+                cv[:, t] = bf16_round(cv[:, t])
+            if device_rows is not None:
+                ck[:, t] = device_rows[li][0][:, t, :lay.rmax]
+                cv[:, t] = device_rows[li][1][:, t, :lay.rmax]
+                _, lat = batched_decode_latent(lay, ck[None], cv[None], t + 1, q[None], tile, 1)
+                lat_p = np.zeros((lay.nh, rpad))
+                lat_p[:, :lay.rmax] = lat[0]
+                o = lat_p.reshape(-1) @ folds[li]
+            else:
+                attn = fused_decode_step(lay, ck, cv, t + 1, q, tile)
+                o = attn.reshape(-1) @ np.asarray(w_os[li], dtype=np.float64)
+            ff1, ff2 = (np.asarray(w, dtype=np.float64) for w in ffn[li])
+            h = np.tanh((bf16_round(o) if device_storage else o) @ ff1)
+            cur = (bf16_round(h) if device_storage else h) @ ff2
+        out[t] = cur
+    return out
+
+
 def batched_append(layer: Layer, ck, cv, pos: int, x, threads: int = 1):
     Bn = ck.shape[0]
     q = np.zeros((Bn, layer.nh, layer.H))

@@ -89,6 +89,9 @@ SIGNATURES = {
     "wsvd_matmul_f32": (C.c_int, [_fp, _fp, _i32, _i32, _i32, _fp, _vp]),
     "wsvd_chain_step": (C.c_int, [C.POINTER(_vp), _i32, _fp, C.POINTER(_vp), _vp]),
     "wsvd_chain_step_host": (C.c_int, [C.POINTER(_vp), _i32, _fp, _fp, _vp]),
+    "wsvd_ffn_create": (C.c_int, [_i32, _i32, _fp, _fp, _i32, C.POINTER(_vp)]),
+    "wsvd_ffn_destroy": (C.c_int, [_vp]),
+    "wsvd_ffn_forward": (C.c_int, [_vp, _fp, _i32, _fp, _vp]),
 }
 
 _lib = None

@@ -33,7 +33,7 @@ CUDA_FLAGS += os.environ.get("WSVD_EXTRA_NVCC", "").split()  # experiment switch
 CXX_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-Wall", "-Wextra", f"-I{os.path.join(ROOT, 'include')}",
              "-I/usr/local/cuda/include"]
 
-CU_SOURCES = ["attn.cu", "attn_tc.cu", "gemm.cu", "append.cu", "step.cu", "step2.cu", "dense.cu", "capi.cu"]
+CU_SOURCES = ["attn.cu", "attn_tc.cu", "gemm.cu", "append.cu", "step.cu", "step2.cu", "gemm_tc.cu", "dense.cu", "capi.cu"]
 # host_decode.cpp (the C++ wsvd::decode drop-in) is NOT part of the library: it
 # is compiled inside the reference build against the reference's own
 # matrix / errors / factorize headers (oracle/Makefile target dropin)

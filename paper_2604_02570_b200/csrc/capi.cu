@@ -272,6 +272,14 @@ struct wsvd_cache_s {
     int* d_done() const { return ctrl.as<int>() + 1; }
 };
 
+struct wsvd_ffn_s {
+    int E = 0, F = 0, device = 0, sms = 148;
+    int Kp1 = 0, Kp2 = 0;  // padded K of the two GEMMs (E, F)
+    bool tc = false;       // E, F multiples of 64: tcgen05 GEMMs over plain row-major bf16 weights
+    DevBuf W1, W2;         // tc: ff1^T [F][E], ff2^T [E][F] bf16; else W-tiles (rows n = output unit)
+    DevBuf P, Hd, Xb;      // split partials; hidden activations; the bf16 input rows (tc)
+};
+
 struct wsvd_comm_s {
     void* comm = nullptr;
     int nranks = 1, rank = 0;
@@ -1674,6 +1682,123 @@ int wsvd_chain_step_host(wsvd_cache_t const* cs, int32_t n, const float* x_host,
         CUDA_TRY(cudaMemcpyAsync(y_host, ys[n - 1], xb, cudaMemcpyDeviceToHost, s));
     }
     CUDA_TRY(cudaStreamSynchronize(s));
+    return WSVD_OK;
+}
+
+// ----------------------------------------------------------- feed-forward --
+// pipe::decode_factored's toy FFN (pipeline.cpp:330-334) on the skinny GEMM
+int wsvd_ffn_create(int32_t E, int32_t F, const float* ff1, const float* ff2, int32_t device, wsvd_ffn_t* out) {
+    if (!ff1 || !ff2 || !out) return set_err(WSVD_ECONFIG, "null argument");
+    if (E <= 0 || F <= 0) return set_err(WSVD_ESHAPE, "empty feed-forward");
+    if (sm100_devices() == 0) return set_err(WSVD_ECUDA, "no sm_100 (B200) device visible");
+    CUDA_TRY(cudaSetDevice(device));
+    auto* f = new wsvd_ffn_s();
+    f->E = E;
+    f->F = F;
+    f->device = device;
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    f->sms = prop.multiProcessorCount;
+    f->Kp1 = round_up(E, 512);
+    f->Kp2 = round_up(F, 512);
+    // W-tiles of a [N][K] row matrix (row n = output unit, K = input): W1 rows are
+    // ff1's columns, W2 rows ff2's columns
+    auto pack = [&](const float* w, int K, int N, int Kp, DevBuf& dst) -> int {
+        const int np = round_up(N, 16);
+        std::vector<uint8_t> rows(static_cast<size_t>(np) * Kp * 2, 0), tiled(rows.size());
+        uint16_t* rr = reinterpret_cast<uint16_t*>(rows.data());
+        for (int n0 = 0; n0 < N; n0 += 64)  // blocked transpose: both sides stay in cache
+            for (int k0 = 0; k0 < K; k0 += 64)
+                for (int k = k0; k < std::min(K, k0 + 64); ++k)
+                    for (int n = n0; n < std::min(N, n0 + 64); ++n)
+                        rr[static_cast<size_t>(n) * Kp + k] = f32_to_bf16_bits(w[static_cast<size_t>(k) * N + n]);
+        pack_wtiles(rows.data(), np, Kp * 2, 512 * 2, tiled.data());
+        CUDA_TRY(dst.alloc(tiled.size()));
+        CUDA_TRY(cudaMemcpy(dst.p, tiled.data(), tiled.size(), cudaMemcpyHostToDevice));
+        return WSVD_OK;
+    };
+    // K-chunk-major bf16 [K/64][N][64] (the tcgen05 GEMM's TMA layout: every
+    // 256-row box of a 64-wide K chunk is one contiguous 32 KB block)
+    auto plain = [&](const float* w, int K, int N, DevBuf& dst) -> int {
+        std::vector<uint16_t> rows(static_cast<size_t>(N) * K);
+        for (int k0 = 0; k0 < K; k0 += 64)
+            for (int k = k0; k < std::min(K, k0 + 64); ++k)
+                for (int n = 0; n < N; ++n)
+                    rows[(static_cast<size_t>(k0 / 64) * N + n) * 64 + (k - k0)] =
+                        f32_to_bf16_bits(w[static_cast<size_t>(k) * N + n]);
+        CUDA_TRY(dst.alloc(rows.size() * 2));
+        CUDA_TRY(cudaMemcpy(dst.p, rows.data(), rows.size() * 2, cudaMemcpyHostToDevice));
+        return WSVD_OK;
+    };
+    static const bool no_tc = getenv("WSVD_FFN_SKINNY") != nullptr;  // A/B switch: the mma.sync skinny GEMM
+    f->tc = !no_tc && tc_gemm_supported(1, F, E) && tc_gemm_supported(1, E, F);
+    int rc = f->tc ? plain(ff1, E, F, f->W1) : pack(ff1, E, F, f->Kp1, f->W1);
+    if (rc == WSVD_OK) rc = f->tc ? plain(ff2, F, E, f->W2) : pack(ff2, F, E, f->Kp2, f->W2);
+    if (rc) {
+        delete f;
+        return rc;
+    }
+    *out = f;
+    return WSVD_OK;
+}
+
+int wsvd_ffn_destroy(wsvd_ffn_t f) {
+    delete f;
+    return WSVD_OK;
+}
+
+int wsvd_ffn_forward(wsvd_ffn_t f, const float* o, int32_t M, float* out, void* stream) {
+    if (!f || !o || !out) return set_err(WSVD_ECONFIG, "null argument");
+    if (M <= 0) return set_err(WSVD_ESHAPE, "feed-forward over zero rows");
+    if (!f->tc && !gemm_fits(BF16, M, 512)) return set_err(WSVD_ECONFIG, std::to_string(M) + " rows do not fit the GEMM kernel");
+    CUDA_TRY(cudaSetDevice(f->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (f->tc) {
+        // tcgen05: hidden = bf16(tanh(bf16(o) . ff1)) in the GEMM epilogue; out
+        // = hidden . ff2 over K splits when its N tiles leave SMs idle (summed by
+        // the reduction kernel in split order)
+        const int ch = std::min(M, 128);
+        const int nt2 = f->E / 64;
+        const int sp2 = std::max(1, std::min(f->F / 64, f->sms / nt2));
+        if (f->Xb.n < static_cast<size_t>(ch) * f->E * 2) CUDA_TRY(f->Xb.alloc(static_cast<size_t>(ch) * f->E * 2));
+        if (f->Hd.n < static_cast<size_t>(ch) * f->F * 2) CUDA_TRY(f->Hd.alloc(static_cast<size_t>(ch) * f->F * 2));
+        if (f->P.n < static_cast<size_t>(sp2) * ch * f->E * 4) CUDA_TRY(f->P.alloc(static_cast<size_t>(sp2) * ch * f->E * 4));
+        for (int m0 = 0; m0 < M; m0 += 128) {
+            const int mc = std::min(128, M - m0);
+            CUDA_TRY(launch_f32_to_bf16(o + static_cast<size_t>(m0) * f->E, f->Xb.p, static_cast<size_t>(mc) * f->E, s));
+            TcGemmArgs g1{f->Xb.p, f->W1.p, f->Hd.p, mc, f->F, f->E, f->F, 1, 1, 1, 0, 0};
+            CUDA_TRY(launch_tc_gemm(g1, s));
+            float* dst = out + static_cast<size_t>(m0) * f->E;
+            TcGemmArgs g2{f->Hd.p, f->W2.p, sp2 == 1 ? static_cast<void*>(dst) : f->P.p, mc, f->E, f->F, f->E, sp2, 0, 0, 0, 0};
+            CUDA_TRY(launch_tc_gemm(g2, s));
+            if (sp2 > 1) CUDA_TRY(launch_reduce_partials(f->P.as<float>(), sp2, mc, f->E, dst, s, 0, 0));
+        }
+        return WSVD_OK;
+    }
+    const int s1 = f->Kp1 / 512, s2 = f->Kp2 / 512;
+    const size_t need = std::max(static_cast<size_t>(s1) * M * f->F, static_cast<size_t>(s2) * M * f->E) * 4;
+    if (f->P.n < need) CUDA_TRY(f->P.alloc(need));
+    if (f->Hd.n < static_cast<size_t>(M) * f->F * 4) CUDA_TRY(f->Hd.alloc(static_cast<size_t>(M) * f->F * 4));
+    auto gemm = [&](const void* W, const float* X, int N, int K, int Kp) -> cudaError_t {
+        GemmArgs g{};
+        g.W = W;
+        g.X = X;
+        g.P = f->P.p;
+        g.M = M;
+        g.N = N;
+        g.K = K;
+        g.Kp = Kp;
+        g.KS = 512;
+        g.ldx = K;
+        g.wdtype = BF16;
+        g.grid = f->sms;
+        return launch_gemm(g, s);
+    };
+    // hidden = tanh(o . ff1)  (pipeline.cpp:330-333), out = hidden . ff2 (:334)
+    CUDA_TRY(gemm(f->W1.p, o, f->F, f->E, f->Kp1));
+    CUDA_TRY(launch_reduce_partials(f->P.as<float>(), s1, M, f->F, f->Hd.as<float>(), s, 1));
+    CUDA_TRY(gemm(f->W2.p, f->Hd.as<float>(), f->E, f->F, f->Kp2));
+    CUDA_TRY(launch_reduce_partials(f->P.as<float>(), s2, M, f->E, out, s, 0));
     return WSVD_OK;
 }
 

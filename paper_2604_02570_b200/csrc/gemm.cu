@@ -528,7 +528,7 @@ cudaError_t launch_wt(const GemmArgs& a, cudaStream_t s) {
 }
 
 __global__ void reduce_partials_kernel(const float* __restrict__ P, int splits, int MN,
-                                       float* __restrict__ y) {
+                                       void* __restrict__ y, int act, int y_bf16) {
     griddep_wait();
     griddep_launch_dependents();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -536,7 +536,9 @@ __global__ void reduce_partials_kernel(const float* __restrict__ P, int splits, 
     float sum = 0.f;
 #pragma unroll 8
     for (int k = 0; k < splits; ++k) sum += __ldcg(P + static_cast<size_t>(k) * MN + i);
-    y[i] = sum;
+    const float v = act == 1 ? tanhf(sum) : sum;  // act 1: the toy FFN's tanh (pipeline.cpp:331-333)
+    if (y_bf16) static_cast<__nv_bfloat16*>(y)[i] = __float2bfloat16_rn(v);
+    else static_cast<float*>(y)[i] = v;
 }
 
 }  // namespace
@@ -586,10 +588,10 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s) {
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_reduce_partials(const float* P, int splits, int M, int N, float* y,
-                                   cudaStream_t s) {
+cudaError_t launch_reduce_partials(const float* P, int splits, int M, int N, void* y,
+                                   cudaStream_t s, int act, int y_bf16) {
     const int MN = M * N;
-    return launch_pdl(reduce_partials_kernel, dim3((MN + 255) / 256), dim3(256), 0, s, P, splits, MN, y);
+    return launch_pdl(reduce_partials_kernel, dim3((MN + 255) / 256), dim3(256), 0, s, P, splits, MN, y, act, y_bf16);
 }
 
 }  // namespace wsvd_k

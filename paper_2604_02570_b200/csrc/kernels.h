@@ -34,8 +34,27 @@ bool f32_rows_path(int M, int Kp, int KS);
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s);
 
 // Sum split partials into fp32 y [M][N] (fixed split order).
-cudaError_t launch_reduce_partials(const float* P, int splits, int M, int N, float* y,
-                                   cudaStream_t s);
+// act 1: tanh of the sum (the toy FFN's hidden activation); y_bf16: y is bf16
+cudaError_t launch_reduce_partials(const float* P, int splits, int M, int N, void* y,
+                                   cudaStream_t s, int act = 0, int y_bf16 = 0);
+
+// ------------------------------------------- dense GEMM on tcgen05 (gemm_tc.cu) --
+// D[M][N] = X[M][K] . W[N][K]^T, bf16 operands: X row-major [M][K], W K-chunk-
+// major [K/64][N][64] (each 64-wide K slice of all rows contiguous), fp32
+// accumulation in TMEM; M <= 128 token rows, N % 64 == 0 (64-column CTA
+// tiles; up to four of a K split share each X chunk by TMA multicast), K % 64 == 0.
+// One split: epilogue act 1 = tanh, out bf16 or fp32 [M][ldo]; `splits` > 1:
+// fp32 partials [splits][M][ldo] for launch_reduce_partials.
+struct TcGemmArgs {
+    const void* X;
+    const void* W;
+    void* out;         // bf16 (out_bf16) or fp32 [M][ldo] after act; fp32 [splits][M][ldo] partials
+    int M, N, K, ldo, splits, act, out_bf16;
+    int ntiles, cl;    // set by launch_tc_gemm
+};
+bool tc_gemm_supported(int M, int N, int K);
+cudaError_t launch_tc_gemm(const TcGemmArgs& a, cudaStream_t s);
+cudaError_t launch_f32_to_bf16(const float* x, void* y, size_t n, cudaStream_t s);  // n % 4 == 0
 
 // ------------------------------------------------------ activation quant --
 // Per token: optional S1 rotation (FWHT over blocks of rot_blk, times

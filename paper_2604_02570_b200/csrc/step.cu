@@ -522,6 +522,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 for (int i = (li == 0 ? ia_pre : 0); i < na; ++i) {
                     const int slot = static_cast<int>(ia_g % kNA);
                     mbar_wait(&emptyA[slot], ((ia_g / kNA) & 1u) ^ 1u);
+                    if (a.trace && li == a.trace_layer && i == 0) a.trace[cta * kTr + 23] = gtimer();
                     mbar_arrive_expect_tx(&fullA[slot], kItem);
                     tma_bulk_g2s(ringA + slot * kItem, a_src(li, i), kItem, &fullA[slot]);
                     ++ia_g;
@@ -701,6 +702,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             }
             if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid, (l == 0) ? xin : nullptr);
             named_bar_sync(2, 32 * kNW);
+            STEP_MARK(20);  // the token slice is staged
             // warps 0-3 take the weight-ring items (ring item i on warp i % 4:
             // every fill of a slot is consumed by one warp, in order, so a
             // parity wait never sees an older phase), warps 4-7 the parked ones
@@ -730,6 +732,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     if (lane == 0) mbar_arrive(&emptyA[slot]);
                     emit(k, facc);
                 }
+                STEP_MARK(21);  // the weight-ring items are done
             } else {
                 for (int b = warp - kNA; b < nBH; b += kNW - kNA) {
                     float facc[MT][2][4];
@@ -739,6 +742,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     if (lane == 0) mbar_arrive(&wdone[b / 2]);
                     emit(kNA + b, facc);
                 }
+                STEP_MARK(22);  // the parked items are done
             }
         }
         // helper: the first segment's M_QK column does not depend on the

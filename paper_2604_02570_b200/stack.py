@@ -10,16 +10,65 @@ The reference's model has no residual or normalisation and a toy FFN of width
 `DecodeLayer` (its own latent cache and factors; append + attention + the
 B_V-folded O-projection run by the library's kernels), heads may be sharded
 across GPUs (the O-projection partial sums meet in one NCCL all-reduce), and
-the FFN is a replicated pair of bf16 cuBLAS GEMMs (a plain library GEMM: it is
-not on the WSVD path).
+the FFN is the library's `FeedForward` (wsvd_ffn_*: two skinny tensor-core
+GEMMs over bf16 weight tiles with the tanh fused into the split reduction),
+replicated on every GPU.
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
+
+import numpy as np
+
+from . import _native as N
+from .errors import ShapeError
+
+
+class FeedForward:
+    """out = tanh(o . ff1) . ff2 on the device (pipeline.cpp:330-334).
+    ff1 [E][F], ff2 [F][E] host arrays (stored as bf16)."""
+
+    def __init__(self, ff1: np.ndarray, ff2: np.ndarray, device: int = 0):
+        ff1 = np.ascontiguousarray(ff1, dtype=np.float32)
+        ff2 = np.ascontiguousarray(ff2, dtype=np.float32)
+        E, F = ff1.shape
+        if ff2.shape != (F, E):
+            raise ShapeError(f"ff2 must be [{F}][{E}], got {ff2.shape}")
+        self.E, self.F, self.device = E, F, device
+        h = C.c_void_p()
+        N.call("wsvd_ffn_create", E, F, C.c_void_p(ff1.ctypes.data), C.c_void_p(ff2.ctypes.data), device,
+               C.byref(h))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and N._lib is not None:
+            N.lib().wsvd_ffn_destroy(self.h)
+            self.h = None
+
+    def forward(self, o, out, stream=None):
+        """o, out: fp32 device tensors [rows][E] (out may alias o)."""
+        import torch
+        s = stream if stream is not None else torch.cuda.current_stream()
+        N.call("wsvd_ffn_forward", self.h, C.c_void_p(o.data_ptr()), int(o.shape[0]), C.c_void_p(out.data_ptr()),
+               C.c_void_p(s.cuda_stream))
+
+
+def toy_ffn_weights(E: int, F: int, seed: int):
+    """ff1 ~ N(0, 1/E), ff2 ~ N(0, 1/F) (toymodel.cpp:81-95 initialisation
+    scale), fp32, rounded to bf16 values (the device's storage)."""
+    rng = np.random.default_rng(seed)
+    ff1 = (rng.standard_normal((E, F), dtype=np.float32) / np.float32(math.sqrt(E)))
+    ff2 = (rng.standard_normal((F, E), dtype=np.float32) / np.float32(math.sqrt(F)))
+    for w in (ff1, ff2):  # round to nearest even bf16 in place
+        u = w.view(np.uint32)
+        u += np.uint32(0x7FFF) + ((u >> 16) & np.uint32(1))
+        u &= np.uint32(0xFFFF0000)
+    return ff1, ff2
 
 
 class DecodeStack:
-    def __init__(self, layers, ffn_dim: int | None = None, comm=None, seed: int = 0, dtype=None):
+    def __init__(self, layers, ffn_dim: int | None = None, comm=None, seed: int = 0, ffn_weights=None):
         import torch
         self.torch = torch
         self.layers = list(layers)
@@ -31,38 +80,37 @@ class DecodeStack:
             raise ValueError("stack layers must project back to the model width")
         self.F = ffn_dim or 2 * self.E
         self.comm = comm
-        dt = dtype or torch.bfloat16
         dev = torch.device("cuda", l0.device)
-        g = torch.Generator(device=dev)
-        g.manual_seed(seed)
-        # ff1 ~ N(0, 1/E), ff2 ~ N(0, 1/F) (toymodel.cpp:81-95 initialisation scale)
-        self.ff1 = [(torch.randn((self.E, self.F), generator=g, device=dev) / math.sqrt(self.E)).to(dt)
-                    for _ in self.layers]
-        self.ff2 = [(torch.randn((self.F, self.E), generator=g, device=dev) / math.sqrt(self.F)).to(dt)
-                    for _ in self.layers]
+        # per layer (ff1, ff2): given, or the toy model's random init (generated
+        # and uploaded one layer at a time; the host copies are not kept)
+        self.ffn_weights = ffn_weights
+        self.ffns = []
+        for i in range(len(self.layers)):
+            w1, w2 = ffn_weights[i] if ffn_weights else toy_ffn_weights(self.E, self.F, seed * 1000 + i)
+            self.ffns.append(FeedForward(w1, w2, device=l0.device))
         self.o = torch.empty((self.B, self.E), device=dev, dtype=torch.float32)
-        self.o16 = torch.empty((self.B, self.E), device=dev, dtype=dt)
-        self.h = torch.empty((self.B, self.F), device=dev, dtype=dt)
-        self.cur16 = torch.empty((self.B, self.E), device=dev, dtype=dt)
         self.cur = torch.empty((self.B, self.E), device=dev, dtype=torch.float32)
 
     def ffn_bytes(self) -> int:
-        return sum(w.numel() * w.element_size() for w in self.ff1 + self.ff2)
+        return 2 * 2 * self.E * self.F * len(self.layers)  # bf16 ff1 + ff2 per layer
 
-    def step(self, x, y, stream=None):
-        """One token for every sequence through every layer: x, y [B][E] fp32."""
-        torch = self.torch
+    def step(self, x, y, stream=None, record=None):
+        """One token for every sequence through every layer: x, y [B][E] fp32.
+        record (a list, tests): per layer (input token, O-projection output,
+        FFN output) copies."""
         cur = x
         n = len(self.layers)
         for i, layer in enumerate(self.layers):
+            if record is not None:
+                record.append([cur.clone()])
             layer.step(cur, self.o, graph=False, stream=stream)
             if self.comm is not None:
                 self.comm.allreduce_(self.o)
-            self.o16.copy_(self.o)
-            torch.matmul(self.o16, self.ff1[i], out=self.h)
-            torch.tanh_(self.h)
-            torch.matmul(self.h, self.ff2[i], out=self.cur16)
             dst = y if i == n - 1 else self.cur
-            dst.copy_(self.cur16)
+            if record is not None:
+                record[-1].append(self.o.clone())
+            self.ffns[i].forward(self.o, dst, stream=stream)
+            if record is not None:
+                record[-1].append(dst.clone())
             cur = dst
         return y

@@ -242,3 +242,19 @@ def test_int_path_rules():
     import ctypes as C
     O.lib().orc_unpack_int4(packed.ctypes.data_as(C.POINTER(C.c_uint8)), 4, out.ctypes.data_as(O._i8p))
     assert list(out) == [-1, -8, 1, 7]
+
+
+def test_oracle_decode_factored_device_storage_close_to_reference():
+    """the oracle's decode_factored: its device-storage variant stays within a
+    few bf16 ulps of the plain fp64 composition (the bf16 storage is the only
+    difference) -- a CPU-side sanity check of the restatement"""
+    from paper_2604_02570_b200.stack import toy_ffn_weights  # noqa: F401 (numpy only)
+    rng = O.Rng(1)
+    E, nh, H, r, F = 256, 2, 128, 32, 512
+    lbs = [O.random_layer(rng, E, H, [[r, r, r]] * nh).map(O.bf16_round) for _ in range(2)]
+    wos = [O.bf16_round(rng.normal_matrix(nh * H, E, 1 / np.sqrt(E))) for _ in range(2)]
+    ffn = [toy_ffn_weights(E, F, i) for i in range(2)]
+    xs = O.bf16_round(rng.normal_matrix(4, E))
+    a = O.decode_factored(lbs, wos, ffn, xs)
+    b = O.decode_factored(lbs, wos, ffn, xs, device_storage=True, rpad=32)
+    assert np.abs(a - b).max() <= 2 ** -6 * np.abs(a).max()
