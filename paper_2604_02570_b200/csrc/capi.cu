@@ -219,6 +219,8 @@ struct wsvd_layer_s {
     DevBuf mqk;                       // [nh][R][R] qt_scale * B_Q . B_K^T (fp32)
     bool mqk_ready = false;
     DevBuf bkt;                       // [nh] B_K^T tiles for the tcgen05 attention (attn_tc.cu)
+    DevBuf Atc;                       // bf16 A in K-chunk-major layout for the tcgen05 token GEMM
+    unsigned atc_gen = ~0u;           // the generation Atc was built from
     bool bkt_ready = false;
     unsigned gen = 0;                 // bumped by every upload: captured step graphs go stale
 };
@@ -235,7 +237,7 @@ struct wsvd_cache_s {
     int len = 0;                      // host mirror of *d_len
     DevBuf data, scales, ctrl;        // ctrl: [0]=d_len, [1]=done
     DevBuf qt, q_tmp, attn_ws, attn_cnt, vlat;
-    DevBuf P, xq, sx;                 // projection workspace
+    DevBuf P, xq, sx, xb;             // projection workspace (xb: bf16 token rows of the tcgen05 GEMM)
     int P_M = 0, P_splits = 0;        // rows / K splits of the last projection
     DevBuf oP, y_tmp;                 // O-proj partials
     DevBuf x_dev, y_dev;              // staging for the host-buffer step
@@ -297,9 +299,41 @@ int check_layer(wsvd_layer_t l) {
 }
 
 // projection of M token rows (fp32 x [M][E]) into the partial workspace
+// Many token rows (prefill; steps at B >= 64) with bf16 weights: the dense
+// projection on tcgen05 (gemm_tc.cu) over a K-chunk-major copy of A, its K
+// splits left as partials for the append epilogue to sum in split order.
+int run_projection_tc(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* splits_out) {
+    wsvd_layer_s* L = c->L;
+    if (L->atc_gen != L->gen || !L->Atc.p) {
+        CUDA_TRY(L->Atc.alloc(static_cast<size_t>(L->Nrows) * L->Kp * 2));
+        CUDA_TRY(launch_wtiles_to_chunks(L->A.p, L->Nrows, L->Kp, L->ks, L->Atc.p, s));
+        L->atc_gen = L->gen;
+    }
+    const int nt = L->Nrows / 64;
+    const int splits = std::max(1, std::min(L->Kp / 64, c->sms / nt));
+    const size_t need = static_cast<size_t>(splits) * M * L->Nrows * 4;
+    if (c->P.n < need) CUDA_TRY(c->P.alloc(need));
+    if (c->xb.n < static_cast<size_t>(128) * L->Kp * 2) CUDA_TRY(c->xb.alloc(static_cast<size_t>(128) * L->Kp * 2));
+    for (int m0 = 0; m0 < M; m0 += 128) {
+        const int mc = std::min(128, M - m0);
+        CUDA_TRY(launch_f32_to_bf16(x + static_cast<size_t>(m0) * L->Kp, c->xb.p, static_cast<size_t>(mc) * L->Kp, s));
+        TcGemmArgs g{c->xb.p, L->Atc.p, c->P.as<float>() + static_cast<size_t>(m0) * L->Nrows, mc, L->Nrows, L->Kp,
+                     L->Nrows, splits, 0, 0, 0, 0, M};
+        CUDA_TRY(launch_tc_gemm(g, s));
+    }
+    *splits_out = splits;
+    c->P_M = M;
+    c->P_splits = splits;
+    return WSVD_OK;
+}
+
 int run_projection(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* splits_out) {
     wsvd_layer_s* L = c->L;
     const int wd = L->d.weight_dtype;
+    static const bool no_tc = getenv("WSVD_PROJ_SKINNY") != nullptr;  // A/B switch
+    if (!no_tc && wd == BF16 && M >= 64 && L->Kp == L->d.embed_dim && L->Kp % 64 == 0 &&
+        tc_gemm_supported(std::min(M, 128), L->Nrows, L->Kp))
+        return run_projection_tc(c, x, M, s, splits_out);
     const int ks = (wd == F32 && f32_rows_path(M, L->Kp, 512)) ? 512 : L->ks;
     if (!gemm_fits(wd, M, ks))
         return set_err(WSVD_ECONFIG, std::to_string(M) + " token rows do not fit the projection kernel");

@@ -218,7 +218,8 @@ __global__ void __launch_bounds__(128, 1) gemm_tc_kernel(const __grid_constant__
             tmem_group(g, v);
             if (row >= a.M) continue;
             float4* dst = reinterpret_cast<float4*>(static_cast<float*>(a.out) +
-                                                    (static_cast<size_t>(split) * a.M + row) * a.ldo + n0 + g * 16);
+                                                    (static_cast<size_t>(split) * (a.ldm ? a.ldm : a.M) + row) * a.ldo +
+                                                    n0 + g * 16);
 #pragma unroll
             for (int q = 0; q < 4; ++q) dst[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
         }
@@ -236,6 +237,18 @@ __global__ void f32_to_bf16_kernel(const float* __restrict__ x, __nv_bfloat16* _
     if (i >= n4) return;
     const float4 v = reinterpret_cast<const float4*>(x)[i];
     reinterpret_cast<uint2*>(y)[i] = make_uint2(pack_bf16x2(v.x, v.y), pack_bf16x2(v.z, v.w));
+}
+
+// one 16-byte unit (8 bf16 of row n, K offset k0) per thread
+__global__ void wtiles_to_chunks_kernel(const uint8_t* __restrict__ wt, int N, int Kp, int ks, uint8_t* __restrict__ out) {
+    const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // unit index, n-major
+    const int upr = Kp / 8;
+    if (i >= static_cast<size_t>(N) * upr) return;
+    const int n = static_cast<int>(i / upr), k0 = static_cast<int>(i % upr) * 8;
+    const int tile = n / 16, rr = n % 16, sp = k0 / ks, u = (k0 % ks) / 8, splits = Kp / ks;
+    const size_t src = ((static_cast<size_t>(tile) * splits + sp) * 16 + rr) * ks * 2 + static_cast<size_t>(u ^ ((rr & 1) << 2)) * 16;
+    const size_t dst = ((static_cast<size_t>(k0 / 64) * N + n) * 64 + (k0 % 64)) * 2;
+    *reinterpret_cast<uint4*>(out + dst) = *reinterpret_cast<const uint4*>(wt + src);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -287,6 +300,14 @@ cudaError_t launch_tc_gemm(const TcGemmArgs& a, cudaStream_t s) {
         attr = true;
     }
     return launch_pdl_cluster(gemm_tc_kernel, dim3(b.ntiles * a.splits), dim3(128), kSmem, s, b.cl, xm, wm, b);
+}
+
+cudaError_t launch_wtiles_to_chunks(const void* wt, int N, int Kp, int ks, void* out, cudaStream_t s) {
+    if (N % 16 || Kp % 64 || Kp % ks || ks % 8) return cudaErrorInvalidValue;
+    const size_t units = static_cast<size_t>(N) * (Kp / 8);
+    wtiles_to_chunks_kernel<<<static_cast<unsigned>((units + 255) / 256), 256, 0, s>>>(
+        static_cast<const uint8_t*>(wt), N, Kp, ks, static_cast<uint8_t*>(out));
+    return cudaGetLastError();
 }
 
 cudaError_t launch_f32_to_bf16(const float* x, void* y, size_t n, cudaStream_t s) {

@@ -51,10 +51,13 @@ struct TcGemmArgs {
     void* out;         // bf16 (out_bf16) or fp32 [M][ldo] after act; fp32 [splits][M][ldo] partials
     int M, N, K, ldo, splits, act, out_bf16;
     int ntiles, cl;    // set by launch_tc_gemm
+    int ldm;           // partials: rows between K splits (0: M)
 };
 bool tc_gemm_supported(int M, int N, int K);
 cudaError_t launch_tc_gemm(const TcGemmArgs& a, cudaStream_t s);
 cudaError_t launch_f32_to_bf16(const float* x, void* y, size_t n, cudaStream_t s);  // n % 4 == 0
+// bf16 W-tiles [N/16][Kp/ks][16][ks] (gemm.cu layout) -> K-chunk-major [Kp/64][N][64]
+cudaError_t launch_wtiles_to_chunks(const void* wt, int N, int Kp, int ks, void* out, cudaStream_t s);
 
 // ------------------------------------------------------ activation quant --
 // Per token: optional S1 rotation (FWHT over blocks of rot_blk, times
