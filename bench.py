@@ -261,7 +261,9 @@ def run_ours(args, cfg_name, cfg):
                 chain_of(start, cnt).step(xs[j // NL], ys[start:start + cnt])
             else:
                 cnt = 1
-                layers[start].step(xs[j // NL] if start == 0 else ys[start - 1], ys[start])
+                # eager launches (PDL-chained): a captured graph is bound to its
+                # buffers, and layer 0's token changes every pass
+                layers[start].step(xs[j // NL] if start == 0 else ys[start - 1], ys[start], graph=False)
                 if comm is not None:
                     comm.allreduce_(ys[start])
             j += cnt

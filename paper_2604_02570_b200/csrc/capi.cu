@@ -334,7 +334,9 @@ int run_projection(wsvd_cache_s* c, const float* x, int M, cudaStream_t s, int* 
     if (!no_tc && wd == BF16 && M >= 64 && L->Kp == L->d.embed_dim && L->Kp % 64 == 0 &&
         tc_gemm_supported(std::min(M, 128), L->Nrows, L->Kp))
         return run_projection_tc(c, x, M, s, splits_out);
-    const int ks = (wd == F32 && f32_rows_path(M, L->Kp, 512)) ? 512 : L->ks;
+    static const bool f32_rows = getenv("WSVD_F32_ROWS") != nullptr;  // A/B switch: the register GEMV
+    const int ks = (wd == F32 && !f32_rows && f32_tma_path(M, L->Kp, L->Kp)) ? L->Kp
+                   : (wd == F32 && f32_rows_path(M, L->Kp, 512)) ? 512 : L->ks;
     if (!gemm_fits(wd, M, ks))
         return set_err(WSVD_ECONFIG, std::to_string(M) + " token rows do not fit the projection kernel");
     const int splits = L->Kp / ks;

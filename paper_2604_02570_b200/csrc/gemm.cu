@@ -459,6 +459,100 @@ __global__ void __launch_bounds__(kF32RowsThreads, 2) skinny_f32_rows_kernel(con
     }
 }
 
+// fp32 decode GEMV over a TMA ring (M <= 4 token rows, Kp <= 4096): one CTA
+// per SM streams a contiguous run of whole weight rows (Kp * 4 bytes each)
+// through 8 stages -- 128 KB in flight per SM, where the register double
+// buffer above holds ~32 KB -- and warp w owns stage w (rows i = w mod 8, so
+// every fill of a stage is consumed by one warp, in order).  The first stages
+// go out before the grid-dependency wait.  One K split: P[0][M][N].
+constexpr int kGvW = 8;  // consumer warps = stages
+template <int M>
+__global__ void __launch_bounds__(32 * (kGvW + 1), 1) gemv_f32_tma_kernel(const GemmArgs a) {
+    extern __shared__ __align__(128) uint8_t gsm[];
+    const int rb = a.Kp * 4;
+    float* xs = reinterpret_cast<float*>(gsm + kGvW * rb);  // [M][Kp]
+    uint64_t* full = reinterpret_cast<uint64_t*>(xs + M * a.Kp);
+    uint64_t* empty = full + kGvW;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n0 = static_cast<int>(static_cast<long>(blockIdx.x) * a.N / gridDim.x);
+    const int n1 = static_cast<int>(static_cast<long>(blockIdx.x + 1) * a.N / gridDim.x);
+    const float* W = reinterpret_cast<const float*>(a.W);
+    if (tid == 0) {
+        for (int i = 0; i < kGvW; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    const int pre = min(kGvW, n1 - n0);
+    if (warp == kGvW && lane == 0)
+        for (int i = 0; i < pre; ++i) {
+            mbar_arrive_expect_tx(&full[i], rb);
+            tma_bulk_g2s(gsm + i * rb, W + static_cast<size_t>(n0 + i) * a.Kp, rb, &full[i]);
+        }
+    griddep_wait();
+    griddep_launch_dependents();
+    if (a.commit_len && blockIdx.x == 0 && tid == 0) atomicAdd(a.commit_len, 1);
+    if (warp == kGvW) {
+        if (lane == 0)
+            for (int i = pre; i < n1 - n0; ++i) {
+                const int st = i % kGvW;
+                mbar_wait(&empty[st], ((i / kGvW) & 1u) ^ 1u);
+                mbar_arrive_expect_tx(&full[st], rb);
+                tma_bulk_g2s(gsm + st * rb, W + static_cast<size_t>(n0 + i) * a.Kp, rb, &full[st]);
+            }
+        return;
+    }
+    const float* X = reinterpret_cast<const float*>(a.X);
+    for (int i = tid; i < M * a.Kp; i += 32 * kGvW) {
+        const int m = i / a.Kp, k = i - m * a.Kp;
+        xs[i] = k < a.K ? X[static_cast<size_t>(m) * a.ldx + k] : 0.f;
+    }
+    named_bar_sync(1, 32 * kGvW);
+    const int kv = a.Kp / 128;  // float4 per lane per row
+    for (int i = warp; i < n1 - n0; i += kGvW) {
+        const int st = i % kGvW;
+        mbar_wait(&full[st], (i / kGvW) & 1u);
+        const float4* wr = reinterpret_cast<const float4*>(gsm + st * rb) + lane;
+        float acc[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = 0.f;
+#pragma unroll 4
+        for (int v = 0; v < kv; ++v) {
+            const float4 w = wr[v * 32];
+#pragma unroll
+            for (int m = 0; m < M; ++m) {
+                const float4 x = reinterpret_cast<const float4*>(xs + m * a.Kp)[v * 32 + lane];
+                acc[m] = fmaf(w.x, x.x, acc[m]);
+                acc[m] = fmaf(w.y, x.y, acc[m]);
+                acc[m] = fmaf(w.z, x.z, acc[m]);
+                acc[m] = fmaf(w.w, x.w, acc[m]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            const float sum = warp_sum(acc[m]);
+            if (lane == 0) reinterpret_cast<float*>(a.P)[static_cast<size_t>(m) * a.N + n0 + i] = sum;
+        }
+    }
+}
+
+template <int M>
+cudaError_t launch_gemv_f32_tma(const GemmArgs& a, cudaStream_t s) {
+    const int smem = kGvW * a.Kp * 4 + M * a.Kp * 4 + 2 * kGvW * 8;
+    auto k = gemv_f32_tma_kernel<M>;
+    static int attr = 0;
+    if (smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    return launch_pdl(k, dim3(std::min(a.grid, a.N)), dim3(32 * (kGvW + 1)), smem, s, a);
+}
+
 template <int M, int U>
 cudaError_t launch_f32_rows_u(const GemmArgs& a, cudaStream_t s) {
     const int smem = M * a.Kp * 4;
@@ -543,6 +637,8 @@ __global__ void reduce_partials_kernel(const float* __restrict__ P, int splits, 
 
 }  // namespace
 
+bool f32_tma_path(int M, int Kp, int KS) { return M >= 1 && M <= kF32RowsM && KS == Kp && Kp % 128 == 0 && Kp <= 4096; }
+
 bool f32_rows_path(int M, int Kp, int KS) {
     return M <= kF32RowsM && (KS == 256 || KS == 512 || KS == 1024) && Kp % KS == 0 && M * Kp * 4 <= 200 * 1024;
 }
@@ -565,6 +661,15 @@ cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s) {
         case I8: return launch_wt<I8>(a, s);
         case I4: return launch_wt<I4>(a, s);
         case F32: {
+            static const bool no_tma = std::getenv("WSVD_F32_ROWS") != nullptr;  // A/B switch: register GEMV
+            if (!no_tma && f32_tma_path(a.M, a.Kp, a.KS)) {
+                switch (a.M) {
+                    case 1: return launch_gemv_f32_tma<1>(a, s);
+                    case 2: return launch_gemv_f32_tma<2>(a, s);
+                    case 3: return launch_gemv_f32_tma<3>(a, s);
+                    default: return launch_gemv_f32_tma<4>(a, s);
+                }
+            }
             if (f32_rows_path(a.M, a.Kp, a.KS)) {
                 switch (a.M) {
                     case 1: return launch_f32_rows<1>(a, s);

@@ -31,6 +31,8 @@ struct GemmArgs {
 bool gemm_fits(int wdtype, int M, int KS);
 // fp32 weights, M <= 4 token rows, KS in {256, 512, 1024}: the balanced row-piece GEMV
 bool f32_rows_path(int M, int Kp, int KS);
+// fp32 weights, M <= 4 token rows, one K split (KS == Kp <= 4096): the TMA-ring GEMV
+bool f32_tma_path(int M, int Kp, int KS);
 cudaError_t launch_gemm(const GemmArgs& a, cudaStream_t s);
 
 // Sum split partials into fp32 y [M][N] (fixed split order).
