@@ -88,15 +88,19 @@ def summarize_launches(tag):
                      f"{m.get('dram__bytes_read.sum', 0) / 1e6:.2f},{m.get('dram__bytes_write.sum', 0) / 1e6:.2f}")
     with open(os.path.join(OUT, f"{tag}_launches.csv"), "w") as fh:
         fh.write("\n".join(lines) + "\n")
-    for key, fname, unit in (("decode_attn", "attn_traffic.json", "decode_attn_kernel"),
-                             ("layer_step", "step_traffic.json", "layer_step_kernel")):
+    for key, fname, unit in (("decode_attn", "attn_traffic.json", "decode_attn_kernel launch"),
+                             ("layer_step", "step_traffic.json", "layer step")):
         ms = [m for (i, k), m in per.items() if key in k]
         if not ms:
             continue
-        traffic = sum(m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0) for m in ms) / len(ms)
+        # a layer_step_kernel launch longer than 200 us is an 8-layer chain
+        # (tools/profile_round.sh captures the bench's chain launches): per layer step
+        div = [8 if key == "layer_step" and m.get("gpu__time_duration.sum", 0) > 200e3 else 1 for m in ms]
+        traffic = sum((m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)) / d
+                      for m, d in zip(ms, div)) / len(ms)
         with open(os.path.join(OUT, fname), "w") as fh:
             json.dump({"7b-r32-b16-ctx4k-bf16": round(traffic), "source": f"profiles/{tag}_launches.csv",
-                       "unit": f"bytes per {unit} launch (dram read + write, ncu)"}, fh, indent=1)
+                       "unit": f"bytes per {unit} (dram read + write, ncu; chain launches / 8)"}, fh, indent=1)
     return per
 
 
@@ -104,10 +108,12 @@ def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     os.makedirs(OUT, exist_ok=True)
     summarize_launches(tag)
-    for name in ("step_full", "attn_full", "tc_full", "gemm_full", "i8_full", "f32rows_full"):
+    for name in ("chain_full", "step_full", "attn_full", "tc_full", "gemm_full", "i8_full", "f32rows_full",
+                 "gemmtc_full", "gemv_full"):
         summarize_full(name, tag)
     for f in ("bench.json", "bench_ref.json", "timing.txt", "gpu.txt", "step_trace.txt", "bench_config3.json",
-              "bench_config1.json", "timing_config3.txt", "timing_config1.txt", "bench_stack_config5.json"):
+              "bench_config1.json", "timing_config3.txt", "timing_config1.txt", "bench_stack_config5.json",
+              "chain_timing.txt", "step_trace_chain.txt", "ffn_timing.txt"):
         src = os.path.join(RAW, f)
         if os.path.exists(src):
             with open(src) as a, open(os.path.join(OUT, f"{tag}_{f}"), "w") as b:
