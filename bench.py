@@ -162,6 +162,17 @@ def synthetic_layer(cfg, seed=0):
     return f, w_o
 
 
+def l2_statement(NL, attn_bytes, step_bytes, l2_bytes):
+    """Whether a step's inputs can be L2-resident: each step reads its layer's
+    cache and weights, last touched NL steps earlier; the cycle is compared with
+    the device's L2 size (queried)."""
+    cycle = NL * step_bytes
+    verdict = "inputs larger than L2" if cycle > l2_bytes else "WARNING: the rotating working set fits in L2"
+    return (f"{verdict}: L2 {l2_bytes / 1e6:.0f} MB; {NL} rotating layers, each step reads its layer's "
+            f"{attn_bytes / 1e6:.0f} MB latent cache and {(step_bytes - attn_bytes) / 1e6:.0f} MB of weights last "
+            f"touched {NL} steps earlier ({cycle / 1e9:.2f} GB cycle)")
+
+
 def algorithmic_bytes(cfg, B, nh_g, L):
     """each byte counted once.  Returns (attention-kernel
     bytes per launch, whole-step bytes)."""
@@ -341,6 +352,7 @@ def run_ours(args, cfg_name, cfg):
     attn_bytes, step_bytes = algorithmic_bytes(cfg, B, nh_g, L_mid)
     peak, peak_kind = measured_peak()
     achieved = attn_bytes / (attn_ms / 1e3) / 1e9
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
     fused = layer.launches_per_step() == 1
 
     def traffic_of(fname):
@@ -429,9 +441,7 @@ def run_ours(args, cfg_name, cfg):
                        "weight_dtype": cfg["weights"], "parallelism": f"heads/{world}",
                        "step": "append(x.A_qkv) + fused decode attention + O-proj"
                                + (" + NCCL all-reduce" if world > 1 else ""),
-                       "l2": f"inputs larger than L2: {NL} rotating layers, each step reads its layer's "
-                             f"{attn_bytes / 1e6:.0f} MB latent cache and {(step_bytes - attn_bytes) / 1e6:.0f} MB "
-                             f"of weights last touched {NL} steps earlier ({NL * step_bytes / 1e9:.2f} GB cycle)",
+                       "l2": l2_statement(NL, attn_bytes, step_bytes, l2_bytes),
                        "layers": NL,
                        "launch": (f"the {NL} rotating layers chained (layer l+1's token = layer l's y): one "
                                   f"persistent kernel per pass over them (wsvd_chain_step); {launches} launches "
@@ -709,7 +719,8 @@ def run_stack(args, cfg_name, cfg):
                               "(gemm_tc.cu), bf16 weights, replicated",
                        "parallelism": f"heads/{shard_of} (each GPU one {shard_of}-way head shard; {world} of "
                                       f"the {shard_of} shards run)",
-                       "l2": f"inputs larger than L2: {nl * lbytes / 1e9:.1f} GB of latent caches per GPU",
+                       "l2": f"inputs larger than L2 ({torch.cuda.get_device_properties(dev).L2_cache_size / 1e6:.0f} MB): "
+                             f"{nl * lbytes / 1e9:.1f} GB of latent caches per GPU",
                        "launch": "whole 32-layer step captured as one CUDA graph"},
             "roofline": {"bound": "hbm", "kernel": "whole stack step (all kernels)", "achieved": round(achieved, 1),
                          "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(achieved / peak, 4),
