@@ -123,6 +123,15 @@ WSVD_DEV void chunk_to_f32<BF16>(const uint4& v, float* f) {
     f[4] = bf16lo(v.z); f[5] = bf16hi(v.z); f[6] = bf16lo(v.w); f[7] = bf16hi(v.w);
 }
 // signed bytes -> float through the 2^23 magic: float(0x4B0000uu) - (2^23 + 128)
+// Exact int <-> float conversions for |v| < 2^22 on the full-rate FP32 / INT
+// pipes (I2F / F2I issue at a quarter rate and were hot in the int8 consumers:
+// profiles/r01_i8_full_summary.json).  The int8 MMA sums stay below 2^22
+// (128 * 127 * 127 for the scores at r <= 128, 32 * 127 * 127 for P.V) and the
+// quantised probabilities below 128; f2i_rn_small rounds to nearest even like
+// __float2int_rn.  Results are bit-identical to the conversion instructions.
+WSVD_DEV float i2f_small(int v) { return __int_as_float(v + 0x4B400000) - 12582912.0f; }
+WSVD_DEV int f2i_rn_small(float x) { return __float_as_int(x + 12582912.0f) - 0x4B400000; }
+
 WSVD_DEV void s8x4_to_f32(uint32_t w, float* f) {
     const uint32_t u = w ^ 0x80808080u;
     f[0] = __uint_as_float(__byte_perm(u, 0x4B000000u, 0x7650)) - 8388736.0f;
@@ -445,9 +454,9 @@ WSVD_DEV void consume_mma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, ui
             }
             const float k0 = __low2float(sc2[t0]), k1 = __low2float(sc2[t1]);
             sc[grp][0] = (t4 == 0 && t0 < rows)
-                ? fmaf(static_cast<float>(d[0]), s1, static_cast<float>(d[1]) * s2) * k0 : -INFINITY;
+                ? fmaf(i2f_small(d[0]), s1, i2f_small(d[1]) * s2) * k0 : -INFINITY;
             sc[grp][1] = (t4 == 0 && t1 < rows)
-                ? fmaf(static_cast<float>(d[2]), s1, static_cast<float>(d[3]) * s2) * k1 : -INFINITY;
+                ? fmaf(i2f_small(d[2]), s1, i2f_small(d[3]) * s2) * k1 : -INFINITY;
         }
         float lm = -INFINITY;
 #pragma unroll
@@ -592,9 +601,9 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
             }
             const float k0 = __low2float(sc2[t0]), k1 = __low2float(sc2[t1]);
             sc[grp][0] = (t4 == 0 && t0 < rows)
-                ? fmaf(static_cast<float>(d[0]), s1, static_cast<float>(d[1]) * s2) * k0 : -INFINITY;
+                ? fmaf(i2f_small(d[0]), s1, i2f_small(d[1]) * s2) * k0 : -INFINITY;
             sc[grp][1] = (t4 == 0 && t1 < rows)
-                ? fmaf(static_cast<float>(d[2]), s1, static_cast<float>(d[3]) * s2) * k1 : -INFINITY;
+                ? fmaf(i2f_small(d[2]), s1, i2f_small(d[3]) * s2) * k1 : -INFINITY;
         }
     };
     mbar_wait(&full[slot], phase);
@@ -673,9 +682,9 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
         uint32_t pa[GPW];
 #pragma unroll
         for (int grp = 0; grp < GPW; ++grp) {
-            const int h0 = __float2int_rn(pp[grp][0] * pi1), h1 = __float2int_rn(pp[grp][1] * pi1);
-            const int l0 = max(-127, min(127, __float2int_rn(fmaf(static_cast<float>(-h0), ps1, pp[grp][0]) * pi2)));
-            const int l1 = max(-127, min(127, __float2int_rn(fmaf(static_cast<float>(-h1), ps1, pp[grp][1]) * pi2)));
+            const int h0 = f2i_rn_small(pp[grp][0] * pi1), h1 = f2i_rn_small(pp[grp][1] * pi1);
+            const int l0 = max(-127, min(127, f2i_rn_small(fmaf(i2f_small(-h0), ps1, pp[grp][0]) * pi2)));
+            const int l1 = max(-127, min(127, f2i_rn_small(fmaf(i2f_small(-h1), ps1, pp[grp][1]) * pi2)));
             const uint32_t w = (static_cast<uint32_t>(h0) & 0xffu) | ((static_cast<uint32_t>(h1) & 0xffu) << 8) |
                                ((static_cast<uint32_t>(l0) & 0xffu) << 16) | (static_cast<uint32_t>(l1) << 24);
             const uint32_t x = __shfl_sync(0xffffffffu, w, src_x), y = __shfl_sync(0xffffffffu, w, src_y);
@@ -702,8 +711,8 @@ WSVD_DEV void consume_imma_i8(const AttnArgs& a, const Unit& g, uint8_t* smem, u
         }
 #pragma unroll
         for (int u = 0; u < UV; ++u) {
-            acc[u][0] = fmaf(static_cast<float>(dI[u][0]), ps1, fmaf(static_cast<float>(dI[u][1]), ps2, acc[u][0]));
-            acc[u][1] = fmaf(static_cast<float>(dI[u][2]), ps1, fmaf(static_cast<float>(dI[u][3]), ps2, acc[u][1]));
+            acc[u][0] = fmaf(i2f_small(dI[u][0]), ps1, fmaf(i2f_small(dI[u][1]), ps2, acc[u][0]));
+            acc[u][1] = fmaf(i2f_small(dI[u][2]), ps1, fmaf(i2f_small(dI[u][3]), ps2, acc[u][1]));
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[cur]);
