@@ -10,9 +10,10 @@ The reference's model has no residual or normalisation and a toy FFN of width
 `DecodeLayer` (its own latent cache and factors; append + attention + the
 B_V-folded O-projection run by the library's kernels), heads may be sharded
 across GPUs (the O-projection partial sums meet in one NCCL all-reduce), and
-the FFN is the library's `FeedForward` (wsvd_ffn_*: two skinny tensor-core
-GEMMs over bf16 weight tiles with the tanh fused into the split reduction),
-replicated on every GPU.
+the FFN is the library's `FeedForward` (wsvd_ffn_*: two tcgen05 GEMMs -- TMA
+multicast operands, TMEM accumulators -- over K-chunk-major bf16 weights, the
+tanh and bf16 rounding fused into the first GEMM's epilogue), replicated on
+every GPU.
 """
 from __future__ import annotations
 
