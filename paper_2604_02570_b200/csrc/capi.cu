@@ -658,6 +658,10 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     a.bgen = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 5);
     a.epoch = c->ctrl.as<int>() + 2;
     a.xcnt = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 16);
+    a.p1gen = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 3);
+    a.p1flag = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 256);  // one 128-byte line per CTA
+    static const int g1 = std::getenv("WSVD_STEP_G1") ? std::atoi(std::getenv("WSVD_STEP_G1")) : 0;
+    a.g1 = g1;
     const size_t xob = step_xo_bytes(c->B, L->oKp);
     if (c->xo.n < xob) CUDA_TRY(c->xo.alloc(xob));  // zeroed: rows past the batch stay 0
     a.xo = c->xo.as<uint8_t>();
@@ -694,7 +698,7 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     a.chain_pre = cpre;
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
     static const int trace_layer = getenv("WSVD_STEP_TRACE_LAYER") ? atoi(getenv("WSVD_STEP_TRACE_LAYER")) : -1;
-    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 24 * 8));
+    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 32 * 8));
     a.trace = trace ? c->trace.as<uint64_t>() : nullptr;
     a.trace_layer = trace_layer >= 0 && trace_layer < n ? trace_layer : n - 1;  // default: the last layer
     int rc = fused_serialize(L->d.device, s);
@@ -767,7 +771,7 @@ int run_chain_pipe(wsvd_cache_s* const* cs, int n, const float* x, float* const*
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;
     static const int trace_layer = getenv("WSVD_STEP_TRACE_LAYER") ? atoi(getenv("WSVD_STEP_TRACE_LAYER")) : -1;
     static const int trace_group = getenv("WSVD_STEP_TRACE_GROUP") ? atoi(getenv("WSVD_STEP_TRACE_GROUP")) : 0;
-    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 24 * 8));
+    if (trace && !c->trace.p) CUDA_TRY(c->trace.alloc(static_cast<size_t>(c->sms) * 32 * 8));
     a.trace = trace ? c->trace.as<uint64_t>() : nullptr;
     a.trace_layer = trace_layer >= 0 && trace_layer < n ? trace_layer : n - 1;
     a.trace_group = trace_group & 1;
@@ -1144,7 +1148,8 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     // + 128 KB: the attention rings copy a slot's first stage whole, which may run past the last row
     cudaError_t e = c->data.alloc(rows * c->row_bytes + (128u << 10));
     if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4 + (16u << 10));  // + a stage of scales
-    if (e == cudaSuccess) e = c->ctrl.alloc(256);  // [0] len [1] done [2] step epoch [4,5] barrier [16..32) x-fetch counters
+    if (e == cudaSuccess) e = c->ctrl.alloc(1024 + 160 * 128);  // [0] len [1] done [2] step epoch [3] layer steps
+                                    // [4,5] barrier [16..32) x-fetch counters [256 + 32 c] projection flags
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     if (e == cudaSuccess)
         e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh *

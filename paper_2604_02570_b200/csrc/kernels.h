@@ -175,6 +175,10 @@ struct StepArgs {
     int* epoch;            // fused launches run so far (x-fetch counter generations)
     unsigned* bgen;        // grid-barrier generations completed so far
     unsigned* bar;         // grid barrier count (monotone, wrap-safe compares)
+    unsigned* p1flag;      // [grid][32] per CTA (one 128-byte line each): layers whose projection partials it has written
+    unsigned* p1gen;       // layer steps run so far (the flags' base)
+    int g1;                // A/B: 1 a grid barrier after the projection instead of the per-CTA
+                           // flags; 2 the cache stream starts at this CTA's projection end
     float* P;              // [splits][B][Nrows] projection partials
     float* ws;             // [grid][kMaxU][36] segment states (step_ws_bytes)
     uint8_t* xo;           // [osplits][2][MT*16][1024] bf16 hi / lo X rows of the O-projection (swizzled)

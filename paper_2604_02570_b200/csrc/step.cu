@@ -9,7 +9,11 @@
 //
 //   P1   latent projection P[split][b][n] = x_b . A[:, n] over one K split
 //        (swap-AB mma.sync over W-tiles streamed by TMA, as gemm.cu);
-//   G1   grid barrier: every projection partial is written;
+//   flag per CTA: its projection partials are written (a release count; no
+//        grid barrier -- the helper that prepares a head's query waits for the
+//        flags of exactly the CTAs that produce that head's rows, all splits;
+//        WSVD_STEP_G1=1 restores the grid barrier for A/B: 1.6-1.9 us per
+//        layer slower, profiles/r02_step_ab.txt);
 //   P2   attention over the cached rows 0 .. pos-1: the B*nh*pos rows of all
 //        (sequence, head) regions are cut into G equal contiguous ranges (at
 //        32-row boundaries), one per CTA, so every SM streams the same bytes.
@@ -65,7 +69,7 @@ constexpr int kMaxSplits = 16;       // projection K splits (host-checked)
 constexpr int kWS = 36;              // floats per segment state in ws: acc[32], m, l, pad (16 B rows)
 constexpr int kMaxG = 160;           // CTAs (the range table)
 constexpr int kCut = 32;             // range boundaries fall on multiples of 32 rows (one warp's share)
-constexpr int kTr = 24;              // trace words per CTA (WSVD_STEP_TRACE): marks 0-9, smid, segments, marks 12-23
+constexpr int kTr = 32;              // trace words per CTA (WSVD_STEP_TRACE): marks 0-9, smid, segments, marks 12-31
 
 template <int R, int MT>
 struct SC {
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     uint64_t* p3bar = sfull + kMaxU;    // P3: X slices landed
     uint64_t* wfull = p3bar + 1;        // [2*NB] projection items parked in the attention ring
     uint64_t* wdone = wfull + 2 * C::NB;  // [NB] those items consumed: the stage is free
-    uint64_t* b1bar = wdone + C::NB;      // grid barrier 1 passed (gates the parked stages' refill)
+    uint64_t* b1bar = wdone + C::NB;      // the first segment's producers are seen (gates the parked stages' refill)
     uint64_t* pbar = b1bar + 1;           // the pair partner's state landed (DSMEM)
     uint64_t* xin = pbar + 1;             // every consumer warp has requested its token-slice loads
     uint64_t* p3done = xin + 1;           // the layer's O-projection no longer uses the attention ring
@@ -500,6 +504,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     const unsigned epoch = static_cast<unsigned>(*a.epoch);  // fused launches so far (x-fetch generations)
     const unsigned bgen0 = *a.bgen;                          // grid barriers completed so far
     unsigned gen = bgen0;
+    const unsigned p1base = *a.p1gen;                        // layer steps completed so far
     // Odd CTAs walk their segments backwards: the region a pair (2k, 2k+1)
     // shares is then the LAST one both attend (its two parts finish together
     // and meet through distributed shared memory), the region shared with
@@ -601,7 +606,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         const int slot = ib % C::NB;
                         if (ib < nWS) {
                             mbar_wait(&wdone[slot], lp);  // its parked projection items are consumed
-                            mbar_wait(b1bar, lp);         // and grid barrier 1 has passed
+                            mbar_wait(b1bar, lp);         // and the projection is published
                         }
                         mbar_wait(&emptyB[slot], ((par >> slot) & 1u) ^ 1u);
                         par ^= 1u << slot;
@@ -763,11 +768,15 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         }
         named_bar_sync(1, kSync);
         STEP_MARK(2);  // every projection warp of this CTA is done
-        grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // G1: every projection partial is written
-        if (tid == 0) mbar_arrive(b1bar);
+        // this CTA's projection partials are written: publish them (release;
+        // the helpers that attend a head wait for exactly its producers -- no
+        // grid barrier between the projection and the attention)
+        if (tid == 0) red_release(a.p1flag + 32 * cta);
+        if (a.g1 == 1) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 1)
+        if (tid == 0 && a.g1 != 0) mbar_arrive(b1bar);
         STEP_MARK(3);
         if (warp < kNW) {
-            while (*tbuilt < l + 1) {  // (built before G1: passes at once)
+            while (*tbuilt < l + 1) {  // (built before P1 ended: passes at once)
             }
             __threadfence_block();
             nseg = meta_of(l)[1];
@@ -826,7 +835,36 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&uready[j]);
             };
-            if (nseg > 0) prep(0, mq0);
+            // the projection partials of head h come from the CTAs whose tile runs
+            // cover its rows [3Rh, 3R(h+1)) in every K split: wait for their flags
+            // (one acquire per producer, the lanes in parallel)
+            const unsigned p1t = p1base + static_cast<unsigned>(l) + 1u;
+            auto wait_heads = [&](int p0, int p1) {
+                int i = lane;  // this lane's flattened (segment, producer) index
+                for (int p = p0; p < p1; ++p) {
+                    const int h = sinf[seg_of(p)].bh % a.nh;
+                    const int t0 = h * 3 * R / 16, t1 = ((h + 1) * 3 * R - 1) / 16;
+                    const int j0 = ((t0 + 1) * cps - 1) / ptiles, j1 = ((t1 + 1) * cps - 1) / ptiles;
+                    const int n = (j1 - j0 + 1) * splits;
+                    for (; i < n; i += 32) {
+                        const unsigned* f = a.p1flag + 32 * ((j0 + i / splits) * splits + i % splits);
+                        while (static_cast<int>(ld_acquire(f) - p1t) < 0) __nanosleep(64);
+                    }
+                    i -= n;
+                }
+                __syncwarp();  // (orders the lanes' acquires before every lane's loads)
+            };
+            if (nseg > 0) wait_heads(0, 1);
+            // the cache stream into the stages that held parked items starts once
+            // the first segment's producers are seen: its burst then does not
+            // queue ahead of the projection loads of CTAs still in P1 (measured:
+            // 0.3 us per layer better than starting it at this CTA's own P1 end)
+            if (a.g1 == 0 && lane == 0) mbar_arrive(b1bar);
+            if (nseg > 0) {
+                if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 24] = gtimer();
+                prep(0, mq0);
+                wait_heads(1, nseg);
+            }
             if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 16] = gtimer();
             for (int p = 1; p < nseg; ++p) {
                 const int h = sinf[seg_of(p)].bh % a.nh;
@@ -1247,6 +1285,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     if (cta == 0 && tid == 0) {
         *a.epoch += 1;  // fused launches run (the x-fetch generations)
         *a.bgen = gen;  // this launch's barriers are all passed (every CTA read bgen before its first)
+        *a.p1gen = p1base + static_cast<unsigned>(nL);  // (every CTA read it before the first G2)
     }
 }
 

@@ -52,7 +52,7 @@ constexpr int kMaxSplits = 16;         // projection K splits (host-checked)
 constexpr int kWS = 36;                // floats per segment state in ws
 constexpr int kMaxG = 160;             // CTAs (the range tables)
 constexpr int kCut = 32;               // range boundaries fall on multiples of 32 rows
-constexpr int kTr = 24;                // trace words per CTA
+constexpr int kTr = 32;                // trace words per CTA
 
 template <int R>
 struct PC {

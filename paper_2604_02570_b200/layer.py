@@ -174,7 +174,7 @@ class DecodeLayer:
         if what == "xq":
             return raw.view(np.int8)
         if what == "trace":
-            return raw.view(np.uint64).reshape(-1, 24)
+            return raw.view(np.uint64).reshape(-1, 32)
         if what == "scores":
             return raw.view(np.int32)
         if what == "acc":

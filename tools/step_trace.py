@@ -19,7 +19,7 @@ from paper_2604_02570_b200.layer import DecodeLayer  # noqa: E402
 
 MARKS = ["entry", "griddep", "P1 done", "q count", "qt ready", "attn done", "merged", "barrier",
          "P3 staged", "end", "P3 mma", "attn start", "kv done", "1st merge",
-         "prep0 done", "w0 start", "w7 start", "stage0 in", "x staged", "ring items", "parked items", "ring item 0 out"]
+         "prep0 done", "w0 start", "w7 start", "stage0 in", "x staged", "ring items", "parked items", "ring item 0 out", "flags seen"]
 
 
 def main():
@@ -73,7 +73,7 @@ def main():
             layer.step(x, y, graph=False)
     torch.cuda.synchronize()
     raw = layer.debug_copy("trace").astype(np.int64)
-    t = np.concatenate([raw[:, :10], raw[:, 12:24]], axis=1)
+    t = np.concatenate([raw[:, :10], raw[:, 12:12 + len(MARKS) - 10]], axis=1)
     smid, nu = raw[:, 10], raw[:, 11]
     t0 = t[:, 0].min()
     rel = (t - t0) / 1e3
