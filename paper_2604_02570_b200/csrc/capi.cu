@@ -660,10 +660,13 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     a.xcnt = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 16);
     a.p1gen = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 3);
     a.p1flag = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 256);  // one 128-byte line per CTA
+    a.yflag = a.p1flag + 32 * 160;
     static const int g1 = std::getenv("WSVD_STEP_G1") ? std::atoi(std::getenv("WSVD_STEP_G1")) : 0;
+    static const int g3 = std::getenv("WSVD_STEP_G3") ? std::atoi(std::getenv("WSVD_STEP_G3")) : 0;
     a.g1 = g1;
-    const size_t xob = step_xo_bytes(c->B, L->oKp);
-    if (c->xo.n < xob) CUDA_TRY(c->xo.alloc(xob));  // zeroed: rows past the batch stay 0
+    a.g3 = g3;
+    const size_t xob = 2 * step_xo_bytes(c->B, L->oKp);  // one per layer parity (chained layers overlap)
+    if (c->xo.n < xob) CUDA_TRY(c->xo.alloc(xob));       // zeroed: rows past the batch stay 0
     a.xo = c->xo.as<uint8_t>();
     const size_t wsb = step_ws_bytes(c->sms);
     if (c->fws.n < wsb) CUDA_TRY(c->fws.alloc(wsb));
@@ -681,6 +684,10 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     static const bool no_cluster = getenv("WSVD_STEP_NOCLUSTER") != nullptr;
     if (c->pair_ok < 0) c->pair_ok = step_pair_clusters_ok(c->B, c->sms);
     a.cluster = (!no_cluster && c->pair_ok == 1) ? 2 : 1;
+    // without pairs, two K splits of the O-projection meet in y by red.add onto
+    // zeros each CTA writes after its projection: a y aliasing x needs every
+    // CTA's token consumed first -- the grid barrier
+    if (a.cluster != 2 && L->oKp / L->oks == 2 && a.g1 == 0) a.g1 = 1;
     // L2 prefetch of the first cache stages before the grid-dependency wait, at
     // the host mirror's length (unknown inside a caller's graph capture)
     cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
@@ -1148,8 +1155,8 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     // + 128 KB: the attention rings copy a slot's first stage whole, which may run past the last row
     cudaError_t e = c->data.alloc(rows * c->row_bytes + (128u << 10));
     if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4 + (16u << 10));  // + a stage of scales
-    if (e == cudaSuccess) e = c->ctrl.alloc(1024 + 160 * 128);  // [0] len [1] done [2] step epoch [3] layer steps
-                                    // [4,5] barrier [16..32) x-fetch counters [256 + 32 c] projection flags
+    if (e == cudaSuccess) e = c->ctrl.alloc(1024 + 2 * 160 * 128);  // [0] len [1] done [2] step epoch [3] layer steps
+        // [4,5] barrier [16..32) x-fetch counters [256 + 32 c] projection flags [5376 + 32 c] y flags
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     if (e == cudaSuccess)
         e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh *

@@ -176,7 +176,9 @@ struct StepArgs {
     unsigned* bgen;        // grid-barrier generations completed so far
     unsigned* bar;         // grid barrier count (monotone, wrap-safe compares)
     unsigned* p1flag;      // [grid][32] per CTA (one 128-byte line each): layers whose projection partials it has written
+    unsigned* yflag;       // [grid][32] per CTA: layers whose O-projection outputs (y) it has written
     unsigned* p1gen;       // layer steps run so far (the flags' base)
+    int g3;                // A/B: 1 a grid barrier between chained layers instead of the y flags
     int g1;                // A/B: 1 a grid barrier after the projection instead of the per-CTA
                            // flags; 2 the cache stream starts at this CTA's projection end
     float* P;              // [splits][B][Nrows] projection partials

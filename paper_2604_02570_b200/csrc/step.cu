@@ -35,8 +35,11 @@
 //   P3   folded O-projection y = v~ . (B_V . W_o) over W-tiles prefetched into
 //        shared memory during P2 (run-to-run deterministic: fixed-order sums,
 //        or exactly two red.add addends onto zeros);
-//   G3   (chains only) grid barrier: y is complete -- it is the next layer's
-//        token (pipeline.cpp:318-336 with the attention blocks chained).
+//   flag (chains) per CTA: its share of y is written (a release count).  y is
+//        the next layer's token (pipeline.cpp:318-336, attention blocks
+//        chained): each CTA's next projection waits for exactly the CTAs whose
+//        O-projection tiles cover its K split -- no grid barrier between the
+//        layers (WSVD_STEP_G3=1 restores it for A/B).
 //
 // The producer warps drive two rings: warp 8 the weight ring (P1 items, then
 // the O-projection items, continuing across layers), warp 9 the cache stream.
@@ -376,7 +379,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         int t3lo, nt3, t3step, p3s0, p3ns, np3, per, xoff, p3lo;
         bool ycontig, ysplit, pairy;
     };
-    auto p3geom = [&](int li) {
+    auto p3geom_of = [&](int li, int cta) {
         P3G g;
         g.ycontig = a.y_host != 0 && li == nL - 1;
         g.ysplit = !g.ycontig && osplits == 2;
@@ -407,6 +410,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         g.p3lo = g.xoff - pb;  // first attention-ring byte P3 uses
         return g;
     };
+    auto p3geom = [&](int li) { return p3geom_of(li, cta); };
     // Projection items beyond the 4-slot weight ring are parked in the
     // attention ring (2 per stage, in consumption order): the attention cannot
     // start before grid barrier 1 anyway, and with every item in flight at
@@ -606,7 +610,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         const int slot = ib % C::NB;
                         if (ib < nWS) {
                             mbar_wait(&wdone[slot], lp);  // its parked projection items are consumed
-                            mbar_wait(b1bar, lp);         // and the projection is published
+                            mbar_wait(b1bar, lp);         // and the first segment's producers are seen
                         }
                         mbar_wait(&emptyB[slot], ((par >> slot) & 1u) ^ 1u);
                         par ^= 1u << slot;
@@ -674,6 +678,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         const StepLayer& Ly = a.layer[l];
         const uint32_t lp = static_cast<uint32_t>(l) & 1u;
         const P3G g3 = p3geom(l);
+        // the O-projection rows, one buffer per layer parity: without a grid
+        // barrier between layers, a CTA may merge layer l + 1's rows while
+        // another still stages layer l's (it cannot get two layers ahead: G2)
+        uint8_t* xo_l = a.xo + static_cast<size_t>(lp) * osplits * C::XB2;
         if (l > 0) {
             STEP_MARK(0);
             STEP_MARK(1);
@@ -704,6 +712,28 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             } else if (l == 0 && pj < cps && tid == 0) {
                 // keep the counters' invariant (cps arrivals per fused launch) in device mode
                 asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.xcnt + ps) : "memory");
+            }
+            if (l > 0 && !a.g3 && np1 > 0) {
+                // the token is the previous layer's y: wait for the CTAs whose
+                // O-projection tiles cover this K split's columns (tile T0 + lane;
+                // a tile's producers are its pair's two CTAs, or one CTA)
+                if (warp == 0) {
+                    const P3G gq = p3geom_of(l - 1, 0);
+                    const int t = ps * (kKS / 16) + lane;
+                    if (t < a.otiles) {
+                        int c0 = t % G, c1 = c0;
+                        if (gq.ysplit) {
+                            const int cps3 = G / 2, pj3 = ((t + 1) * cps3 - 1) / a.otiles;
+                            c0 = 2 * pj3;
+                            c1 = 2 * pj3 + 1;
+                        }
+                        const unsigned yt = p1base + static_cast<unsigned>(l);
+                        for (int c = c0; c <= c1; ++c)
+                            while (static_cast<int>(ld_acquire(a.yflag + 32 * c) - yt) < 0) __nanosleep(64);
+                    }
+                    __syncwarp();
+                }
+                named_bar_sync(2, 32 * kNW);
             }
             if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid, (l == 0) ? xin : nullptr);
             named_bar_sync(2, 32 * kNW);
@@ -751,7 +781,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             }
         }
         // helper: the first segment's M_QK column does not depend on the
-        // projection; load it while the barrier drains
+        // projection; load it while the producers publish
         float mq0[R];
         int nseg = 0, pos = 0;
         long long* cut = cut_of(l);
@@ -878,6 +908,15 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             // the next layer's table into the other buffer, while this layer's
             // attention streams (its readers use this layer's buffer)
             if (l + 1 < nL) build_table(l + 1);
+            if (l > 0 && !a.g3 && a.cluster == 2 && (cta & 1)) {
+                // this CTA writes into its even partner's shared memory below
+                // (the merge area): the partner is past layer l - 1's O-projection
+                // (no grid barrier orders the two; in practice long since)
+                if (lane == 0)
+                    while (static_cast<int>(ld_acquire(a.yflag + 32 * (cta - 1)) - (p1base + static_cast<unsigned>(l))) < 0)
+                        __nanosleep(64);
+                __syncwarp();
+            }
             // (b) per segment as the consumers finish it: merge the kNW warp states
             //     in warp order (+ the own token for a region's last segment).  A
             //     region held by one CTA is complete.  A region shared by the two
@@ -979,7 +1018,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 const float vo = a2 / L2;
                 const __nv_bfloat16 vh = __float2bfloat16_rn(vo);
                 const __nv_bfloat16 vl = __float2bfloat16_rn(vo - __bfloat162float(vh));
-                uint8_t* xs = a.xo + static_cast<size_t>(sx) * C::XB2;
+                uint8_t* xs = xo_l + static_cast<size_t>(sx) * C::XB2;
                 const uint32_t eb = static_cast<uint32_t>((kk & 7) * 2);
                 *reinterpret_cast<__nv_bfloat16*>(xs + xrow_off(b, kk >> 3) + eb) = vh;
                 *reinterpret_cast<__nv_bfloat16*>(xs + xrow_off(MT * 16 + b, kk >> 3) + eb) = vl;
@@ -1140,7 +1179,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                             asm volatile("fence.proxy.async.global;" ::: "memory");
                             mbar_arrive_expect_tx(p3bar, static_cast<uint32_t>(g.per * C::XB2));
                             for (int s = s0; s < s0 + g.per; ++s)
-                                tma_bulk_g2s(xsl + (s - s0) * C::XB2, a.xo + static_cast<size_t>(g.p3s0 + s) * C::XB2,
+                                tma_bulk_g2s(xsl + (s - s0) * C::XB2, xo_l + static_cast<size_t>(g.p3s0 + s) * C::XB2,
                                              C::XB2, p3bar);
                         }
                         mbar_wait(p3bar, p3cnt & 1u);
@@ -1150,7 +1189,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         constexpr int V = C::XB2 / 16;  // uint4 per split
                         constexpr int NV = (V + 32 * kNW - 1) / (32 * kNW);
                         for (int s = s0; s < s0 + g.per; ++s) {
-                            const uint4* src = reinterpret_cast<const uint4*>(a.xo + static_cast<size_t>(g.p3s0 + s) * C::XB2);
+                            const uint4* src = reinterpret_cast<const uint4*>(xo_l + static_cast<size_t>(g.p3s0 + s) * C::XB2);
                             uint4* dst = reinterpret_cast<uint4*>(xsl + (s - s0) * C::XB2);
                             uint4 v[NV];
 #pragma unroll
@@ -1277,10 +1316,13 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             // parked items (their generic writes ordered before those TMA writes)
             fence_proxy_async_smem();
             named_bar_sync(2, 32 * kNW);
-            if (tid == 0) mbar_arrive(p3done);
+            if (tid == 0) {
+                mbar_arrive(p3done);
+                red_release(a.yflag + 32 * cta);  // this CTA's share of y is written (release)
+            }
         }
         abase += static_cast<unsigned>(nA1 + g3.np3);
-        if (l + 1 < nL) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // G3: y is the next layer's token
+        if (l + 1 < nL && a.g3) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 3)
     }
     if (cta == 0 && tid == 0) {
         *a.epoch += 1;  // fused launches run (the x-fetch generations)
