@@ -665,6 +665,8 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     static const int g3 = std::getenv("WSVD_STEP_G3") ? std::atoi(std::getenv("WSVD_STEP_G3")) : 0;
     a.g1 = g1;
     a.g3 = g3;
+    static const int short_seg = std::getenv("WSVD_STEP_SHORTSEG") ? std::atoi(std::getenv("WSVD_STEP_SHORTSEG")) : 2048;
+    a.short_seg = short_seg;
     const size_t xob = 2 * step_xo_bytes(c->B, L->oKp);  // one per layer parity (chained layers overlap)
     if (c->xo.n < xob) CUDA_TRY(c->xo.alloc(xob));       // zeroed: rows past the batch stay 0
     a.xo = c->xo.as<uint8_t>();

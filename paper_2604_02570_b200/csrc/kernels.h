@@ -179,6 +179,7 @@ struct StepArgs {
     unsigned* yflag;       // [grid][32] per CTA: layers whose O-projection outputs (y) it has written
     unsigned* p1gen;       // layer steps run so far (the flags' base)
     int g3;                // A/B: 1 a grid barrier between chained layers instead of the y flags
+    int short_seg;         // rows: a first segment shorter than this is processed second (0: never)
     int g1;                // A/B: 1 a grid barrier after the projection instead of the per-CTA
                            // flags; 2 the cache stream starts at this CTA's projection end
     float* P;              // [splits][B][Nrows] projection partials

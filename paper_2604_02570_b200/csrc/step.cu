@@ -178,6 +178,12 @@ WSVD_DEV long long cut_row(int c, int G, long long T, int pos) {
 struct Seg {
     int bh, t0, t1;
 };
+// processing order p -> segment (range order): odd CTAs walk their range
+// backwards (rev); swap01 exchanges the first two
+WSVD_DEV int seg_index(int p, int nseg, bool rev, int swap01) {
+    const int q = (swap01 && p < 2) ? 1 - p : p;
+    return rev ? nseg - 1 - q : q;
+}
 // this CTA's segments, resolved once per layer: region, rows, and the CTAs
 // [c0, c1) whose ranges reach into the region (owners of them hold a part)
 struct SegInfo {
@@ -598,7 +604,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 const size_t cap = static_cast<size_t>(Ly.cap);
                 int ib = 0;  // stage fills of this layer: slot ib % NB
                 for (int p = 0; p < nseg; ++p) {
-                    const SegInfo& sg = sinf[rev ? nseg - 1 - p : p];
+                    const SegInfo& sg = sinf[seg_index(p, nseg, rev, meta_of(li)[2])];
                     for (int t = sg.t0; t < sg.t1; t += kST) {
                         const int rows = min(kST, sg.t1 - t);
                         // every slot's first fill of a layer is a whole stage (finite
@@ -658,6 +664,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         if (lane == 0) {
             meta[0] = pos;
             meta[1] = nseg;
+            // a short first segment would leave the consumers waiting for the
+            // second one's query: process the (whole-region) second one first
+            const int f = rev ? nseg - 1 : 0;
+            meta[2] = (nseg >= 3 && sinf[f].t1 - sinf[f].t0 < a.short_seg) ? 1 : 0;
             if (a.trace && li == a.trace_layer) a.trace[cta * kTr + 11] = static_cast<uint64_t>(nseg);
         }
         __syncwarp();
@@ -790,7 +800,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             nseg = meta_of(l)[1];
             pos = meta_of(l)[0];
             if (nseg > 0) {
-                const int h0 = sinf[rev ? nseg - 1 : 0].bh % a.nh;
+                const int h0 = sinf[seg_index(0, nseg, rev, meta_of(l)[2])].bh % a.nh;
                 const float* mq = Ly.mqk + static_cast<size_t>(h0) * R * R + lane;
 #pragma unroll
                 for (int jj = 0; jj < R; ++jj) mq0[jj] = __ldg(mq + jj * R);
@@ -812,7 +822,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             nseg = meta_of(l)[1];
             pos = meta_of(l)[0];
         }
-        auto seg_of = [&](int p) { return rev ? nseg - 1 - p : p; };
+        const int swap01 = meta_of(l)[2];
+        auto seg_of = [&](int p) { return seg_index(p, nseg, rev, swap01); };
         const size_t cap = static_cast<size_t>(Ly.cap);
 
         if (warp == kHelp) {
