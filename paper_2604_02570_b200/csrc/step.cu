@@ -152,11 +152,13 @@ WSVD_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared:
 // a fire-and-forget release reduction and everyone polls with acquire loads
 // (1.2 us on B200 against 2.0 for a count-and-release barrier,
 // tools/micro_barrier.cu).
-WSVD_DEV void grid_sync(unsigned* bar, unsigned target) {
+WSVD_DEV void grid_sync(unsigned* bar, unsigned target, uint64_t* tr = nullptr) {
     named_bar_sync(1, kSync);
     if (threadIdx.x == 0) {
+        if (tr) tr[25] = gtimer();
         red_release(bar);
         wait_count(bar, target);
+        if (tr) tr[7] = gtimer();
     }
     named_bar_sync(1, kSync);
 }
@@ -1163,8 +1165,9 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             STEP_MARK(5);
         }
         // G2: every (sequence, head) row is merged; every CTA has read the length
-        grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));
-        STEP_MARK(7);
+        // (trace: thread 0's arrival -> mark 25, its exit -> mark 7; a mark
+        // taken after the barrier by every warp reads the timer early)
+        grid_sync(a.bar, (++gen) * static_cast<unsigned>(G), (a.trace && l == a.trace_layer) ? a.trace + cta * kTr : nullptr);
         if (cta == 0 && tid == 0) *Ly.d_len = pos + 1;
 
         if (warp != kHelp) {
@@ -1266,6 +1269,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         }
                         __syncwarp();
                         if (lane == 0) mbar_arrive_remote(cluster_map(smem_u32(ybar), 0u));
+                        if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 26] = gtimer();
                     } else {
                         float own[4][4];  // this CTA's split-0 sums (<= 4 groups per thread at B <= 32, nt3 <= 4)
                         for (int u = 0, i = tid; i < q4; ++u, i += 32 * kNW) {
@@ -1274,7 +1278,9 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
 #pragma unroll
                             for (int e = 0; e < 4; ++e) own[u & 3][e] = psum(ti, n0 + e, m);
                         }
+                        if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 27] = gtimer();
                         mbar_wait_cluster(ybar, ycnt & 1u);
+                        if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 26] = gtimer();
                         for (int u = 0, i = tid; i < q4; ++u, i += 32 * kNW) {
                             const int ti = i / (a.B * 4), r = i - ti * a.B * 4;
                             const int m = r >> 2, n0 = (r & 3) * 4;
@@ -1329,6 +1335,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             named_bar_sync(2, 32 * kNW);
             if (tid == 0) {
                 mbar_arrive(p3done);
+                if (a.trace && l == a.trace_layer) a.trace[cta * kTr + 28] = gtimer();
                 red_release(a.yflag + 32 * cta);  // this CTA's share of y is written (release)
             }
         }
