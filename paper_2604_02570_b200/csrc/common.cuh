@@ -210,6 +210,13 @@ WSVD_DEV void st_cluster_v4(uint32_t addr, float x, float y, float z, float w) {
     asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(x), "f"(y), "f"(z), "f"(w)
                  : "memory");
 }
+// 16 bytes into a peer CTA's shared memory that count as transaction bytes on
+// its mbarrier (no release fence: the barrier's phase completion publishes them)
+WSVD_DEV void st_async_v4(uint32_t addr, float x, float y, float z, float w, uint32_t bar_cluster_addr) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1, %2, %3, %4}, [%5];"
+                 ::"r"(addr), "f"(x), "f"(y), "f"(z), "f"(w), "r"(bar_cluster_addr)
+                 : "memory");
+}
 WSVD_DEV void mbar_arrive_remote(uint32_t bar_cluster_addr) {  // release at cluster scope
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster_addr) : "memory");
 }

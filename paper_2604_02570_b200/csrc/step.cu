@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     uint64_t* pbar = b1bar + 1;           // the pair partner's state landed (DSMEM)
     uint64_t* xin = pbar + 1;             // every consumer warp has requested its token-slice loads
     uint64_t* p3done = xin + 1;           // the layer's O-projection no longer uses the attention ring
-    uint64_t* ybar = p3done + 1;          // pair P3: the odd CTA's split-1 sums landed (DSMEM, kNW arrivals)
+    uint64_t* ybar = p3done + 1;          // pair P3: the odd CTA's split-1 sums landed (DSMEM st.async bytes)
     static_assert((2 * kNA + 2 * C::NB + 2 * kMaxU + 1 + 2 * C::NB + C::NB + 6) * 8 <= 504,
                   "mbarriers overflow their shared-memory region");
 
@@ -452,7 +452,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             mbar_init(xin, kNW);
             *tbuilt = 0;
             mbar_init(p3done, 1);
-            mbar_init(ybar, kNW);
+            mbar_init(ybar, 1);
         }
         fence_mbar_init();  // every lane: the fence covers the executing thread's inits
     }
@@ -1241,10 +1241,12 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                                     pj3[n * MT * 16 + m] = facc[mt][hh][i] + facc[mt + MT][hh][i];
                                 }
                     }
+                    if (a.trace && l == a.trace_layer && (tid & 31) == 0) a.trace[cta * kTr + 29 + (warp < 4 ? 0 : 1)] = gtimer();
                     named_bar_sync(2, 32 * kNW);  // the X buffer is free again / every partial is written
                 }
                 // the weight ring's P3 slots are free (both halves have run)
                 if (tid < g.np3) mbar_arrive(&emptyA[(a3 + static_cast<unsigned>(tid)) % kNA]);
+                if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 31] = gtimer();
                 STEP_MARK(12);
                 // part[(half * kNA + j)] -> sum over halves, then splits
                 auto psum = [&](int ti, int n, int m) {
@@ -1255,40 +1257,53 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     }
                     return v;
                 };
+                // one K split per CTA (pairs): the same sum, straight-line
+                auto psum1 = [&](int ti, int n, int m) {
+                    return part[(ti * 16 + n) * MT * 16 + m] + part[((kNA + ti) * 16 + n) * MT * 16 + m];
+                };
                 if (g.pairy) {
                     // [tile][row m][16 columns] fp32 split-1 sums, in the even CTA's merge area
                     float* recv = reinterpret_cast<float*>(smem + C::RED_OFF + (C::PART_IN_RED ? C::PARTB : 0));
                     const int q4 = g.nt3 * a.B * 4;  // 4-column groups
                     if (cta & 1) {
-                        const uint32_t dst = cluster_map(smem_u32(recv), 0u);
+                        // st.async: every 16 bytes complete transaction bytes on the even
+                        // CTA's barrier (which expects q4 * 16) -- no release fence
+                        const uint32_t dst = cluster_map(smem_u32(recv), 0u), rbar = cluster_map(smem_u32(ybar), 0u);
                         for (int i = tid; i < q4; i += 32 * kNW) {
                             const int ti = i / (a.B * 4), r = i - ti * a.B * 4;
                             const int m = r >> 2, n0 = (r & 3) * 4;
-                            st_cluster_v4(dst + 4u * static_cast<uint32_t>((ti * a.B + m) * 16 + n0), psum(ti, n0, m),
-                                          psum(ti, n0 + 1, m), psum(ti, n0 + 2, m), psum(ti, n0 + 3, m));
+                            st_async_v4(dst + 4u * static_cast<uint32_t>((ti * a.B + m) * 16 + n0), psum1(ti, n0, m),
+                                        psum1(ti, n0 + 1, m), psum1(ti, n0 + 2, m), psum1(ti, n0 + 3, m), rbar);
                         }
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_remote(cluster_map(smem_u32(ybar), 0u));
                         if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 26] = gtimer();
                     } else {
-                        float own[4][4];  // this CTA's split-0 sums (<= 4 groups per thread at B <= 32, nt3 <= 4)
-                        for (int u = 0, i = tid; i < q4; ++u, i += 32 * kNW) {
+                        // this CTA's split-0 sums: <= 4 groups per thread (B <= 32, nt3 <= 4),
+                        // in registers (unrolled: a dynamic index would put them in local memory)
+                        float own[4][4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = tid + u * 32 * kNW;
+                            if (i >= q4) break;
                             const int ti = i / (a.B * 4), r = i - ti * a.B * 4;
                             const int m = r >> 2, n0 = (r & 3) * 4;
 #pragma unroll
-                            for (int e = 0; e < 4; ++e) own[u & 3][e] = psum(ti, n0 + e, m);
+                            for (int e = 0; e < 4; ++e) own[u][e] = psum1(ti, n0 + e, m);
                         }
                         if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 27] = gtimer();
+                        if (tid == 0) mbar_arrive_expect_tx(ybar, static_cast<uint32_t>(q4) * 16u);
                         mbar_wait_cluster(ybar, ycnt & 1u);
                         if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 26] = gtimer();
-                        for (int u = 0, i = tid; i < q4; ++u, i += 32 * kNW) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int i = tid + u * 32 * kNW;
+                            if (i >= q4) break;
                             const int ti = i / (a.B * 4), r = i - ti * a.B * 4;
                             const int m = r >> 2, n0 = (r & 3) * 4;
                             const int col = (g.t3lo + ti) * 16 + n0;
                             const float4 o = *reinterpret_cast<const float4*>(recv + (ti * a.B + m) * 16 + n0);
                             float* yr = Ly.y + static_cast<size_t>(m) * a.e_out;
-                            const float v0 = own[u & 3][0] + o.x, v1 = own[u & 3][1] + o.y;
-                            const float v2 = own[u & 3][2] + o.z, v3 = own[u & 3][3] + o.w;
+                            const float v0 = own[u][0] + o.x, v1 = own[u][1] + o.y;
+                            const float v2 = own[u][2] + o.z, v3 = own[u][3] + o.w;
                             if (col + 4 <= a.e_out && (a.e_out & 3) == 0) {
                                 *reinterpret_cast<float4*>(yr + col) = make_float4(v0, v1, v2, v3);
                             } else {
