@@ -243,6 +243,7 @@ struct wsvd_cache_s {
     DevBuf x_dev, y_dev;              // staging for the host-buffer step
     DevBuf trace;                     // fused-step phase timeline (WSVD_STEP_TRACE)
     DevBuf xo;                        // fused step: bf16 X rows of the O-projection
+    DevBuf Pt;                        // fused step: tagged projection partials
     DevBuf fws;                       // fused step: per-CTA segment states
     DevBuf pP, pxo, pws;              // two-group chain (step2.cu): partials, O-proj rows, segment states
     DevBuf dbg;                       // test hook: int8 score accumulators [B*nh][cap_alloc][2]
@@ -642,8 +643,6 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     }
     a.nlayers = n;
     const int splits = L->Kp / L->ks;
-    const size_t need = static_cast<size_t>(splits) * c->B * L->Nrows * 4;
-    if (c->P.n < need) CUDA_TRY(c->P.alloc(need));
     a.x = x;
     a.x_host = x_host ? 1 : 0;
     a.y_host = y_host ? 1 : 0;
@@ -652,15 +651,16 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
         if (c->x_dev.n < xb) CUDA_TRY(c->x_dev.alloc(xb));
         a.xd = c->x_dev.as<float>();
     }
-    a.P = c->P.as<float>();
+    const size_t needt = static_cast<size_t>(splits) * c->B * L->Nrows * 8;
+    if (c->Pt.n < needt) CUDA_TRY(c->Pt.alloc(needt));  // zeroed: tag 0 is never a layer step's
+    a.Pt = c->Pt.as<unsigned long long>();
     // ctrl: [0] len [1] done [2] fused launches [4] grid barrier [5] barrier generations [16..32) x-fetch counters
     a.bar = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 4);
     a.bgen = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 5);
     a.epoch = c->ctrl.as<int>() + 2;
     a.xcnt = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 16);
     a.p1gen = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 3);
-    a.p1flag = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 256);  // one 128-byte line per CTA
-    a.yflag = a.p1flag + 32 * 160;
+    a.yflag = reinterpret_cast<unsigned*>(c->ctrl.as<int>() + 256);  // one 128-byte line per CTA
     static const int g1 = std::getenv("WSVD_STEP_G1") ? std::atoi(std::getenv("WSVD_STEP_G1")) : 0;
     static const int g3 = std::getenv("WSVD_STEP_G3") ? std::atoi(std::getenv("WSVD_STEP_G3")) : 0;
     a.g1 = g1;
@@ -713,8 +713,7 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     int rc = fused_serialize(L->d.device, s);
     if (rc) return rc;
     CUDA_TRY(launch_layer_step(a, s));
-    c->P_M = c->B;
-    c->P_splits = splits;
+    c->P_M = 0;  // (the fused step's partials are tagged, in Pt: nothing for debug_copy)
     return WSVD_OK;
 }
 
@@ -1157,8 +1156,8 @@ int wsvd_cache_create(wsvd_layer_t L, int32_t batch, int32_t capacity, int32_t c
     // + 128 KB: the attention rings copy a slot's first stage whole, which may run past the last row
     cudaError_t e = c->data.alloc(rows * c->row_bytes + (128u << 10));
     if (e == cudaSuccess && cache_dtype == WSVD_I8) e = c->scales.alloc(rows * 4 + (16u << 10));  // + a stage of scales
-    if (e == cudaSuccess) e = c->ctrl.alloc(1024 + 2 * 160 * 128);  // [0] len [1] done [2] step epoch [3] layer steps
-        // [4,5] barrier [16..32) x-fetch counters [256 + 32 c] projection flags [5376 + 32 c] y flags
+    if (e == cudaSuccess) e = c->ctrl.alloc(1024 + 160 * 128);  // [0] len [1] done [2] step epoch [3] layer steps
+        // [4,5] barrier [16..32) x-fetch counters [256 + 32 c] y flags
     if (e == cudaSuccess) e = c->qt.alloc(static_cast<size_t>(batch) * nh * L->R * 4);
     if (e == cudaSuccess)
         e = c->attn_ws.alloc(static_cast<size_t>(batch) * nh *

@@ -175,14 +175,13 @@ struct StepArgs {
     int* epoch;            // fused launches run so far (x-fetch counter generations)
     unsigned* bgen;        // grid-barrier generations completed so far
     unsigned* bar;         // grid barrier count (monotone, wrap-safe compares)
-    unsigned* p1flag;      // [grid][32] per CTA (one 128-byte line each): layers whose projection partials it has written
     unsigned* yflag;       // [grid][32] per CTA: layers whose O-projection outputs (y) it has written
     unsigned* p1gen;       // layer steps run so far (the flags' base)
     int g3;                // A/B: 1 a grid barrier between chained layers instead of the y flags
     int short_seg;         // rows: a first segment shorter than this is processed second (0: never)
     int g1;                // A/B: 1 a grid barrier after the projection instead of the per-CTA
                            // flags; 2 the cache stream starts at this CTA's projection end
-    float* P;              // [splits][B][Nrows] projection partials
+    unsigned long long* Pt;  // [splits][B][Nrows] projection partials, each (layer-step tag << 32 | fp32 bits)
     float* ws;             // [grid][kMaxU][36] segment states (step_ws_bytes)
     uint8_t* xo;           // [osplits][2][MT*16][1024] bf16 hi / lo X rows of the O-projection (swizzled)
     uint64_t* trace;       // [grid][24] %globaltimer at the phase marks of layer trace_layer, or null

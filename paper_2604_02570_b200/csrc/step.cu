@@ -127,6 +127,18 @@ WSVD_DEV unsigned ld_acquire(const unsigned* p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// a projection partial and the layer step that wrote it, as one 64-bit word:
+// single-copy atomic, so a reader that sees the step's tag sees its value
+// (no release / flag round trips between the projection and its readers)
+WSVD_DEV void st_tagged(unsigned long long* p, float v, unsigned tag) {
+    const unsigned long long w = (static_cast<unsigned long long>(tag) << 32) | __float_as_uint(v);
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(w) : "memory");
+}
+WSVD_DEV unsigned long long ld_tagged(const unsigned long long* p) {
+    unsigned long long w;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(w) : "l"(p) : "memory");
+    return w;
+}
 WSVD_DEV void red_release(unsigned* p) {
     asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p) : "memory");
 }
@@ -755,7 +767,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             // parity wait never sees an older phase), warps 4-7 the parked ones
             auto emit = [&](int k, const float (&facc)[MT][2][4]) {
                 const int tile = plo + k;
-                float* P = a.P + static_cast<size_t>(ps) * pstride;
+                unsigned long long* P = a.Pt + static_cast<size_t>(ps) * pstride;
+                const unsigned tag = p1base + static_cast<unsigned>(l) + 1u;
 #pragma unroll
                 for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
@@ -764,7 +777,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         for (int i = 0; i < 4; ++i) {
                             const int n = tile * 16 + g8 + ((i & 2) ? 8 : 0);
                             const int m = mt * 16 + hh * 8 + 2 * t4 + (i & 1);
-                            if (m < a.B) P[static_cast<size_t>(m) * a.Nrows + n] = facc[mt][hh][i];
+                            if (m < a.B) st_tagged(P + static_cast<size_t>(m) * a.Nrows + n, facc[mt][hh][i], tag);
                         }
             };
             if (warp < kNA) {
@@ -792,32 +805,18 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 STEP_MARK(22);  // the parked items are done
             }
         }
-        // helper: the first segment's M_QK column does not depend on the
-        // projection; load it while the producers publish
-        float mq0[R];
         int nseg = 0, pos = 0;
         long long* cut = cut_of(l);
         const SegInfo* sinf = sinf_of(l);
-        if (warp == kHelp) {
-            nseg = meta_of(l)[1];
-            pos = meta_of(l)[0];
-            if (nseg > 0) {
-                const int h0 = sinf[seg_index(0, nseg, rev, meta_of(l)[2])].bh % a.nh;
-                const float* mq = Ly.mqk + static_cast<size_t>(h0) * R * R + lane;
-#pragma unroll
-                for (int jj = 0; jj < R; ++jj) mq0[jj] = __ldg(mq + jj * R);
-            }
-        }
         named_bar_sync(1, kSync);
         STEP_MARK(2);  // every projection warp of this CTA is done
-        // this CTA's projection partials are written: publish them (release;
-        // the helpers that attend a head wait for exactly its producers -- no
-        // grid barrier between the projection and the attention)
-        if (tid == 0) red_release(a.p1flag + 32 * cta);
+        // (the projection partials carry their layer step's tag: readers
+        // validate each word -- no grid barrier between the projection and
+        // the attention)
         if (a.g1 == 1) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 1)
         if (tid == 0 && a.g1 != 0) mbar_arrive(b1bar);
         STEP_MARK(3);
-        if (warp < kNW) {
+        if (warp < kNW || warp == kHelp) {
             while (*tbuilt < l + 1) {  // (built before P1 ended: passes at once)
             }
             __threadfence_block();
@@ -843,24 +842,59 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             //     gets the step's own K / V latents (summed the same way, rounded to
             //     the cache's bf16 -- the row the reference appends before
             //     attending, decode.cpp:143-149), written to cache row pos
-            auto prep = [&](int p, const float (&mqv)[R]) {
+            const unsigned p1t = p1base + static_cast<unsigned>(l) + 1u;  // this layer step's tag
+            auto prep = [&](int p) {
                 const int j = seg_of(p);
                 const SegInfo& s = sinf[j];
                 const int b = s.bh / a.nh, h = s.bh - b * a.nh;
                 const bool own = s.t1 == pos;
-                const float* pb = a.P + static_cast<size_t>(b) * a.Nrows + static_cast<size_t>(h) * 3 * R + lane;
-                float pv[3][kMaxSplits];
+                // M_QK's column (independent of the projection: in flight with the
+                // partials' loads)
+                float mqv[R];
+                const float* mq = Ly.mqk + static_cast<size_t>(h) * R * R + lane;
 #pragma unroll
-                for (int sp = 0; sp < kMaxSplits; ++sp) {
-                    pv[0][sp] = sp < splits ? __ldcg(pb + sp * pstride) : 0.f;
-                    pv[1][sp] = (own && sp < splits) ? __ldcg(pb + sp * pstride + R) : 0.f;
-                    pv[2][sp] = (own && sp < splits) ? __ldcg(pb + sp * pstride + 2 * R) : 0.f;
-                }
+                for (int jj = 0; jj < R; ++jj) mqv[jj] = __ldg(mq + jj * R);
+                // every K split's partial of head h's rows, each word validated by
+                // its tag (written by this layer step: re-read the stale ones)
+                const unsigned long long* pb = a.Pt + static_cast<size_t>(b) * a.Nrows + static_cast<size_t>(h) * 3 * R + lane;
+                const unsigned long long fresh = static_cast<unsigned long long>(p1t) << 32;  // a +0.0 of this step
+                constexpr int SB = kMaxSplits / 2;  // splits per batch (8: E <= 4096 needs one)
                 float v[3] = {0.f, 0.f, 0.f};
+                for (int s0 = 0; s0 < splits; s0 += SB) {
+                    unsigned long long w[3][SB];
 #pragma unroll
-                for (int sp = 0; sp < kMaxSplits; ++sp)
+                    for (int q = 0; q < SB; ++q)
 #pragma unroll
-                    for (int r = 0; r < 3; ++r) v[r] += pv[r][sp];  // zeros past `splits` leave the sum exact
+                        for (int r = 0; r < 3; ++r)
+                            w[r][q] = (s0 + q < splits && (r == 0 || own)) ? ld_tagged(pb + (s0 + q) * pstride + r * R)
+                                                                         : fresh;
+                    for (;;) {
+                        bool ok = true;
+#pragma unroll
+                        for (int q = 0; q < SB; ++q)
+#pragma unroll
+                            for (int r = 0; r < 3; ++r) ok = ok && static_cast<unsigned>(w[r][q] >> 32) == p1t;
+                        if (__all_sync(0xffffffffu, ok)) break;
+                        __nanosleep(32);
+#pragma unroll
+                        for (int q = 0; q < SB; ++q)
+#pragma unroll
+                            for (int r = 0; r < 3; ++r)
+                                if (static_cast<unsigned>(w[r][q] >> 32) != p1t) w[r][q] = ld_tagged(pb + (s0 + q) * pstride + r * R);
+                    }
+#pragma unroll
+                    for (int q = 0; q < SB; ++q)
+#pragma unroll
+                        for (int r = 0; r < 3; ++r)  // +0.0 past `splits` leaves the sum exact
+                            v[r] += __uint_as_float(static_cast<unsigned>(w[r][q]));
+                }
+                if (p == 0) {
+                    // the cache stream into the stages that held parked items starts
+                    // once the first segment's partials are complete: its burst then
+                    // does not queue ahead of the projection loads of CTAs still in P1
+                    if (a.g1 == 0 && lane == 0) mbar_arrive(b1bar);
+                    if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 24] = gtimer();
+                }
                 float qt = 0.f;
 #pragma unroll
                 for (int jj = 0; jj < R; ++jj) qt = fmaf(__shfl_sync(0xffffffffu, v[0], jj), mqv[jj], qt);
@@ -878,45 +912,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&uready[j]);
             };
-            // the projection partials of head h come from the CTAs whose tile runs
-            // cover its rows [3Rh, 3R(h+1)) in every K split: wait for their flags
-            // (one acquire per producer, the lanes in parallel)
-            const unsigned p1t = p1base + static_cast<unsigned>(l) + 1u;
-            auto wait_heads = [&](int p0, int p1) {
-                int i = lane;  // this lane's flattened (segment, producer) index
-                for (int p = p0; p < p1; ++p) {
-                    const int h = sinf[seg_of(p)].bh % a.nh;
-                    const int t0 = h * 3 * R / 16, t1 = ((h + 1) * 3 * R - 1) / 16;
-                    const int j0 = ((t0 + 1) * cps - 1) / ptiles, j1 = ((t1 + 1) * cps - 1) / ptiles;
-                    const int n = (j1 - j0 + 1) * splits;
-                    for (; i < n; i += 32) {
-                        const unsigned* f = a.p1flag + 32 * ((j0 + i / splits) * splits + i % splits);
-                        while (static_cast<int>(ld_acquire(f) - p1t) < 0) __nanosleep(64);
-                    }
-                    i -= n;
-                }
-                __syncwarp();  // (orders the lanes' acquires before every lane's loads)
-            };
-            if (nseg > 0) wait_heads(0, 1);
-            // the cache stream into the stages that held parked items starts once
-            // the first segment's producers are seen: its burst then does not
-            // queue ahead of the projection loads of CTAs still in P1 (measured:
-            // 0.3 us per layer better than starting it at this CTA's own P1 end)
-            if (a.g1 == 0 && lane == 0) mbar_arrive(b1bar);
-            if (nseg > 0) {
-                if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 24] = gtimer();
-                prep(0, mq0);
-                wait_heads(1, nseg);
-            }
+            if (nseg > 0) prep(0);
+            else if (a.g1 == 0 && lane == 0) mbar_arrive(b1bar);
             if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 16] = gtimer();
-            for (int p = 1; p < nseg; ++p) {
-                const int h = sinf[seg_of(p)].bh % a.nh;
-                float mqv[R];
-                const float* mq = Ly.mqk + static_cast<size_t>(h) * R * R + lane;
-#pragma unroll
-                for (int jj = 0; jj < R; ++jj) mqv[jj] = __ldg(mq + jj * R);
-                prep(p, mqv);
-            }
+            for (int p = 1; p < nseg; ++p) prep(p);
             if (nseg > 0) STEP_MARK(4);
             // the next layer's table into the other buffer, while this layer's
             // attention streams (its readers use this layer's buffer)
@@ -1225,10 +1224,12 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         const int slot = static_cast<int>(ia % kNA), s = j % g.p3ns;
                         if (slot != hslot || s < s0 || s >= s0 + g.per) continue;
                         mbar_wait(&fullA[slot], (ia / kNA) & 1u);
+                        if (a.trace && l == a.trace_layer && tid == 0 && j == 0) a.trace[cta * kTr + 12] = gtimer();
                         // token columns 0..MT*16-1 are the hi rows, MT*16.. the lo rows
                         float facc[2 * MT][2][4];
                         item_mma<2 * MT>(smem_u32(ringA + slot * kItem), smem_u32(xsl + (s - s0) * C::XB2), lane, facc,
                                          half * kKS / 64, (half + 1) * kKS / 64);
+                        if (a.trace && l == a.trace_layer && tid == 0 && j == 0) a.trace[cta * kTr + 14] = gtimer();
                         float* pj3 = part + (half * kNA + j) * 16 * MT * 16;
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt)
@@ -1247,7 +1248,6 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 // the weight ring's P3 slots are free (both halves have run)
                 if (tid < g.np3) mbar_arrive(&emptyA[(a3 + static_cast<unsigned>(tid)) % kNA]);
                 if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 31] = gtimer();
-                STEP_MARK(12);
                 // part[(half * kNA + j)] -> sum over halves, then splits
                 auto psum = [&](int ti, int n, int m) {
                     float v = 0.f;
