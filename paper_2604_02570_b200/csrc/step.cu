@@ -8,12 +8,12 @@
 // This kernel runs the same arithmetic with one CTA per SM.  Per layer:
 //
 //   P1   latent projection P[split][b][n] = x_b . A[:, n] over one K split
-//        (swap-AB mma.sync over W-tiles streamed by TMA, as gemm.cu);
-//   flag per CTA: its projection partials are written (a release count; no
-//        grid barrier -- the helper that prepares a head's query waits for the
-//        flags of exactly the CTAs that produce that head's rows, all splits;
-//        WSVD_STEP_G1=1 restores the grid barrier for A/B: 1.6-1.9 us per
-//        layer slower, profiles/r02_step_ab.txt);
+//        (swap-AB mma.sync over W-tiles streamed by TMA, as gemm.cu); every
+//        partial is stored with its layer step's tag in one 64-bit word, and
+//        the helper that prepares a head's query re-reads any word whose tag
+//        is stale -- no grid barrier, release or flag between the projection
+//        and the attention (WSVD_STEP_G1=1 restores a grid barrier for A/B:
+//        ~2 us per layer slower, profiles/r02_step_ab.txt);
 //   P2   attention over the cached rows 0 .. pos-1: the B*nh*pos rows of all
 //        (sequence, head) regions are cut into G equal contiguous ranges (at
 //        32-row boundaries), one per CTA, so every SM streams the same bytes.

@@ -19,7 +19,7 @@ from paper_2604_02570_b200.layer import DecodeLayer  # noqa: E402
 
 MARKS = ["entry", "griddep", "P1 done", "q count", "qt ready", "attn done", "merged", "G2 exit",
          "P3 staged", "end", "P3 item0 in", "attn start", "P3 item0 mma", "1st merge",
-         "prep0 done", "w0 start", "w7 start", "stage0 in", "x staged", "ring items", "parked items", "ring item 0 out", "flags seen", "G2 arrive", "P3 y sent/recv", "P3 own psum", "P3 done", "P3 w0-3 items", "P3 w4-7 items", "P3 bar (tid0)"]
+         "prep0 done", "w0 start", "w7 start", "stage0 in", "x staged", "ring items", "parked items", "ring item 0 out", "P0 valid", "G2 arrive", "P3 y sent/recv", "P3 own psum", "P3 done", "P3 w0-3 items", "P3 w4-7 items", "P3 bar (tid0)"]
 
 
 def main():
