@@ -244,6 +244,7 @@ struct wsvd_cache_s {
     DevBuf trace;                     // fused-step phase timeline (WSVD_STEP_TRACE)
     DevBuf xo;                        // fused step: bf16 X rows of the O-projection
     DevBuf Pt;                        // fused step: tagged projection partials
+    DevBuf xtag;                      // fused chain: tagged bf16 tokens between layers
     DevBuf fws;                       // fused step: per-CTA segment states
     DevBuf pP, pxo, pws;              // two-group chain (step2.cu): partials, O-proj rows, segment states
     DevBuf dbg;                       // test hook: int8 score accumulators [B*nh][cap_alloc][2]
@@ -690,6 +691,15 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     // zeros each CTA writes after its projection: a y aliasing x needs every
     // CTA's token consumed first -- the grid barrier
     if (a.cluster != 2 && L->oKp / L->oks == 2 && a.g1 == 0) a.g1 = 1;
+    // chained layers with pair O-projections: the next layer's token also as
+    // tagged bf16 pairs (its projection validates each word: no flag round trip)
+    static const bool no_xtag = getenv("WSVD_STEP_NOXTAG") != nullptr;  // A/B switch
+    a.xtagged = (!no_xtag && n > 1 && a.cluster == 2 && L->oKp / L->oks == 2 && a.E % L->ks == 0 && a.g3 == 0) ? 1 : 0;
+    if (a.xtagged) {
+        const size_t xtb = 2 * static_cast<size_t>(c->B) * a.E / 2 * 8;
+        if (c->xtag.n < xtb) CUDA_TRY(c->xtag.alloc(xtb));
+        a.xtag = c->xtag.as<unsigned long long>();
+    }
     // L2 prefetch of the first cache stages before the grid-dependency wait, at
     // the host mirror's length (unknown inside a caller's graph capture)
     cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;

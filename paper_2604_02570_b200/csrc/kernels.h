@@ -176,6 +176,8 @@ struct StepArgs {
     unsigned* bgen;        // grid-barrier generations completed so far
     unsigned* bar;         // grid barrier count (monotone, wrap-safe compares)
     unsigned* yflag;       // [grid][32] per CTA: layers whose O-projection outputs (y) it has written
+    unsigned long long* xtag;  // [2][B][E/2] chained tokens (layer parity): bf16 pairs | layer-step tag << 32
+    int xtagged;           // 1: pair O-projections also write xtag; the next projection stages from it
     unsigned* p1gen;       // layer steps run so far (the flags' base)
     int g3;                // A/B: 1 a grid barrier between chained layers instead of the y flags
     int short_seg;         // rows: a first segment shorter than this is processed second (0: never)

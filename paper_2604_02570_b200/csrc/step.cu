@@ -706,6 +706,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         // barrier between layers, a CTA may merge layer l + 1's rows while
         // another still stages layer l's (it cannot get two layers ahead: G2)
         uint8_t* xo_l = a.xo + static_cast<size_t>(lp) * osplits * C::XB2;
+        const bool xt_out = a.xtagged && g3.pairy && l + 1 < nL;  // this layer's y also as tagged bf16 pairs
         if (l > 0) {
             STEP_MARK(0);
             STEP_MARK(1);
@@ -737,7 +738,48 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 // keep the counters' invariant (cps arrivals per fused launch) in device mode
                 asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(a.xcnt + ps) : "memory");
             }
-            if (l > 0 && !a.g3 && np1 > 0) {
+            const bool xt_in = l > 0 && a.xtagged && p3geom(l - 1).pairy;
+            if (xt_in && np1 > 0) {
+                // the token is the previous layer's y as tagged bf16 pairs: every
+                // 16-byte unit of the slice from 4 words, each re-read until it
+                // carries the previous layer step's tag (no flag round trip)
+                const unsigned long long* xs = a.xtag + static_cast<size_t>((l - 1) & 1) * a.B * (a.E / 2);
+                const unsigned want = p1base + static_cast<unsigned>(l);
+                constexpr int PER = kKS / 8, NIT = MT * 16 * PER / (32 * kNW);
+                unsigned long long w[NIT][4];
+#pragma unroll
+                for (int u = 0; u < NIT; ++u) {
+                    const int i = tid + u * 32 * kNW, m = i / PER, kk = (i - m * PER) * 8;
+                    const unsigned long long* src = xs + static_cast<size_t>(m) * (a.E / 2) + (ps * kKS + kk) / 2;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        w[u][q] = m < a.B ? ld_tagged(src + q) : (static_cast<unsigned long long>(want) << 32);
+                }
+                for (;;) {
+                    bool ok = true;
+#pragma unroll
+                    for (int u = 0; u < NIT; ++u)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) ok = ok && static_cast<unsigned>(w[u][q] >> 32) == want;
+                    if (ok) break;
+                    __nanosleep(32);
+#pragma unroll
+                    for (int u = 0; u < NIT; ++u) {
+                        const int i = tid + u * 32 * kNW, m = i / PER, kk = (i - m * PER) * 8;
+                        const unsigned long long* src = xs + static_cast<size_t>(m) * (a.E / 2) + (ps * kKS + kk) / 2;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (static_cast<unsigned>(w[u][q] >> 32) != want) w[u][q] = ld_tagged(src + q);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < NIT; ++u) {
+                    const int i = tid + u * 32 * kNW, m = i / PER, kk = (i - m * PER) * 8;
+                    *reinterpret_cast<uint4*>(xbuf + xrow_off(m, kk / 8)) =
+                        make_uint4(static_cast<unsigned>(w[u][0]), static_cast<unsigned>(w[u][1]),
+                                   static_cast<unsigned>(w[u][2]), static_cast<unsigned>(w[u][3]));
+                }
+            } else if (l > 0 && !a.g3 && np1 > 0) {
                 // the token is the previous layer's y: wait for the CTAs whose
                 // O-projection tiles cover this K split's columns (tile T0 + lane;
                 // a tile's producers are its pair's two CTAs, or one CTA)
@@ -759,7 +801,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 }
                 named_bar_sync(2, 32 * kNW);
             }
-            if (np1 > 0) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid, (l == 0) ? xin : nullptr);
+            if (np1 > 0 && !xt_in) stage_rows<MT>(xsrc, a.B, a.E, a.E, ps * kKS, xbuf, tid, (l == 0) ? xin : nullptr);
             named_bar_sync(2, 32 * kNW);
             STEP_MARK(20);  // the token slice is staged
             // warps 0-3 take the weight-ring items (ring item i on warp i % 4:
@@ -1304,6 +1346,13 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                             float* yr = Ly.y + static_cast<size_t>(m) * a.e_out;
                             const float v0 = own[u][0] + o.x, v1 = own[u][1] + o.y;
                             const float v2 = own[u][2] + o.z, v3 = own[u][3] + o.w;
+                            if (xt_out) {  // (e_out == E, a multiple of 512: whole groups)
+                                unsigned long long* xd = a.xtag + static_cast<size_t>(l & 1) * a.B * (a.E / 2) +
+                                                         static_cast<size_t>(m) * (a.E / 2) + col / 2;
+                                const unsigned long long tg = static_cast<unsigned long long>(p1base + static_cast<unsigned>(l) + 1u) << 32;
+                                const unsigned long long w0 = tg | pack_bf16x2(v0, v1), w1 = tg | pack_bf16x2(v2, v3);
+                                asm volatile("st.relaxed.gpu.global.v2.b64 [%0], {%1, %2};" ::"l"(xd), "l"(w0), "l"(w1) : "memory");
+                            }
                             if (col + 4 <= a.e_out && (a.e_out & 3) == 0) {
                                 *reinterpret_cast<float4*>(yr + col) = make_float4(v0, v1, v2, v3);
                             } else {
@@ -1351,8 +1400,13 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             if (tid == 0) {
                 mbar_arrive(p3done);
                 if (a.trace && l == a.trace_layer) a.trace[cta * kTr + 28] = gtimer();
-                red_release(a.yflag + 32 * cta);  // this CTA's share of y is written (release)
+                // this CTA's share of y is written (release; with tagged tokens the
+                // helper releases it, off the next projection's path)
+                if (!a.xtagged) red_release(a.yflag + 32 * cta);
             }
+        } else if (a.xtagged) {
+            mbar_wait(p3done, lp);  // (this CTA's O-projection is done)
+            if (lane == 0) red_release(a.yflag + 32 * cta);
         }
         abase += static_cast<unsigned>(nA1 + g3.np3);
         if (l + 1 < nL && a.g3) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 3)
