@@ -698,6 +698,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     unsigned pcnt = 0;  // helper: pair-partner states received (pbar phases)
     unsigned p3cnt = 0; // consumers: TMA-staged P3 rounds (p3bar phases)
     unsigned ycnt = 0;  // consumers: pair P3 rounds (ybar phases)
+    uint32_t upar = 0;  // consumers: per segment slot, parity of the uready phases consumed
+    uint32_t spar = 0;  // helper: per segment slot, parity of the sfull phases consumed
     for (l = 0; l < nL; ++l) {
         const StepLayer& Ly = a.layer[l];
         const uint32_t lp = static_cast<uint32_t>(l) & 1u;
@@ -856,7 +858,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         // validate each word -- no grid barrier between the projection and
         // the attention)
         if (a.g1 == 1) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 1)
-        if (tid == 0 && a.g1 != 0) mbar_arrive(b1bar);
+        if (tid == 0 && a.g1 != 0 && nWS > 0) mbar_arrive(b1bar);
         STEP_MARK(3);
         if (warp < kNW || warp == kHelp) {
             while (*tbuilt < l + 1) {  // (built before P1 ended: passes at once)
@@ -871,13 +873,6 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
 
         if (warp == kHelp) {
             // ============================================================ helper warp
-            // segment slots this layer does not use complete their phases anyway
-            // (every segment barrier turns over exactly once per layer)
-            if (lane == 0)
-                for (int j = nseg; j < kMaxU; ++j) {
-                    mbar_arrive(&uready[j]);
-                    mbar_arrive_n(&sfull[j], kNW);
-                }
             // (a) per segment, in processing order, ahead of the consumers:
             //     qt = (sum_split c_Q) . M_QK (the append epilogue's order: fixed
             //     split order, sequential fma); the segment that ends a region also
@@ -934,7 +929,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     // the cache stream into the stages that held parked items starts
                     // once the first segment's partials are complete: its burst then
                     // does not queue ahead of the projection loads of CTAs still in P1
-                    if (a.g1 == 0 && lane == 0) mbar_arrive(b1bar);
+                    if (a.g1 == 0 && nWS > 0 && lane == 0) mbar_arrive(b1bar);  // (waited only with parked stages)
                     if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 24] = gtimer();
                 }
                 float qt = 0.f;
@@ -955,7 +950,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 if (lane == 0) mbar_arrive(&uready[j]);
             };
             if (nseg > 0) prep(0);
-            else if (a.g1 == 0 && lane == 0) mbar_arrive(b1bar);
+            else if (a.g1 == 0 && nWS > 0 && lane == 0) mbar_arrive(b1bar);
             if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 16] = gtimer();
             for (int p = 1; p < nseg; ++p) prep(p);
             if (nseg > 0) STEP_MARK(4);
@@ -981,7 +976,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             //     (SoftmaxState::merge, decode.cpp:59-75) -- nobody waits.
             for (int p = 0; p < nseg; ++p) {
                 const int j = seg_of(p);
-                mbar_wait(&sfull[j], lp);
+                mbar_wait(&sfull[j], (spar >> j) & 1u);
+                spar ^= 1u << j;
                 if (p == 0) STEP_MARK(15);
                 const SegInfo& s = sinf[j];
                 const float* rb = wst + j * kNW * (R + 2);
@@ -1096,7 +1092,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 const SegInfo& s = sinf[j];
                 const int ntok = s.t1 - s.t0;
                 const int ns = (ntok + kST - 1) / kST;
-                mbar_wait(&uready[j], lp);
+                mbar_wait(&uready[j], (upar >> j) & 1u);
+                upar ^= 1u << j;
                 if (p == 0) {
                     STEP_MARK(13);
                     if (a.trace && l == a.trace_layer && lane == 0 && (warp == 0 || warp == kNW - 1))
