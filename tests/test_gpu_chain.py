@@ -188,3 +188,56 @@ def test_two_group_chain_in_subprocess():
                        env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_chain_and_layer_steps_interleave_on_the_same_caches():
+    """chain launches and single-layer launches alternate on the same caches
+    (each keeps its own control block: barrier counts, layer-step tags of the
+    projection partials and of the chained tokens): the results equal a twin
+    stepped layer by layer throughout, bit for bit"""
+    import os
+    if os.environ.get("WSVD_CHAIN_PIPE") == "1":
+        pytest.skip("the two-group chain splits rows differently (1e-5, test_chain_equals_layer_steps)")
+    from paper_2604_02570_b200.layer import DecodeChain
+    E, nh, B, lens = 1024, 32, 16, [200, 201, 202]
+    n = len(lens)
+    dev = torch.device("cuda", 0)
+    rng, lays, wos, make = _build(n, E, nh, B, [L + 12 for L in lens], 9300)
+    a, b = make(), make()
+    _prefill(a, lens, O.Rng(78), B, E, dev)
+    _prefill(b, lens, O.Rng(78), B, E, dev)
+    chain = DecodeChain(a)
+    for step in range(6):
+        x = torch.from_numpy(O.bf16_round(rng.normal_matrix(B, E)).astype(np.float32)).to(dev)
+        ya = [torch.empty((B, E), device=dev) for _ in range(n)]
+        yb = [torch.empty((B, E), device=dev) for _ in range(n)]
+        if step % 3 == 1:  # this pass one launch per layer on the chain's caches
+            for i in range(n):
+                a[i].step(x if i == 0 else ya[i - 1], ya[i], graph=False)
+        else:
+            chain.step(x, ya)
+        for i in range(n):
+            b[i].step(x if i == 0 else yb[i - 1], yb[i], graph=False)
+        torch.cuda.synchronize()
+        for i in range(n):
+            assert torch.equal(ya[i], yb[i]), f"step {step} layer {i}"
+
+
+@pytest.mark.parametrize("env", ["WSVD_STEP_NOCLUSTER=1", "WSVD_STEP_NOXTAG=1", "WSVD_STEP_G1=1",
+                                 "WSVD_STEP_G3=1", "WSVD_STEP_SHORTSEG=0"])
+def test_chain_switches_in_subprocess(env):
+    """the A/B switches of the fused step (read once per process): without CTA
+    pairs (y through red.add, grid barrier 1 kept), untagged chained tokens
+    (y flags), the grid barriers restored, short first segments in place --
+    the chain still equals the single-layer steps bit for bit"""
+    import os
+    import subprocess
+    import sys
+    k, v = env.split("=")
+    if os.environ.get(k) == v or os.environ.get("WSVD_CHAIN_PIPE") == "1":
+        pytest.skip("already a switched run")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", __file__, "-k",
+                        "test_chain_equals_layer_steps or interleave"],
+                       env=dict(os.environ, **{k: v}), capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
