@@ -713,7 +713,10 @@ int run_chain_fused(wsvd_cache_s* const* cs, int n, const float* x, float* const
     a.x_first = x_first ? 1 : 0;
     static const int l2n = getenv("WSVD_STEP_L2NEXT") ? atoi(getenv("WSVD_STEP_L2NEXT")) : 1;  // A/B switch
     a.l2_next = l2n;
-    static const int cpre = getenv("WSVD_CHAIN_PRE") ? atoi(getenv("WSVD_CHAIN_PRE")) : 0;  // A/B switch
+    // the next layer's first stages per CTA into L2 once this CTA's O-projection
+    // is done (every attention stream has ended: HBM is idle until the next
+    // layer's starts): 4 measured best (54.1 -> 53.4 us per layer; 8+ no gain)
+    static const int cpre = getenv("WSVD_CHAIN_PRE") ? atoi(getenv("WSVD_CHAIN_PRE")) : 4;  // A/B switch
     a.chain_pre = cpre;
     static const bool trace = getenv("WSVD_STEP_TRACE") != nullptr;  // phase timeline (debug_copy 4)
     static const int trace_layer = getenv("WSVD_STEP_TRACE_LAYER") ? atoi(getenv("WSVD_STEP_TRACE_LAYER")) : -1;

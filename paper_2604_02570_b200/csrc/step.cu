@@ -563,10 +563,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             const uint64_t pol = policy_evict_first();
             uint32_t par = 0;  // per attention-ring slot: parity of its fills so far
             // The first a.chain_pre stages of this CTA's range of layer li into
-            // L2, issued in the previous layer's tail once its projection items
-            // are out: HBM is otherwise idle until layer li's attention starts
-            // (O-projection, barriers, projection, query preparation), and those
-            // stages then stream from L2
+            // L2, issued once this CTA's previous O-projection is done (every
+            // attention stream of that layer has ended -- issued earlier, the
+            // prefetch slows the stragglers): HBM is otherwise idle until layer
+            // li's attention starts, and those stages then stream from L2
             auto prefetch_cache = [&](int li) {
                 if (a.chain_pre <= 0) return;
                 const StepLayer& Ly = a.layer[li];
@@ -597,16 +597,16 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     for (int st = 0; st < nWS; ++st) {
                         mbar_wait(&emptyB[st], ((par >> st) & 1u) ^ 1u);
                         if (!p3w && (st + 1) * C::STAGE > gp.p3lo) {
-                            prefetch_cache(li);
                             mbar_wait(p3done, lp ^ 1u);
+                            prefetch_cache(li);  // (HBM is idle: every CTA is past its attention)
                             p3w = true;
                         }
                         issue_parked(li, 2 * st, 2 * st + 2);
                     }
                     // every other stage of the ring may hold P3 data until P3 is done
                     if (!p3w) {
-                        prefetch_cache(li);
                         mbar_wait(p3done, lp ^ 1u);
+                        prefetch_cache(li);
                     }
                 }
                 while (*tbuilt < li + 1) {
