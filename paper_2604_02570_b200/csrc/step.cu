@@ -120,7 +120,7 @@ WSVD_DEV uint64_t gtimer() {
 }
 // phase marks of layer a.trace_layer (variable l in scope)
 #define STEP_MARK(k) \
-    do { if (a.trace && l == a.trace_layer && (tid & 31) == 0) a.trace[cta * kTr + (k)] = gtimer(); } while (0)
+    do { if (trc && l == a.trace_layer && (tid & 31) == 0) trc[cta * kTr + (k)] = gtimer(); } while (0)
 
 WSVD_DEV unsigned ld_acquire(const unsigned* p) {
     unsigned v;
@@ -327,8 +327,10 @@ WSVD_DEV void item_mma(uint32_t slot_addr, uint32_t xs_addr, int lane, float (&f
     }
 }
 
-template <int R, int MT>
+template <int R, int MT, bool TR>
 __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_constant__ StepArgs a) {
+    // the phase marks (WSVD_STEP_TRACE) only in the TR instantiation
+    uint64_t* const trc = TR ? a.trace : nullptr;
     static_assert(R == 32, "the fused step is specialised for rank 32 (one latent dim per lane)");
     using C = SC<R, MT>;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -369,10 +371,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     int l = 0;  // the layer (trace marks)
 
     STEP_MARK(0);
-    if (a.trace && tid == 0) {
+    if (trc && tid == 0) {
         unsigned smid;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        a.trace[cta * kTr + 10] = smid;
+        trc[cta * kTr + 10] = smid;
     }
     // ---- projection geometry (the same for every layer): K split ps, a
     // contiguous run [plo, phi) of the split's 16-row W-tiles (rows n =
@@ -551,7 +553,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 for (int i = (li == 0 ? ia_pre : 0); i < na; ++i) {
                     const int slot = static_cast<int>(ia_g % kNA);
                     mbar_wait(&emptyA[slot], ((ia_g / kNA) & 1u) ^ 1u);
-                    if (a.trace && li == a.trace_layer && i == 0) a.trace[cta * kTr + 23] = gtimer();
+                    if (trc && li == a.trace_layer && i == 0) trc[cta * kTr + 23] = gtimer();
                     mbar_arrive_expect_tx(&fullA[slot], kItem);
                     tma_bulk_g2s(ringA + slot * kItem, a_src(li, i), kItem, &fullA[slot]);
                     ++ia_g;
@@ -682,7 +684,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             // second one's query: process the (whole-region) second one first
             const int f = rev ? nseg - 1 : 0;
             meta[2] = (nseg >= 3 && sinf[f].t1 - sinf[f].t0 < a.short_seg) ? 1 : 0;
-            if (a.trace && li == a.trace_layer) a.trace[cta * kTr + 11] = static_cast<uint64_t>(nseg);
+            if (trc && li == a.trace_layer) trc[cta * kTr + 11] = static_cast<uint64_t>(nseg);
         }
         __syncwarp();
         if (lane == 0) {
@@ -930,7 +932,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     // once the first segment's partials are complete: its burst then
                     // does not queue ahead of the projection loads of CTAs still in P1
                     if (a.g1 == 0 && nWS > 0 && lane == 0) mbar_arrive(b1bar);  // (waited only with parked stages)
-                    if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 24] = gtimer();
+                    if (trc && l == a.trace_layer && lane == 0) trc[cta * kTr + 24] = gtimer();
                 }
                 float qt = 0.f;
 #pragma unroll
@@ -951,7 +953,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             };
             if (nseg > 0) prep(0);
             else if (a.g1 == 0 && nWS > 0 && lane == 0) mbar_arrive(b1bar);
-            if (a.trace && l == a.trace_layer && lane == 0) a.trace[cta * kTr + 16] = gtimer();
+            if (trc && l == a.trace_layer && lane == 0) trc[cta * kTr + 16] = gtimer();
             for (int p = 1; p < nseg; ++p) prep(p);
             if (nseg > 0) STEP_MARK(4);
             // the next layer's table into the other buffer, while this layer's
@@ -1096,8 +1098,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 upar ^= 1u << j;
                 if (p == 0) {
                     STEP_MARK(13);
-                    if (a.trace && l == a.trace_layer && lane == 0 && (warp == 0 || warp == kNW - 1))
-                        a.trace[cta * kTr + (warp == 0 ? 17 : 18)] = gtimer();
+                    if (trc && l == a.trace_layer && lane == 0 && (warp == 0 || warp == kNW - 1))
+                        trc[cta * kTr + (warp == 0 ? 17 : 18)] = gtimer();
                 }
                 uint32_t qf[KR][2];
 #pragma unroll
@@ -1120,8 +1122,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 for (int st = 0; st < ns; ++st) {
                     mbar_wait(&fullB[slot], (parc >> slot) & 1u);
                     parc ^= 1u << slot;
-                    if (a.trace && l == a.trace_layer && p == 0 && st == 0 && warp == 0 && lane == 0)
-                        a.trace[cta * kTr + 19] = gtimer();
+                    if (trc && l == a.trace_layer && p == 0 && st == 0 && warp == 0 && lane == 0)
+                        trc[cta * kTr + 19] = gtimer();
                     const uint32_t sbase = smem_u32(ringB + slot * C::STAGE);
                     const int rows = min(kST, ntok - st * kST);
                     if (warp * 32 < rows) {
@@ -1205,7 +1207,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         // G2: every (sequence, head) row is merged; every CTA has read the length
         // (trace: thread 0's arrival -> mark 25, its exit -> mark 7; a mark
         // taken after the barrier by every warp reads the timer early)
-        grid_sync(a.bar, (++gen) * static_cast<unsigned>(G), (a.trace && l == a.trace_layer) ? a.trace + cta * kTr : nullptr);
+        grid_sync(a.bar, (++gen) * static_cast<unsigned>(G), (trc && l == a.trace_layer) ? trc + cta * kTr : nullptr);
         if (cta == 0 && tid == 0) *Ly.d_len = pos + 1;
 
         if (warp != kHelp) {
@@ -1263,12 +1265,12 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         const int slot = static_cast<int>(ia % kNA), s = j % g.p3ns;
                         if (slot != hslot || s < s0 || s >= s0 + g.per) continue;
                         mbar_wait(&fullA[slot], (ia / kNA) & 1u);
-                        if (a.trace && l == a.trace_layer && tid == 0 && j == 0) a.trace[cta * kTr + 12] = gtimer();
+                        if (trc && l == a.trace_layer && tid == 0 && j == 0) trc[cta * kTr + 12] = gtimer();
                         // token columns 0..MT*16-1 are the hi rows, MT*16.. the lo rows
                         float facc[2 * MT][2][4];
                         item_mma<2 * MT>(smem_u32(ringA + slot * kItem), smem_u32(xsl + (s - s0) * C::XB2), lane, facc,
                                          half * kKS / 64, (half + 1) * kKS / 64);
-                        if (a.trace && l == a.trace_layer && tid == 0 && j == 0) a.trace[cta * kTr + 14] = gtimer();
+                        if (trc && l == a.trace_layer && tid == 0 && j == 0) trc[cta * kTr + 14] = gtimer();
                         float* pj3 = part + (half * kNA + j) * 16 * MT * 16;
 #pragma unroll
                         for (int mt = 0; mt < MT; ++mt)
@@ -1281,12 +1283,12 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                                     pj3[n * MT * 16 + m] = facc[mt][hh][i] + facc[mt + MT][hh][i];
                                 }
                     }
-                    if (a.trace && l == a.trace_layer && (tid & 31) == 0) a.trace[cta * kTr + 29 + (warp < 4 ? 0 : 1)] = gtimer();
+                    if (trc && l == a.trace_layer && (tid & 31) == 0) trc[cta * kTr + 29 + (warp < 4 ? 0 : 1)] = gtimer();
                     named_bar_sync(2, 32 * kNW);  // the X buffer is free again / every partial is written
                 }
                 // the weight ring's P3 slots are free (both halves have run)
                 if (tid < g.np3) mbar_arrive(&emptyA[(a3 + static_cast<unsigned>(tid)) % kNA]);
-                if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 31] = gtimer();
+                if (trc && l == a.trace_layer && tid == 0) trc[cta * kTr + 31] = gtimer();
                 // part[(half * kNA + j)] -> sum over halves, then splits
                 auto psum = [&](int ti, int n, int m) {
                     float v = 0.f;
@@ -1314,7 +1316,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                             st_async_v4(dst + 4u * static_cast<uint32_t>((ti * a.B + m) * 16 + n0), psum1(ti, n0, m),
                                         psum1(ti, n0 + 1, m), psum1(ti, n0 + 2, m), psum1(ti, n0 + 3, m), rbar);
                         }
-                        if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 26] = gtimer();
+                        if (trc && l == a.trace_layer && tid == 0) trc[cta * kTr + 26] = gtimer();
                     } else {
                         // this CTA's split-0 sums: <= 4 groups per thread (B <= 32, nt3 <= 4),
                         // in registers (unrolled: a dynamic index would put them in local memory)
@@ -1328,10 +1330,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
 #pragma unroll
                             for (int e = 0; e < 4; ++e) own[u][e] = psum1(ti, n0 + e, m);
                         }
-                        if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 27] = gtimer();
+                        if (trc && l == a.trace_layer && tid == 0) trc[cta * kTr + 27] = gtimer();
                         if (tid == 0) mbar_arrive_expect_tx(ybar, static_cast<uint32_t>(q4) * 16u);
                         mbar_wait_cluster(ybar, ycnt & 1u);
-                        if (a.trace && l == a.trace_layer && tid == 0) a.trace[cta * kTr + 26] = gtimer();
+                        if (trc && l == a.trace_layer && tid == 0) trc[cta * kTr + 26] = gtimer();
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int i = tid + u * 32 * kNW;
@@ -1396,7 +1398,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             named_bar_sync(2, 32 * kNW);
             if (tid == 0) {
                 mbar_arrive(p3done);
-                if (a.trace && l == a.trace_layer) a.trace[cta * kTr + 28] = gtimer();
+                if (trc && l == a.trace_layer) trc[cta * kTr + 28] = gtimer();
                 // this CTA's share of y is written (release; with tagged tokens the
                 // helper releases it, off the next projection's path)
                 if (!a.xtagged) red_release(a.yflag + 32 * cta);
@@ -1421,12 +1423,12 @@ cudaError_t launch_mt(const StepArgs& a, cudaStream_t s) {
     if constexpr (!C::OK) {
         return cudaErrorInvalidValue;
     } else {
-        auto k = layer_step_kernel<32, MT>;
-        static bool attr = false;
-        if (!attr) {
+        auto k = a.trace ? layer_step_kernel<32, MT, true> : layer_step_kernel<32, MT, false>;
+        static bool attr[2] = {false, false};
+        if (!attr[a.trace ? 1 : 0]) {
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
             if (e != cudaSuccess) return e;
-            attr = true;
+            attr[a.trace ? 1 : 0] = true;
         }
         // the counts and the barrier need every CTA resident: one CTA per SM
         // fits (the host checks occupancy once and serialises fused steps of
@@ -1477,15 +1479,15 @@ int step_resident_ctas_per_sm(int B) {
             n = 0;
         }
     };
-    if ((B + 15) / 16 == 1) probe(layer_step_kernel<32, 1>, SC<32, 1>::SMEM);
-    else probe(layer_step_kernel<32, 2>, SC<32, 2>::SMEM);
+    if ((B + 15) / 16 == 1) probe(layer_step_kernel<32, 1, false>, SC<32, 1>::SMEM);
+    else probe(layer_step_kernel<32, 2, false>, SC<32, 2>::SMEM);
     return n;
 }
 
 template <int MT>
 int pair_ok(int grid) {
     using C = SC<32, MT>;
-    auto k = layer_step_kernel<32, MT>;
+    auto k = layer_step_kernel<32, MT, false>;
     if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) != cudaSuccess) {
         cudaGetLastError();
         return 0;
