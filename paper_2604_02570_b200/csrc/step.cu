@@ -327,10 +327,19 @@ WSVD_DEV void item_mma(uint32_t slot_addr, uint32_t xs_addr, int lane, float (&f
     }
 }
 
-template <int R, int MT, bool TR>
+template <int R, int MT, bool GEN>
 __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_constant__ StepArgs a) {
-    // the phase marks (WSVD_STEP_TRACE) only in the TR instantiation
-    uint64_t* const trc = TR ? a.trace : nullptr;
+    // The production instantiation (GEN = false) has no phase marks and the
+    // A/B switches at their defaults (capi.cu); GEN = true reads them (and the
+    // WSVD_STEP_TRACE marks) from the arguments.
+    uint64_t* const trc = GEN ? a.trace : nullptr;
+    const int ab_p3_tma = GEN ? a.p3_tma : 0;
+    const int ab_g3 = GEN ? a.g3 : 0;
+    const int ab_x_first = GEN ? a.x_first : 1;
+    const int ab_l2_next = GEN ? a.l2_next : 1;
+    const int ab_chain_pre = GEN ? a.chain_pre : 4;
+    const int ab_pre_stages = GEN ? a.pre_stages : 0;
+    const int ab_short_seg = GEN ? a.short_seg : 2048;
     static_assert(R == 32, "the fused step is specialised for rank 32 (one latent dim per lane)");
     using C = SC<R, MT>;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -502,10 +511,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             mbar_arrive_expect_tx(&fullA[ia_pre], kItem);
             tma_bulk_g2s(ringA + ia_pre * kItem, a_src(0, ia_pre), kItem, &fullA[ia_pre]);
         }
-        if (!a.x_first) issue_parked(0, 0, nBH);
+        if (!ab_x_first) issue_parked(0, 0, nBH);
     }
     const int nbh = a.B * a.nh;
-    if (warp == kNW + 1 && lane == 0 && a.pos_hint > 0 && a.pre_stages > 0) {
+    if (warp == kNW + 1 && lane == 0 && a.pos_hint > 0 && ab_pre_stages > 0) {
         // Before the predecessor has drained: request the first stages of this
         // CTA's layer-0 cache range into L2 (a prefetch is only a hint -- L2 is
         // the point of coherence), at the length the host expects
@@ -513,7 +522,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         long long cc[2] = {cut_row(cta, G, Th, a.pos_hint), cut_row(cta + 1, G, Th, a.pos_hint)};
         const long long* ct = cc - cta;  // a two-entry table seen from this CTA
         const int ns = seg_count(ct, cta, G, a.pos_hint, nbh);
-        int left = a.pre_stages;
+        int left = ab_pre_stages;
         for (int p = 0; p < ns && left > 0; ++p) {
             const Seg sg = seg_at(ct, cta, G, a.pos_hint, (cta & 1) ? ns - 1 - p : p);
             for (int t = sg.t0; t < sg.t1 && left > 0; t += kST, --left) {
@@ -543,7 +552,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     if (warp == kNW || warp == kNW + 1) {
         if (warp == kNW && lane == 0) {
             // the weight ring: every layer's P1 ring items, then its P3 items
-            if (a.x_first && nBH > 0) {
+            if (ab_x_first && nBH > 0) {
                 mbar_wait(xin, 0u);
                 issue_parked(0, 0, nBH);
             }
@@ -570,7 +579,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             // prefetch slows the stragglers): HBM is otherwise idle until layer
             // li's attention starts, and those stages then stream from L2
             auto prefetch_cache = [&](int li) {
-                if (a.chain_pre <= 0) return;
+                if (ab_chain_pre <= 0) return;
                 const StepLayer& Ly = a.layer[li];
                 const int pos = *static_cast<volatile const int*>(Ly.d_len);
                 if (pos <= 0) return;
@@ -578,7 +587,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 long long cc[2] = {cut_row(cta, G, T, pos), cut_row(cta + 1, G, T, pos)};
                 const long long* ct = cc - cta;  // a two-entry table seen from this CTA
                 const int ns = seg_count(ct, cta, G, pos, nbh);
-                int left = a.chain_pre;
+                int left = ab_chain_pre;
                 for (int p = 0; p < ns && left > 0; ++p) {
                     const Seg sg = seg_at(ct, cta, G, pos, rev ? ns - 1 - p : p);
                     for (int t = sg.t0; t < sg.t1 && left > 0; t += kST, --left) {
@@ -642,7 +651,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         ++ib;
                     }
                 }
-                if (a.l2_next && li + 1 < nL) {
+                if (ab_l2_next && li + 1 < nL) {
                     // the next layer's items that are loaded last (after this
                     // layer's P3): into L2 now, while this CTA's last stages stream
                     const P3G g = p3geom(li);
@@ -683,7 +692,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             // a short first segment would leave the consumers waiting for the
             // second one's query: process the (whole-region) second one first
             const int f = rev ? nseg - 1 : 0;
-            meta[2] = (nseg >= 3 && sinf[f].t1 - sinf[f].t0 < a.short_seg) ? 1 : 0;
+            meta[2] = (nseg >= 3 && sinf[f].t1 - sinf[f].t0 < ab_short_seg) ? 1 : 0;
             if (trc && li == a.trace_layer) trc[cta * kTr + 11] = static_cast<uint64_t>(nseg);
         }
         __syncwarp();
@@ -783,7 +792,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                         make_uint4(static_cast<unsigned>(w[u][0]), static_cast<unsigned>(w[u][1]),
                                    static_cast<unsigned>(w[u][2]), static_cast<unsigned>(w[u][3]));
                 }
-            } else if (l > 0 && !a.g3 && np1 > 0) {
+            } else if (l > 0 && !ab_g3 && np1 > 0) {
                 // the token is the previous layer's y: wait for the CTAs whose
                 // O-projection tiles cover this K split's columns (tile T0 + lane;
                 // a tile's producers are its pair's two CTAs, or one CTA)
@@ -959,7 +968,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             // the next layer's table into the other buffer, while this layer's
             // attention streams (its readers use this layer's buffer)
             if (l + 1 < nL) build_table(l + 1);
-            if (l > 0 && !a.g3 && a.cluster == 2 && (cta & 1)) {
+            if (l > 0 && !ab_g3 && a.cluster == 2 && (cta & 1)) {
                 // this CTA writes into its even partner's shared memory below
                 // (the merge area): the partner is past layer l - 1's O-projection
                 // (no grid barrier orders the two; in practice long since)
@@ -1226,7 +1235,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             const unsigned a3 = abase + static_cast<unsigned>(nA1);  // ring-A index of P3 item 0
             if (g.np3 > 0) {
                 for (int s0 = 0; s0 < g.p3ns; s0 += g.per) {
-                    if (a.p3_tma) {
+                    if (ab_p3_tma) {
                         if (tid == 0) {
                             // xo was written by other CTAs' generic stores (ordered by the
                             // barrier); order them before this thread's async-proxy reads
@@ -1408,7 +1417,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
             if (lane == 0) red_release(a.yflag + 32 * cta);
         }
         abase += static_cast<unsigned>(nA1 + g3.np3);
-        if (l + 1 < nL && a.g3) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 3)
+        if (l + 1 < nL && ab_g3) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 3)
     }
     if (cta == 0 && tid == 0) {
         *a.epoch += 1;  // fused launches run (the x-fetch generations)
@@ -1423,12 +1432,15 @@ cudaError_t launch_mt(const StepArgs& a, cudaStream_t s) {
     if constexpr (!C::OK) {
         return cudaErrorInvalidValue;
     } else {
-        auto k = a.trace ? layer_step_kernel<32, MT, true> : layer_step_kernel<32, MT, false>;
+        // the generic instantiation only for traces and non-default A/B switches
+        const bool gen = a.trace || a.p3_tma != 0 || a.g3 != 0 || a.x_first != 1 || a.l2_next != 1 ||
+                         a.chain_pre != 4 || a.pre_stages != 0 || a.short_seg != 2048;
+        auto k = gen ? layer_step_kernel<32, MT, true> : layer_step_kernel<32, MT, false>;
         static bool attr[2] = {false, false};
-        if (!attr[a.trace ? 1 : 0]) {
+        if (!attr[gen ? 1 : 0]) {
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
             if (e != cudaSuccess) return e;
-            attr[a.trace ? 1 : 0] = true;
+            attr[gen ? 1 : 0] = true;
         }
         // the counts and the barrier need every CTA resident: one CTA per SM
         // fits (the host checks occupancy once and serialises fused steps of
