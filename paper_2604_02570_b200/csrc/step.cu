@@ -340,6 +340,10 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     const int ab_chain_pre = GEN ? a.chain_pre : 4;
     const int ab_pre_stages = GEN ? a.pre_stages : 0;
     const int ab_short_seg = GEN ? a.short_seg : 2048;
+    // production geometry: CTA pairs and two O-projection K splits (the host
+    // launches the generic instantiation otherwise)
+    const int kcl = GEN ? a.cluster : 2;
+    const int ab_g1 = GEN ? a.g1 : 0;
     static_assert(R == 32, "the fused step is specialised for rank 32 (one latent dim per lane)");
     using C = SC<R, MT>;
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -395,7 +399,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
     const int plo = pj < cps ? static_cast<int>(static_cast<long>(pj) * ptiles / cps) : 0;
     const int phi = pj < cps ? static_cast<int>(static_cast<long>(pj + 1) * ptiles / cps) : 0;
     const int np1 = phi - plo;
-    const int osplits = a.oKp / kKS;
+    const int osplits = GEN ? a.oKp / kKS : 2;
     // P3 items (tile, K split) of layer l.  Device y with two K splits: CTA c
     // takes split c % 2 of a run of tiles, so it stages only that split's X
     // rows; the two partial sums meet in y through fp32 red.add onto zeros --
@@ -417,7 +421,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         // CTA pairs: the odd CTA's split-1 sums cross into the even CTA through
         // distributed shared memory, which writes y = split 0 + split 1 with
         // plain stores (no zeroing pass, no atomics; the same fixed order)
-        g.pairy = g.ysplit && a.cluster == 2;
+        g.pairy = g.ysplit && kcl == 2;
         const int cps3 = G / 2;
         if (g.ysplit) {
             const int pj3 = cta / 2;
@@ -480,7 +484,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         fence_mbar_init();  // every lane: the fence covers the executing thread's inits
     }
     __syncthreads();
-    if (a.cluster > 1) cluster_sync_all();  // the partner's barriers are initialised before any remote arrive
+    if (kcl > 1) cluster_sync_all();  // the partner's barriers are initialised before any remote arrive
     // ring-A item ia (in-layer sequence) of layer li -> source
     auto a_src = [&](int li, int ia) -> const uint8_t* {
         const StepLayer& Ly = a.layer[li];
@@ -868,8 +872,8 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
         // (the projection partials carry their layer step's tag: readers
         // validate each word -- no grid barrier between the projection and
         // the attention)
-        if (a.g1 == 1) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 1)
-        if (tid == 0 && a.g1 != 0 && nWS > 0) mbar_arrive(b1bar);
+        if (ab_g1 == 1) grid_sync(a.bar, (++gen) * static_cast<unsigned>(G));  // (A/B: the old grid barrier 1)
+        if (tid == 0 && ab_g1 != 0 && nWS > 0) mbar_arrive(b1bar);
         STEP_MARK(3);
         if (warp < kNW || warp == kHelp) {
             while (*tbuilt < l + 1) {  // (built before P1 ended: passes at once)
@@ -940,7 +944,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     // the cache stream into the stages that held parked items starts
                     // once the first segment's partials are complete: its burst then
                     // does not queue ahead of the projection loads of CTAs still in P1
-                    if (a.g1 == 0 && nWS > 0 && lane == 0) mbar_arrive(b1bar);  // (waited only with parked stages)
+                    if (ab_g1 == 0 && nWS > 0 && lane == 0) mbar_arrive(b1bar);  // (waited only with parked stages)
                     if (trc && l == a.trace_layer && lane == 0) trc[cta * kTr + 24] = gtimer();
                 }
                 float qt = 0.f;
@@ -961,14 +965,14 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                 if (lane == 0) mbar_arrive(&uready[j]);
             };
             if (nseg > 0) prep(0);
-            else if (a.g1 == 0 && nWS > 0 && lane == 0) mbar_arrive(b1bar);
+            else if (ab_g1 == 0 && nWS > 0 && lane == 0) mbar_arrive(b1bar);
             if (trc && l == a.trace_layer && lane == 0) trc[cta * kTr + 16] = gtimer();
             for (int p = 1; p < nseg; ++p) prep(p);
             if (nseg > 0) STEP_MARK(4);
             // the next layer's table into the other buffer, while this layer's
             // attention streams (its readers use this layer's buffer)
             if (l + 1 < nL) build_table(l + 1);
-            if (l > 0 && !ab_g3 && a.cluster == 2 && (cta & 1)) {
+            if (l > 0 && !ab_g3 && kcl == 2 && (cta & 1)) {
                 // this CTA writes into its even partner's shared memory below
                 // (the merge area): the partner is past layer l - 1's O-projection
                 // (no grid barrier orders the two; in practice long since)
@@ -1016,7 +1020,7 @@ __global__ void __launch_bounds__(kThr, 1) layer_step_kernel(const __grid_consta
                     M = Mn;
                 }
                 const int c0 = s.c0, c1 = s.c1, owners = s.owners;
-                const bool pair = a.cluster == 2 && owners == 2 && c1 - c0 == 2 && (c0 & 1) == 0;
+                const bool pair = kcl == 2 && owners == 2 && c1 - c0 == 2 && (c0 & 1) == 0;
                 float L2 = Ls, a2 = av;
                 if (pair && cta == c0 + 1) {
                     // the later part of the pair's shared region -> the even CTA
@@ -1434,7 +1438,8 @@ cudaError_t launch_mt(const StepArgs& a, cudaStream_t s) {
     } else {
         // the generic instantiation only for traces and non-default A/B switches
         const bool gen = a.trace || a.p3_tma != 0 || a.g3 != 0 || a.x_first != 1 || a.l2_next != 1 ||
-                         a.chain_pre != 4 || a.pre_stages != 0 || a.short_seg != 2048;
+                         a.chain_pre != 4 || a.pre_stages != 0 || a.short_seg != 2048 || a.cluster != 2 ||
+                         a.oKp / kKS != 2 || a.g1 != 0;
         auto k = gen ? layer_step_kernel<32, MT, true> : layer_step_kernel<32, MT, false>;
         static bool attr[2] = {false, false};
         if (!attr[gen ? 1 : 0]) {
