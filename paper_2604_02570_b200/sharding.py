@@ -40,21 +40,27 @@ def shard_oproj(w_o: np.ndarray, n_heads: int, head_dim: int, world: int, rank: 
     return w_o[h0 * head_dim:h1 * head_dim]
 
 
+def exchange_unique_id(rank: int, device: int = 0, group=None) -> np.ndarray:
+    """Rank 0's NCCL unique id (from the native library) on every rank of an
+    existing torch.distributed group (nccl: through device memory; gloo: host)."""
+    import torch
+    import torch.distributed as dist
+    uid = np.zeros(128, dtype=np.uint8)
+    if rank == 0:
+        N.call("wsvd_nccl_unique_id", uid.ctypes.data_as(C.POINTER(C.c_uint8)))
+    t = torch.from_numpy(uid.astype(np.int64))
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda(device)
+    dist.broadcast(t, src=0, group=group)
+    return t.cpu().numpy().astype(np.uint8)
+
+
 class NcclComm:
     """NCCL communicator owned by the native library (dlopen'd libnccl); the
     unique id travels over an existing torch.distributed group."""
 
     def __init__(self, world: int, rank: int, device: int, group=None):
-        import torch
-        import torch.distributed as dist
-        uid = np.zeros(128, dtype=np.uint8)
-        if rank == 0:
-            N.call("wsvd_nccl_unique_id", uid.ctypes.data_as(C.POINTER(C.c_uint8)))
-        t = torch.from_numpy(uid.astype(np.int64))
-        if dist.get_backend(group) == "nccl":
-            t = t.cuda(device)
-        dist.broadcast(t, src=0, group=group)
-        uid = t.cpu().numpy().astype(np.uint8)
+        uid = exchange_unique_id(rank, device, group)
         h = C.c_void_p()
         N.call("wsvd_comm_create", uid.ctypes.data_as(C.POINTER(C.c_uint8)), world, rank, device,
                C.byref(h))

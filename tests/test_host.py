@@ -126,3 +126,29 @@ def test_mirror_validates_before_touching_the_device():
         D.DeviceLayer(D.LayerFactors())
     with pytest.raises(ConfigError):
         D.DeviceLayer(to_factors(O.random_layer(O.Rng(1), 16, 4, [[2, 2, 2]])), weight_dtype="fp8")
+
+
+def _uid_worker(rank, world, port, out_dir):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    uid = S.exchange_unique_id(rank)
+    np.save(os.path.join(out_dir, f"uid{rank}.npy"), uid)
+    dist.destroy_process_group()
+
+
+def test_nccl_unique_id_exchange_gloo(tmp_path):
+    """NcclComm's bootstrap on CPU: rank 0's NCCL unique id (the native
+    library's wsvd_nccl_unique_id) reaches every rank of a world-size-2 gloo
+    group unchanged; the communicator itself (wsvd_comm_create) needs GPUs
+    (tests/test_gpu_nccl.py)"""
+    import socket
+
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mp.spawn(_uid_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    u0, u1 = np.load(tmp_path / "uid0.npy"), np.load(tmp_path / "uid1.npy")
+    assert u0.shape == (128,) and u0.any() and np.array_equal(u0, u1)
