@@ -840,8 +840,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-strong", action="store_true",
                     help="skip the config-4 strong-scaling point (fixed B = 64, heads over the N GPUs)")
-    ap.add_argument("--layers", type=int, default=8,
-                    help="rotating layers (own weights and cache each): step i runs layer i mod n")
+    ap.add_argument("--layers", type=int, default=32,
+                    help="rotating layers (own weights and cache each; 32 = LLaVA-7B's depth, one chain launch "
+                         "per token through all of them): step i runs layer i mod n")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-predelay", action="store_true",
                     help="start the timed region on an idle device (the first launch's host latency inside it)")

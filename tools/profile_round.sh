@@ -14,7 +14,7 @@ timeout 300 python tools/chain_timing.py > gpurun_out/chain_timing.txt 2>&1
 # warm-up chain launch and the two timed 8-layer chain launches
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:layer_step -s 8 -c 3 --csv --log-file gpurun_out/launches.csv \
-    python bench.py --steps 16 --warmup 8 --no-cpu-baseline --soak-ms 0 --no-baselines --no-strong > /dev/null 2>&1
+    python bench.py --layers 8 --steps 16 --warmup 8 --no-cpu-baseline --soak-ms 0 --no-baselines --no-strong > /dev/null 2>&1
 # one full capture of an 8-layer chain launch (source-level, for the summaries)
 timeout 900 ncu --set full --import-source on --clock-control none -k regex:layer_step -s 9 -c 1 \
     -o gpurun_out/chain_full python tools/chain_timing.py --only 8 --reps 2 > /dev/null 2>&1
